@@ -1,0 +1,114 @@
+/*
+ * ifmm_b200.h -- C ABI of the B200-native IFMM factorize+solve engine.
+ *
+ * Plain pointers and sizes only (no torch types).  Every entry point maps
+ * onto one function of the reference Python package
+ * (/root/reference/pkg/src/ifmm); the mapping is given per function as
+ * `file:line`.  Status codes: 0 ok, 1 ValueError, 2 SingularPivotError,
+ * 3 CUDA error, 4 out of device memory, 5 AssertionError (broken invariant).
+ * `ifmm_last_error()` returns the message of the last failure on the
+ * calling thread.  There is no CPU fallback: without a CUDA device every
+ * compute entry point fails with status 3.
+ */
+#ifndef IFMM_B200_H
+#define IFMM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library / context ------------------------------------------------ */
+int ifmm_abi_version(void);
+const char* ifmm_last_error(void);
+/* Device arena + stream.  arena_bytes == 0 -> 90% of free device memory. */
+void* ifmm_ctx_create(int device, unsigned long long arena_bytes);
+void ifmm_ctx_destroy(void* ctx);
+/* Bytes of the arena in use / high-water mark. */
+int ifmm_ctx_memory(void* ctx, unsigned long long* in_use, unsigned long long* peak);
+
+/* ---- tree + topology:  tree.py:107-239 ---------------------------------
+ * The octree itself (depth rule, Morton keys, stable sort; tree.py:107-196)
+ * is built host-side in the Python mirror; this call receives it and
+ * computes compute_topology (tree.py:205-239) natively.
+ *   points: N x 3 Morton-sorted, perm: points[i] = original[perm[i]];
+ *   per cluster: level, parent (-1 root),
+ *   start, stop, cell (3 ints), center (3), half_width; children CSR.  */
+void* ifmm_tree_create(void* ctx, int n_points, const double* points, const int* perm, int depth,
+                       int n_clusters, const int* level, const int* parent,
+                       const int* start, const int* stop, const long long* cell,
+                       const double* center, const double* half_width,
+                       const int* child_ptr, const int* child_idx);
+void ifmm_tree_destroy(void* tree);
+int ifmm_tree_topology_sizes(void* tree, long long* n_nbr, long long* n_int);
+int ifmm_tree_topology(void* tree, long long* nbr_ptr, int* nbr_idx,
+                       long long* int_ptr, int* int_idx);
+
+/* ---- H2 operators:  h2.py:104-182 (chebyshev_operators) --------------
+ * kernel_kind: 1 exp(-r), 2 inverse multiquadric 1/sqrt(r^2+p0^2),
+ * 3 benchmark kernel (kernels.py:42-56, d = p0), 4 zero.              */
+void* ifmm_h2_build(void* tree, int kernel_kind, double p0, int n_cheb, double epsilon);
+void ifmm_h2_destroy(void* h2);
+int ifmm_h2_ranks(void* h2, int* ranks_out /* n_clusters, -1 if none */);
+/* initialize_weights, rigorous mode (h2.py:185-231). */
+int ifmm_h2_weights(void* h2);
+/* Host copy of one stored block for inspection (tests / views):
+ * which: 0 leaf_u[i], 1 leaf_v[i], 2 transfer_u[i], 3 transfer_vt[i],
+ *        4 coupling[(i,j)], 5 near[(i,j)], 6 sigma_u[i], 7 sigma_v[i].
+ * With out == NULL only the shape is returned.                          */
+int ifmm_h2_block(void* h2, int which, int i, int j, double* out, int* rows, int* cols);
+/* h2_matvec (krylov.py:119-159), x/y in ORIGINAL point order, host or
+ * device pointers (on_device = 1).                                       */
+int ifmm_h2_matvec(void* h2, const double* x, double* y, int on_device);
+
+/* ---- extended graph:  graph.py:219-229 / sigma0 graph.py:232-241 ------ */
+void* ifmm_graph_build(void* h2);
+void ifmm_graph_destroy(void* graph);
+int ifmm_graph_info(void* graph, long long* dim, long long* n_nodes, long long* n_edges);
+/* randomized_svd(start_rank=1, max_rank=1) of the extended matrix with the
+ * caller-supplied Gaussian sketch omega (dim x width, row-major), exactly
+ * the draw of graph.py:235-240 / lowrank.py:100-113.                      */
+int ifmm_graph_sigma0(void* graph, const double* omega, int width, int power_iters,
+                      double* sigma0_out);
+
+/* ---- factorize:  factor.py:176-230 --------------------------------------
+ * Consumes (mutates) the graph like the reference.  flags bit0: exact
+ * (non-wave) pair order.                                                   */
+void* ifmm_factorize(void* graph, double epsilon, double sigma0, int flags);
+void ifmm_factor_destroy(void* factor);
+/* Scalar stats: out[0..] = peak_edges, n_clusters, max_basis_rank,
+ * max_fill_rank, forced_rank_truncations, n_levels, n_events_elim,
+ * n_events_rebase, n_events_merge, n_top, top_dim.                       */
+int ifmm_factor_stats(void* factor, long long* out, int n_out);
+/* Per level (elimination order L..2): level, compressed_pairs, added,
+ * dropped_pairs, sum_ranks, max_rank, n_ranks, forced.  8 per level.      */
+int ifmm_factor_level_stats(void* factor, long long* out, int n_levels);
+/* Ranks list of one level (n_ranks entries). */
+int ifmm_factor_level_ranks(void* factor, int level_index, int* out);
+/* Timings (seconds): lu_and_triangular_solves, matmul_updates,
+ * lowrank_approximations, operator_transfer, total, gemm_flops (count),
+ * all_flops (count).                                                       */
+int ifmm_factor_timings(void* factor, double* out, int n_out);
+/* IFMMFactorization.solve (factor.py:99-157): b, x length N (original
+ * order), host or device pointers.                                         */
+int ifmm_solve(void* factor, const double* b, double* x, int on_device);
+
+/* ---- device micro-kernel entry points (tests and benchmarks) ---------- */
+/* C[M,N] = alpha*op(A)op(B) + beta*C on device pointers (row-major). */
+int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,
+                  const double* B, int ldb, int tb, double* C, int ldc, double alpha,
+                  double beta);
+/* Truncated SVD (absolute threshold) of a row-major m x n device matrix. */
+int ifmm_dev_svd(void* ctx, int m, int n, const double* A, double thr, double* U,
+                 double* S, double* V, int* rank);
+/* LU with partial pivoting + solve of nrhs right-hand sides (device). */
+int ifmm_dev_lu_solve(void* ctx, int n, double* A, int* piv, double* X, int nrhs);
+/* weighted_basis_union (lowrank.py:166-199) on device pointers. */
+int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const double* w,
+                   const double* F, const double* wf, double thr, int min_rank,
+                   double* NB, double* NW, double* OM, double* FM, int* rank);
+int ifmm_dev_sync(void* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFMM_B200_H */

@@ -771,9 +771,18 @@ def _top_lu(g, top, tsz):
     return _lu(M, "top-level system")
 
 
+TRACE = None  # optional list collecting per-pair decisions (triage only)
+
+
+def _tr(*a):
+    if TRACE is not None:
+        TRACE.append(" ".join(str(int(v)) if not isinstance(v, str) else v for v in a))
+
+
 def eliminate_one(g: Graph, c, st: LevelStats, ctx, compress_ws=True):
     """factor.py:259-326."""
     nxid, nzid, nyid = g.nx[c], g.nz[c], g.ny[c]
+    _tr("E", c, g.sizes[nxid], g.sizes[nzid])
     m, k = g.sizes[nxid], g.sizes[nzid]
     D = g.take(nxid, nxid)
     U = g.take(nxid, nzid)
@@ -869,6 +878,7 @@ def unions_for(g: Graph, c, fu, wu, fv, wv, st, ctx):
 def rebase(g: Graph, c, uu: Union, uv: Union, partner, events):
     """factor.py:395-430."""
     nxid, nzid, nyid = g.nx[c], g.nz[c], g.ny[c]
+    _tr("R", c, uu.old_map.shape[1], uu.rank, uv.rank)
     py = g.ny[partner]
     r, t = uu.old_map, uv.old_map
     kn = uu.rank
@@ -903,9 +913,11 @@ def redirect(g: Graph, cj, ck, F_kj, F_jk, st: LevelStats, ctx):
     r2 = f_jk.rank if f_jk is not None else 0
     if r1 == 0 and r2 == 0:
         st.dropped_pairs += 1
+        _tr("D", cj, ck)
         return
     st.compressed_pairs += 1
     st.ranks.append(max(r1, r2))
+    _tr("P", cj, ck, r1, r2, ej, ek)
     yj, yk = g.ny[cj], g.ny[ck]
     old_kj = g.E.get((yk, yj))
     old_jk = g.E.get((yj, yk))

@@ -1,0 +1,462 @@
+// C ABI (include/ifmm_b200.h): exception-to-status translation and handle
+// plumbing.  No computation here beyond argument checks.
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/ifmm_b200.h"
+#include "engine.h"
+
+using namespace ifmm;
+
+namespace ifmm {
+const char* last_error_cstr();
+}
+
+#define ABI_TRY try {
+#define ABI_CATCH                                        \
+  }                                                      \
+  catch (const ifmm::Error& e) {                         \
+    set_last_error(e.what());                            \
+    return e.code;                                       \
+  }                                                      \
+  catch (const std::exception& e) {                      \
+    set_last_error(std::string("internal: ") + e.what()); \
+    return E_ASSERT;                                     \
+  }
+#define ABI_CATCH_NULL                                   \
+  }                                                      \
+  catch (const ifmm::Error& e) {                         \
+    set_last_error(e.what());                            \
+    return nullptr;                                      \
+  }                                                      \
+  catch (const std::exception& e) {                      \
+    set_last_error(std::string("internal: ") + e.what()); \
+    return nullptr;                                      \
+  }
+
+extern "C" {
+
+int ifmm_abi_version(void) { return 1; }
+const char* ifmm_last_error(void) { return last_error_cstr(); }
+
+void* ifmm_ctx_create(int device, unsigned long long arena_bytes) {
+  ABI_TRY
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(E_CUDA, "no CUDA device available (the IFMM engine has no CPU fallback)");
+  CUDA_CHECK(cudaSetDevice(device));
+  Ctx* c = new Ctx;
+  c->device = device;
+  CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  if (arena_bytes == 0) {
+    size_t fr = 0, tot = 0;
+    CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+    arena_bytes = (unsigned long long)(fr * 0.85);
+  }
+  c->arena.init(arena_bytes);
+  c->stage.init((size_t)256 << 20);
+  CUDA_CHECK(cudaMalloc(&c->d_status, 16));
+  CUDA_CHECK(cudaMemset(c->d_status, 0, 16));
+  return c;
+  ABI_CATCH_NULL
+}
+
+void ifmm_ctx_destroy(void* p) {
+  if (!p) return;
+  Ctx* c = (Ctx*)p;
+  cudaStreamSynchronize(c->st);
+  c->arena.release();
+  c->stage.release();
+  if (c->d_status) cudaFree(c->d_status);
+  if (c->h_pinned_i) cudaFreeHost(c->h_pinned_i);
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+int ifmm_ctx_memory(void* p, unsigned long long* in_use, unsigned long long* peak) {
+  Ctx* c = (Ctx*)p;
+  *in_use = c->arena.in_use();
+  *peak = c->arena.peak();
+  return 0;
+}
+
+// ---- tree -------------------------------------------------------------------
+void* ifmm_tree_create(void* ctx, int n_points, const double* points, const int* perm, int depth,
+                       int n_clusters, const int* level, const int* parent, const int* start,
+                       const int* stop, const long long* cell, const double* center,
+                       const double* half_width, const int* child_ptr, const int* child_idx) {
+  ABI_TRY
+  // ctx == NULL: host-only tree (topology queries, no device upload)
+  Ctx* Cp = (Ctx*)ctx;
+  if (n_points <= 0) throw Error(E_VALUE, "points must be non-empty");
+  Tree* t = new Tree;
+  t->ctx = Cp;
+  t->n_points = n_points;
+  t->depth = depth;
+  t->nc = n_clusters;
+  t->points.assign(points, points + 3 * (size_t)n_points);
+  t->perm.assign(perm, perm + n_points);
+  t->level.assign(level, level + n_clusters);
+  t->parent.assign(parent, parent + n_clusters);
+  t->start.assign(start, start + n_clusters);
+  t->stop.assign(stop, stop + n_clusters);
+  t->cell.assign(cell, cell + 3 * (size_t)n_clusters);
+  t->center.assign(center, center + 3 * (size_t)n_clusters);
+  t->hw.assign(half_width, half_width + n_clusters);
+  t->children.assign(n_clusters, {});
+  for (int c = 0; c < n_clusters; ++c)
+    t->children[c].assign(child_idx + child_ptr[c], child_idx + child_ptr[c + 1]);
+  t->levels.assign(depth + 1, {});
+  for (int c = 0; c < n_clusters; ++c) {
+    if (level[c] < 0 || level[c] > depth) throw Error(E_VALUE, "cluster level out of range");
+    t->levels[level[c]].push_back(c);
+  }
+  // ids within a level are Morton ordered by construction (tree.py:158-193)
+  t->build_topology();
+  if (Cp) {
+    t->d_points = Cp->arena.alloc(3 * (size_t)n_points, &t->d_points_cls);
+    CUDA_CHECK(cudaMemcpy(t->d_points, points, sizeof(double) * 3 * n_points, cudaMemcpyHostToDevice));
+    t->d_perm = Cp->arena.alloc_int(n_points, &t->d_perm_cls);
+    CUDA_CHECK(cudaMemcpy(t->d_perm, perm, sizeof(int) * n_points, cudaMemcpyHostToDevice));
+  }
+  return t;
+  ABI_CATCH_NULL
+}
+
+void ifmm_tree_destroy(void* p) {
+  if (!p) return;
+  Tree* t = (Tree*)p;
+  if (t->ctx) {
+    t->ctx->sync();
+    t->ctx->free_raw(t->d_points, t->d_points_cls);
+    t->ctx->free_raw(t->d_perm, t->d_perm_cls);
+    t->ctx->flush();
+  }
+  delete t;
+}
+
+int ifmm_tree_topology_sizes(void* p, long long* nn, long long* ni) {
+  Tree* t = (Tree*)p;
+  long long a = 0, b = 0;
+  for (int c = 0; c < t->nc; ++c) { a += t->nbrs[c].size(); b += t->inters[c].size(); }
+  *nn = a; *ni = b;
+  return 0;
+}
+
+int ifmm_tree_topology(void* p, long long* nbr_ptr, int* nbr_idx, long long* int_ptr,
+                       int* int_idx) {
+  Tree* t = (Tree*)p;
+  long long a = 0, b = 0;
+  for (int c = 0; c < t->nc; ++c) {
+    nbr_ptr[c] = a; int_ptr[c] = b;
+    for (int q : t->nbrs[c]) nbr_idx[a++] = q;
+    for (int q : t->inters[c]) int_idx[b++] = q;
+  }
+  nbr_ptr[t->nc] = a; int_ptr[t->nc] = b;
+  return 0;
+}
+
+// ---- H2 ---------------------------------------------------------------------
+void* ifmm_h2_build(void* tree, int kernel_kind, double p0, int n_cheb, double epsilon) {
+  ABI_TRY
+  Tree* t = (Tree*)tree;
+  if (!t->ctx) throw Error(E_CUDA, "tree has no device context");
+  if (n_cheb < 1) throw Error(E_VALUE, "n must be >= 1");
+  if (n_cheb > MAX_CHEB) throw Error(E_VALUE, "n_cheb too large");
+  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
+  H2* h = new H2;
+  h->ctx = t->ctx;
+  h->tree = t;
+  h->kern.kind = kernel_kind;
+  h->kern.p0 = p0;
+  h->ncheb = n_cheb;
+  h->eps = epsilon;
+  try {
+    h->build();
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+  ABI_CATCH_NULL
+}
+
+void ifmm_h2_destroy(void* p) {
+  if (!p) return;
+  H2* h = (H2*)p;
+  h->ctx->sync();
+  delete h;
+}
+
+int ifmm_h2_ranks(void* p, int* out) {
+  H2* h = (H2*)p;
+  for (int c = 0; c < h->tree->nc; ++c) out[c] = h->rank[c];
+  return 0;
+}
+
+int ifmm_h2_weights(void* p) {
+  ABI_TRY
+  ((H2*)p)->weights();
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_h2_block(void* p, int which, int i, int j, double* out, int* rows, int* cols) {
+  ABI_TRY
+  H2* h = (H2*)p;
+  const int nc = h->tree->nc;
+  if (i < 0 || i >= nc || ((which == 4 || which == 5) && (j < 0 || j >= nc)))
+    throw Error(E_VALUE, "cluster id out of range");
+  const Blk* b = nullptr;
+  switch (which) {
+    case 0: b = &h->leaf_u[i]; break;
+    case 1: b = &h->leaf_v[i]; break;
+    case 2: b = &h->tu[i]; break;
+    case 3: b = &h->tvt[i]; break;
+    case 4: { auto it = h->coupling.find(key2(i, j)); if (it != h->coupling.end()) b = &it->second; break; }
+    case 5: { auto it = h->near.find(key2(i, j)); if (it != h->near.end()) b = &it->second; break; }
+    case 6: b = &h->su[i]; break;
+    case 7: b = &h->sv[i]; break;
+    default: throw Error(E_VALUE, "bad block selector");
+  }
+  if (!b || !b->p) { *rows = -1; *cols = -1; return 0; }
+  *rows = b->r; *cols = b->c;
+  if (out) {
+    h->ctx->sync();
+    CUDA_CHECK(cudaMemcpy(out, b->p, sizeof(double) * b->r * b->c, cudaMemcpyDeviceToHost));
+  }
+  return 0;
+  ABI_CATCH
+}
+
+// gather/scatter by the tree permutation on device
+namespace {
+__global__ void k_gather(const double* in, const int* perm, int n, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[perm[i]];
+}
+__global__ void k_scatter(const double* in, const int* perm, int n, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = in[i];
+}
+}  // namespace
+
+int ifmm_h2_matvec(void* p, const double* x, double* y, int on_device) {
+  ABI_TRY
+  H2* h = (H2*)p;
+  Ctx& C = *h->ctx;
+  const int N = h->tree->n_points;
+  Blk xin = C.alloc(1, N), xs = C.alloc(1, N), ys = C.alloc(1, N), yo = C.alloc(1, N);
+  if (on_device) CUDA_CHECK(cudaMemcpyAsync(xin.p, x, 8 * (size_t)N, cudaMemcpyDeviceToDevice, C.st));
+  else CUDA_CHECK(cudaMemcpyAsync(xin.p, x, 8 * (size_t)N, cudaMemcpyHostToDevice, C.st));
+  k_gather<<<(N + 255) / 256, 256, 0, C.st>>>(xin.p, h->tree->d_perm, N, xs.p);
+  h->matvec(xs.p, ys.p);
+  k_scatter<<<(N + 255) / 256, 256, 0, C.st>>>(ys.p, h->tree->d_perm, N, yo.p);
+  if (on_device) CUDA_CHECK(cudaMemcpyAsync(y, yo.p, 8 * (size_t)N, cudaMemcpyDeviceToDevice, C.st));
+  else CUDA_CHECK(cudaMemcpyAsync(y, yo.p, 8 * (size_t)N, cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  for (Blk* b : {&xin, &xs, &ys, &yo}) C.free(*b);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
+// ---- graph ------------------------------------------------------------------
+void* ifmm_graph_build(void* h2) {
+  ABI_TRY
+  H2* h = (H2*)h2;
+  if (h->tree->depth >= 2 && !h->weighted)
+    throw Error(E_VALUE, "operators have no basis weights; run initialize_weights first");
+  Graph* g = new Graph;
+  g->ctx = h->ctx;
+  try {
+    g->build(h);
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  return g;
+  ABI_CATCH_NULL
+}
+
+void ifmm_graph_destroy(void* p) {
+  if (!p) return;
+  Graph* g = (Graph*)p;
+  g->ctx->sync();
+  delete g;
+}
+
+int ifmm_graph_info(void* p, long long* dim, long long* nn, long long* ne) {
+  Graph* g = (Graph*)p;
+  *dim = g->dim();
+  *nn = (long long)g->size.size();
+  *ne = (long long)g->E.size();
+  return 0;
+}
+
+int ifmm_graph_sigma0(void* p, const double* omega, int width, int power_iters, double* out) {
+  ABI_TRY
+  Graph* g = (Graph*)p;
+  if (g->consumed) throw Error(E_VALUE, "graph already factorized");
+  *out = g->sigma0(omega, width, power_iters);
+  return 0;
+  ABI_CATCH
+}
+
+// ---- factorize / solve --------------------------------------------------------
+void* ifmm_factorize(void* graph, double epsilon, double sigma0, int flags) {
+  ABI_TRY
+  return factorize((Graph*)graph, epsilon, sigma0, flags);
+  ABI_CATCH_NULL
+}
+
+void ifmm_factor_destroy(void* p) {
+  if (!p) return;
+  Factor* f = (Factor*)p;
+  f->ctx->sync();
+  delete f;
+}
+
+int ifmm_factor_stats(void* p, long long* out, int n) {
+  Factor* f = (Factor*)p;
+  long long ne = 0, nr = 0, nm = 0;
+  for (auto& e : f->events) { if (e.type == 0) ne++; else if (e.type == 1) nr++; else nm++; }
+  long long mfr = 0, forced = 0;
+  for (auto& l : f->levels) {
+    for (int r : l.ranks) mfr = std::max<long long>(mfr, r);
+    forced += l.forced;
+  }
+  long long topdim = 0;
+  for (int s : f->top_sizes) topdim += s;
+  long long v[11] = {f->peak_edges, f->n_clusters, f->max_basis_rank, mfr, forced,
+                     (long long)f->levels.size(), ne, nr, nm, (long long)f->top_nodes.size(),
+                     topdim};
+  for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
+  return 0;
+}
+
+int ifmm_factor_level_stats(void* p, long long* out, int n) {
+  Factor* f = (Factor*)p;
+  for (int i = 0; i < n && i < (int)f->levels.size(); ++i) {
+    const LevelStats& l = f->levels[i];
+    long long s = 0, mx = 0;
+    for (int r : l.ranks) { s += r; mx = std::max<long long>(mx, r); }
+    long long v[8] = {l.level, l.compressed, l.added, l.dropped, s, mx, (long long)l.ranks.size(),
+                      l.forced};
+    for (int j = 0; j < 8; ++j) out[8 * i + j] = v[j];
+  }
+  return 0;
+}
+
+int ifmm_factor_level_ranks(void* p, int li, int* out) {
+  Factor* f = (Factor*)p;
+  if (li < 0 || li >= (int)f->levels.size()) return E_VALUE;
+  const auto& r = f->levels[li].ranks;
+  for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+  return 0;
+}
+
+int ifmm_factor_timings(void* p, double* out, int n) {
+  Factor* f = (Factor*)p;
+  double v[7] = {f->t_lu, f->t_mm, f->t_lr, f->t_tr, f->t_total, f->gemm_flops, f->all_flops};
+  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+  return 0;
+}
+
+int ifmm_solve(void* p, const double* b, double* x, int on_device) {
+  ABI_TRY
+  Factor* f = (Factor*)p;
+  Ctx& C = *f->ctx;
+  const int N = f->n_points;
+  if (on_device) {
+    f->solve(b, x);
+    C.sync();
+  } else {
+    Blk bi = C.alloc(1, N), xo = C.alloc(1, N);
+    CUDA_CHECK(cudaMemcpyAsync(bi.p, b, 8 * (size_t)N, cudaMemcpyHostToDevice, C.st));
+    f->solve(bi.p, xo.p);
+    CUDA_CHECK(cudaMemcpyAsync(x, xo.p, 8 * (size_t)N, cudaMemcpyDeviceToHost, C.st));
+    C.sync();
+    C.free(bi);
+    C.free(xo);
+    C.flush();
+  }
+  return 0;
+  ABI_CATCH
+}
+
+// ---- micro-kernel entry points --------------------------------------------------
+int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,
+                  const double* B, int ldb, int tb, double* Cm, int ldc, double alpha,
+                  double beta) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  GemmBatch g;
+  g.add(A, lda, ta, B, ldb, tb, Cm, ldc, M, N, K, alpha, beta);
+  g.run(C);
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_dev_svd(void* ctx, int m, int n, const double* A, double thr, double* U, double* S,
+                 double* V, int* rank) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  Blk w = C.alloc(1, (int)svd_work_doubles(m, n));
+  std::vector<SvdDesc> d(1);
+  d[0].src = A; d[0].m = m; d[0].n = n; d[0].s_r = n; d[0].s_c = 1;
+  d[0].U = U; d[0].S = S; d[0].V = V; d[0].rank = rank; d[0].work = w.p;
+  launch_svd(C.stage.push_vec(C, d), 1, thr, 0, C.st, 0);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  C.free(w);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_dev_lu_solve(void* ctx, int n, double* A, int* piv, double* X, int nrhs) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  lu_any(C, A, n, piv, 0);
+  std::vector<LuSolveDesc> d(1);
+  d[0].LU = A; d[0].piv = piv; d[0].n = n; d[0].lda = n; d[0].X = X; d[0].nrhs = nrhs;
+  d[0].ldx = nrhs;
+  if (nrhs > 0) launch_lusolve(C.stage.push_vec(C, d), 1, nrhs, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  C.check_status("test ");
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const double* w,
+                   const double* F, const double* wf, double thr, int min_rank, double* NB,
+                   double* NW, double* OM, double* FM, int* rank) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  Blk wk = C.alloc(1, (int)union_work_doubles(m, k_old, k_f));
+  std::vector<UnionDesc> d(1);
+  d[0].B = B; d[0].w = w; d[0].F = F; d[0].wf = wf;
+  d[0].m = m; d[0].k_old = k_old; d[0].k_f = k_f;
+  d[0].b_r = k_old; d[0].b_c = 1; d[0].f_r = k_f; d[0].f_c = 1;  // row-major inputs
+  d[0].min_rank = min_rank;
+  d[0].NB = NB; d[0].nb_r = 1; d[0].nb_c = m;                    // col-major output
+  d[0].NW = NW; d[0].OM = OM; d[0].FM = FM; d[0].rank = rank; d[0].work = wk.p;
+  launch_union(C.stage.push_vec(C, d), 1, thr, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  C.free(wk);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_dev_sync(void* ctx) {
+  ABI_TRY
+  ((Ctx*)ctx)->sync();
+  return 0;
+  ABI_CATCH
+}
+
+}  // extern "C"

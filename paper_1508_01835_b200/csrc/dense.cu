@@ -1,0 +1,1019 @@
+// Batched small dense fp64 linear algebra for the IFMM elimination (sm_100a).
+//
+//  * grouped GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA),
+//  * LU with partial pivoting (getrf semantics, factor.py:166-173) and
+//    multi-RHS LU solves (factor.py:160-163),
+//  * one-sided Jacobi SVD (truncated_svd, lowrank.py:54-61),
+//  * full-pivot ACA + Householder QR-QR-SVD basis union
+//    (aca_svd / weighted_basis_union, lowrank.py:128-199),
+//  * strided block copy / accumulate (graph edge updates, merge tiling).
+//
+// Every routine is a CTA-cooperative device function over generic pointers
+// (shared or global memory) wrapped by a batched kernel: one CTA per matrix,
+// many matrices per launch.
+#include "common.cuh"
+#include "dense.h"
+
+#include <cstdio>
+
+namespace ifmm {
+
+// ============================================================================
+// Grouped GEMM (DMMA)
+// ============================================================================
+
+namespace {
+constexpr int GT_M = 64, GT_N = 64, GT_K = 16, G_LD = GT_M + 4;
+
+__global__ void __launch_bounds__(128)
+gemm_grouped_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ tstart,
+                    int nprob, int total) {
+  __shared__ double As[2][GT_K][G_LD];
+  __shared__ double Bs[2][GT_K][G_LD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    // locate problem: largest p with tstart[p] <= tile
+    int lo = 0, hi = nprob - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (tstart[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    const GemmDesc d = descs[lo];
+    const int local = tile - tstart[lo];
+    const int tiles_n = (d.N + GT_N - 1) / GT_N;
+    const int m0 = (local / tiles_n) * GT_M, n0 = (local % tiles_n) * GT_N;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    double ra[8], rb[8];
+    auto load_tile = [&](int k0) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        int mm, kk;
+        if (d.ta == 0) { kk = tid & 15; mm = (tid >> 4) + 8 * r; }
+        else { mm = tid & 63; kk = (tid >> 6) + 2 * r; }
+        int gm = m0 + mm, gk = k0 + kk;
+        double v = 0.0;
+        if (gm < d.M && gk < d.K) {
+          v = d.ta == 0 ? d.A[(size_t)gm * d.lda + gk] : d.A[(size_t)gk * d.lda + gm];
+          if (d.dscale) v *= d.dscale[gk];
+        }
+        ra[r] = v;
+        int nn, kb;
+        if (d.tb == 0) { nn = tid & 63; kb = (tid >> 6) + 2 * r; }
+        else { kb = tid & 15; nn = (tid >> 4) + 8 * r; }
+        int gn = n0 + nn, gkb = k0 + kb;
+        double w = 0.0;
+        if (gn < d.N && gkb < d.K)
+          w = d.tb == 0 ? d.B[(size_t)gkb * d.ldb + gn] : d.B[(size_t)gn * d.ldb + gkb];
+        rb[r] = w;
+      }
+    };
+    auto store_tile = [&](int buf) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        int mm, kk;
+        if (d.ta == 0) { kk = tid & 15; mm = (tid >> 4) + 8 * r; }
+        else { mm = tid & 63; kk = (tid >> 6) + 2 * r; }
+        As[buf][kk][mm] = ra[r];
+        int nn, kb;
+        if (d.tb == 0) { nn = tid & 63; kb = (tid >> 6) + 2 * r; }
+        else { kb = tid & 15; nn = (tid >> 4) + 8 * r; }
+        Bs[buf][kb][nn] = rb[r];
+      }
+    };
+
+    const int nk = (d.K + GT_K - 1) / GT_K;
+    if (nk > 0) {
+      load_tile(0);
+      store_tile(0);
+    }
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+      const int buf = kt & 1;
+      if (kt + 1 < nk) load_tile((kt + 1) * GT_K);
+#pragma unroll
+      for (int k4 = 0; k4 < GT_K; k4 += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][k4 + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      if (kt + 1 < nk) store_tile(buf ^ 1);
+      __syncthreads();
+    }
+    // epilogue
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
+      if (gm >= d.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gn = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + e;
+          if (gn >= d.N) continue;
+          double* c = d.C + (size_t)gm * d.ldc + gn;
+          double v = d.alpha * acc[i][j][e];
+          if (d.beta != 0.0) v += d.beta * (*c);
+          *c = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob, int total_tiles,
+                 cudaStream_t s) {
+  if (total_tiles <= 0) return;
+  int grid = total_tiles < 148 * 8 ? total_tiles : 148 * 8;
+  gemm_grouped_kernel<<<grid, 128, 0, s>>>(d_descs, d_tile_start, nprob, total_tiles);
+}
+
+// ============================================================================
+// Strided copy / accumulate
+// ============================================================================
+
+namespace {
+__global__ void copy_kernel(const CopyDesc* __restrict__ descs, int n) {
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const CopyDesc d = descs[b];
+    const long long tot = (long long)d.rows * d.cols;
+    for (long long e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int i = (int)(e / d.cols), j = (int)(e % d.cols);
+      double* o = d.dst + (size_t)i * d.ds_r + (size_t)j * d.ds_c;
+      switch (d.mode) {
+        case 0: *o = (d.rscale ? d.alpha * d.rscale[i] : d.alpha) * d.src[(size_t)i * d.ss_r + (size_t)j * d.ss_c]; break;
+        case 1: *o += (d.rscale ? d.alpha * d.rscale[i] : d.alpha) * d.src[(size_t)i * d.ss_r + (size_t)j * d.ss_c]; break;
+        case 2: *o = (i == j) ? d.alpha : 0.0; break;
+        case 4: *o = d.alpha; break;
+        default: *o = 0.0; break;
+      }
+    }
+  }
+}
+}  // namespace
+
+void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  copy_kernel<<<n < 4096 ? n : 4096, 256, 0, s>>>(d_descs, n);
+}
+
+// ============================================================================
+// One-sided Jacobi SVD (Hestenes) -- CTA cooperative
+// ============================================================================
+
+// W: col-major rows x cols (ld ldw, rows >= cols); V: col-major cols x cols
+// (ld cols) initialised here to I.  On exit W's columns are sigma_j u_j
+// (unsorted) and V holds the accumulated rotations.
+__device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, int* sflag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < cols * cols; e += blockDim.x)
+    V[e] = (e % (cols + 1) == 0) ? 1.0 : 0.0;
+  const double tol = kEps * sqrt((double)(rows > 1 ? rows : 1));
+  const int cp = cols + (cols & 1);
+  __syncthreads();
+  if (cols < 2) return;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) *sflag = 0;
+    __syncthreads();
+    for (int r = 0; r < cp - 1; ++r) {
+      for (int pi = warp; pi < cp / 2; pi += nw) {
+        int p, q;
+        if (pi == 0) { p = r; q = cp - 1; }
+        else { p = (r + pi) % (cp - 1); q = (r - pi + cp - 1) % (cp - 1); }
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= cols) continue;
+        double* x = W + (size_t)p * ldw;
+        double* y = W + (size_t)q * ldw;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < rows; i += 32) {
+          const double u = x[i], v = y[i];
+          a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
+        }
+        a = warp_sum(a); b = warp_sum(b); g = warp_sum(g);
+        if (g != 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = lane; i < rows; i += 32) {
+            const double u = x[i], v = y[i];
+            x[i] = c * u - s * v;
+            y[i] = s * u + c * v;
+          }
+          double* vx = V + (size_t)p * cols;
+          double* vy = V + (size_t)q * cols;
+          for (int i = lane; i < cols; i += 32) {
+            const double u = vx[i], v = vy[i];
+            vx[i] = c * u - s * v;
+            vy[i] = s * u + c * v;
+          }
+          if (lane == 0) *sflag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int again = *sflag;
+    __syncthreads();
+    if (!again) break;
+  }
+}
+
+// Column norms -> sigma[j]; order[pos] = j sorted by sigma desc (ties: lower j).
+__device__ void cta_sv_order(const double* W, int rows, int cols, int ldw, double* sig, int* order) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < cols; j += nw) {
+    double a = 0.0;
+    for (int i = lane; i < rows; i += 32) { const double u = W[(size_t)j * ldw + i]; a = fma(u, u, a); }
+    a = warp_sum(a);
+    if (lane == 0) sig[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+    const double sj = sig[j];
+    int pos = 0;
+    for (int l = 0; l < cols; ++l) {
+      const double sl = sig[l];
+      pos += (sl > sj) || (sl == sj && l < j);
+    }
+    order[pos] = j;
+  }
+  __syncthreads();
+}
+
+__host__ __device__ size_t svd_work_doubles(int m, int n) {
+  const int rows = m > n ? m : n, cols = m > n ? n : m;
+  return (size_t)rows * cols + (size_t)cols * cols + 2 * (size_t)cols + 8;
+}
+
+namespace {
+__global__ void __launch_bounds__(512)
+svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_doubles, int rel_mode) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int sflag;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const SvdDesc d = descs[b];
+    const bool tr = d.m < d.n;
+    const int rows = tr ? d.n : d.m, cols = tr ? d.m : d.n;
+    if (cols == 0) { if (threadIdx.x == 0) *d.rank = 0; continue; }
+    const size_t need = svd_work_doubles(d.m, d.n);
+    double* W = (need <= (size_t)smem_doubles) ? smem : d.work;
+    double* V = W + (size_t)rows * cols;
+    double* sig = V + (size_t)cols * cols;
+    int* order = (int*)(sig + cols);
+    // load (col-major rows x cols) and Frobenius norm
+    double fro = 0.0;
+    for (long long e = threadIdx.x; e < (long long)rows * cols; e += blockDim.x) {
+      const int j = (int)(e / rows), i = (int)(e % rows);
+      // element (i,j) of the oriented matrix
+      const double v = tr ? d.src[(size_t)j * d.s_r + (size_t)i * d.s_c]
+                          : d.src[(size_t)i * d.s_r + (size_t)j * d.s_c];
+      W[e] = v;
+      fro = fma(v, v, fro);
+    }
+    fro = block_sum(fro, red);
+    // exact pre-filter: sigma_1 <= ||F||_F <= thr  =>  rank 0
+    if (!rel_mode && sqrt(fro) <= thr * (1.0 - 1e-12)) {
+      if (threadIdx.x == 0) *d.rank = 0;
+      __syncthreads();
+      continue;
+    }
+    cta_jacobi(W, rows, cols, rows, V, &sflag);
+    cta_sv_order(W, rows, cols, rows, sig, order);
+    int k = 0;
+    if (rel_mode) {  // h2.py:124-127: max(1, #{s > rel * s0})
+      const double t = thr * sig[order[0]];
+      for (int j = 0; j < cols; ++j) k += sig[order[j]] > t;
+      if (k < 1) k = 1;
+    } else {
+      for (int j = 0; j < cols; ++j) k += sig[order[j]] > thr;
+    }
+    // write U (m x k) col-major ld m, S, V (n x k) col-major ld n
+    for (long long e = threadIdx.x; e < (long long)rows * k; e += blockDim.x) {
+      const int pos = (int)(e / rows), i = (int)(e % rows);
+      const int j = order[pos];
+      const double u = W[(size_t)j * rows + i] / sig[j];
+      if (!tr) d.U[(size_t)pos * d.m + i] = u; else d.V[(size_t)pos * d.n + i] = u;
+    }
+    for (long long e = threadIdx.x; e < (long long)cols * k; e += blockDim.x) {
+      const int pos = (int)(e / cols), i = (int)(e % cols);
+      const double v = V[(size_t)order[pos] * cols + i];
+      if (!tr) d.V[(size_t)pos * d.n + i] = v; else d.U[(size_t)pos * d.m + i] = v;
+    }
+    for (int pos = threadIdx.x; pos < k; pos += blockDim.x) d.S[pos] = sig[order[pos]];
+    if (threadIdx.x == 0) *d.rank = k;
+    __syncthreads();
+  }
+}
+}  // namespace
+
+size_t svd_smem_doubles(int max_smem_dim) {
+  size_t need = svd_work_doubles(max_smem_dim, max_smem_dim);
+  return need * sizeof(double) > 200 * 1024 ? 0 : need;
+}
+
+void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim, cudaStream_t s,
+                int rel_mode) {
+  if (n <= 0) return;
+  // shared-memory workspace for blocks up to max_smem_dim^2 (fits 200 KB)
+  size_t bytes = svd_smem_doubles(max_smem_dim) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  svd_kernel<<<n < 4096 ? n : 4096, 512, bytes, s>>>(d_descs, n, thr, (int)(bytes / sizeof(double)),
+                                                     rel_mode);
+}
+
+// ============================================================================
+// Householder QR (dgeqrf/dlarfg conventions) -- CTA cooperative
+// ============================================================================
+
+// A: col-major rows x cols (ld lda), rows >= cols.  In place: R in the upper
+// triangle, Householder vectors (implicit unit head) below; tau[cols].
+__device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double s_beta, s_tau, s_scale;
+  for (int j = 0; j < cols; ++j) {
+    double* a = A + (size_t)j * lda;
+    double nx = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) nx = fma(a[i], a[i], nx);
+    nx = block_sum(nx, red);
+    if (threadIdx.x == 0) {
+      const double alpha = a[j];
+      if (nx == 0.0) { s_tau = 0.0; s_beta = alpha; s_scale = 0.0; }
+      else {
+        const double beta = -copysign(sqrt(alpha * alpha + nx), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scale = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+      tau[j] = s_tau;
+    }
+    __syncthreads();
+    const double sc = s_scale, tj = s_tau;
+    if (tj != 0.0)
+      for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) a[i] *= sc;
+    __syncthreads();
+    if (threadIdx.x == 0) a[j] = s_beta;
+    // apply H = I - tau v v^T to trailing columns
+    if (tj != 0.0) {
+      for (int c = j + 1 + warp; c < cols; c += nw) {
+        double* ac = A + (size_t)c * lda;
+        double w = (lane == 0) ? ac[j] : 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) w = fma(a[i], ac[i], w);
+        w = warp_sum(w) * tj;
+        if (lane == 0) ac[j] -= w;
+        for (int i = j + 1 + lane; i < rows; i += 32) ac[i] -= w * a[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Form Q (rows x cols, col-major ld ldq) from cta_geqrf output.
+__device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
+                          double* Q, int ldq) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long long e = threadIdx.x; e < (long long)rows * cols; e += blockDim.x) {
+    const int c = (int)(e / rows), i = (int)(e % rows);
+    Q[(size_t)c * ldq + i] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = cols - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj != 0.0) {
+      const double* v = A + (size_t)j * lda;
+      for (int c = j + warp; c < cols; c += nw) {
+        double* qc = Q + (size_t)c * ldq;
+        double w = (lane == 0) ? qc[j] : 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) w = fma(v[i], qc[i], w);
+        w = warp_sum(w) * tj;
+        if (lane == 0) qc[j] -= w;
+        for (int i = j + 1 + lane; i < rows; i += 32) qc[i] -= w * v[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================
+// Weighted basis union: ACA (full pivot) + QR + QR + Jacobi SVD
+// ============================================================================
+
+size_t union_work_doubles(int m, int k_old, int k_f) {
+  const size_t C = (size_t)k_old + k_f;
+  const size_t s = (size_t)(m < (int)C ? m : (int)C);
+  // M(mC) Acol(m s) Bt(C s) QA(m s) QB(C s) core(s s) V(s s) tau 2s sig s order s
+  return (size_t)m * C + 2 * (size_t)m * s + 2 * C * s + 2 * s * s + 5 * s + 16;
+}
+
+namespace {
+__global__ void __launch_bounds__(512)
+union_kernel(const UnionDesc* __restrict__ descs, int n, double thr) {
+  __shared__ double red[32];
+  __shared__ long long redi[32];
+  __shared__ int sflag;
+  __shared__ double s_piv;
+  __shared__ int s_p, s_q, s_stop;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const UnionDesc d = descs[b];
+    const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
+    const int smax = m < C ? m : C;
+    double* M = d.work;
+    double* Acol = M + (size_t)m * C;
+    double* Bt = Acol + (size_t)m * smax;
+    double* QA = Bt + (size_t)C * smax;
+    double* QB = QA + (size_t)m * smax;
+    double* core = QB + (size_t)C * smax;
+    double* Vc = core + (size_t)smax * smax;
+    double* tauA = Vc + (size_t)smax * smax;
+    double* tauB = tauA + smax;
+    double* sig = tauB + smax;
+    int* order = (int*)(sig + smax);
+
+    // concat [B*diag(w) | F*diag(wf)]  (col-major m x C)
+    for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
+      const int j = (int)(e / m), i = (int)(e % m);
+      M[e] = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
+                    : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+    }
+    __syncthreads();
+    // ---- ACA with full pivoting, floor thr/8 (lowrank.py:145-151) ----
+    const double floor_ = thr / 8.0;
+    int steps = 0;
+    for (int it = 0; it < smax; ++it) {
+      double bv = -1.0;
+      long long bi = (1LL << 62);
+      for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
+        const double v = fabs(M[e]);
+        const int j = (int)(e / m), i = (int)(e % m);
+        const long long flat = (long long)i * C + j;  // numpy row-major order
+        if (v > bv || (v == bv && flat < bi)) { bv = v; bi = flat; }
+      }
+      block_argmax(bv, bi, red, redi);
+      if (threadIdx.x == 0) {
+        s_p = (int)(bi / C); s_q = (int)(bi % C);
+        s_piv = M[(size_t)s_q * m + s_p];
+        s_stop = (s_piv == 0.0 || (fabs(s_piv) <= floor_ && steps >= d.min_rank)) ? 1 : 0;
+      }
+      __syncthreads();
+      if (s_stop) break;
+      const int p = s_p, q = s_q;
+      const double piv = s_piv;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) Acol[(size_t)steps * m + i] = M[(size_t)q * m + i];
+      for (int j = threadIdx.x; j < C; j += blockDim.x) Bt[(size_t)steps * C + j] = M[(size_t)j * m + p] / piv;
+      __syncthreads();
+      const double* cc = Acol + (size_t)steps * m;
+      const double* rr = Bt + (size_t)steps * C;
+      for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
+        const int j = (int)(e / m), i = (int)(e % m);
+        M[e] -= cc[i] * rr[j];
+      }
+      ++steps;
+      __syncthreads();
+    }
+    if (steps == 0) {
+      if (threadIdx.x == 0) *d.rank = 0;
+      __syncthreads();
+      continue;
+    }
+    const int s = steps;
+    // ---- QR(A), QR(B^T) ----
+    cta_geqrf(Acol, m, s, m, tauA, red);
+    cta_geqrf(Bt, C, s, C, tauB, red);
+    // core = RA * RB^T (s x s, col-major)
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+      const int j = e / s, i = e % s;
+      double acc = 0.0;
+      for (int l = (i > j ? i : j); l < s; ++l)
+        acc = fma(Acol[(size_t)l * m + i], Bt[(size_t)l * C + j], acc);
+      core[(size_t)j * s + i] = acc;
+    }
+    cta_orgqr(Acol, m, s, m, tauA, QA, m);
+    cta_orgqr(Bt, C, s, C, tauB, QB, C);
+    __syncthreads();
+    cta_jacobi(core, s, s, s, Vc, &sflag);
+    cta_sv_order(core, s, s, s, sig, order);
+    int kk = 0;
+    for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
+    const int mr = d.min_rank < s ? d.min_rank : s;
+    const int k = kk > mr ? kk : mr;
+    // new basis = QA * Wcore[:, :k]  (Wcore col = core col / sigma)
+    for (long long e = threadIdx.x; e < (long long)m * k; e += blockDim.x) {
+      const int a = (int)(e / m), i = (int)(e % m);
+      const int j = order[a];
+      const double inv = sig[j] > 0.0 ? 1.0 / sig[j] : 0.0;
+      double acc = 0.0;
+      for (int l = 0; l < s; ++l) acc = fma(QA[(size_t)l * m + i], core[(size_t)j * s + l], acc);
+      d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc * inv;
+    }
+    // V_full = QB * Vc[:, order[:k]]  (C x k); maps = sigma_a V_full[col][a] / weight
+    for (long long e = threadIdx.x; e < (long long)C * k; e += blockDim.x) {
+      const int a = (int)(e / C), col = (int)(e % C);
+      const int j = order[a];
+      double acc = 0.0;
+      for (int l = 0; l < s; ++l) acc = fma(QB[(size_t)l * C + col], Vc[(size_t)j * s + l], acc);
+      const double v = sig[j] * acc;
+      if (col < ko) d.OM[(size_t)a * ko + col] = v / d.w[col];
+      else d.FM[(size_t)a * d.k_f + (col - ko)] = v / d.wf[col - ko];
+    }
+    for (int a = threadIdx.x; a < k; a += blockDim.x) d.NW[a] = sig[order[a]];
+    if (threadIdx.x == 0) *d.rank = k;
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s) {
+  if (n <= 0) return;
+  union_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d_descs, n, thr);
+}
+
+// ============================================================================
+// LU with partial pivoting (row-major, in place) -- CTA cooperative
+// ============================================================================
+
+namespace {
+__global__ void __launch_bounds__(512)
+lu_kernel(const LuDesc* __restrict__ descs, int n, int* status, int smem_doubles) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ long long redi[32];
+  __shared__ int s_p;
+  __shared__ int s_bad;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const LuDesc d = descs[b];
+    const int N = d.n;
+    const bool sm = (long long)N * N <= smem_doubles;
+    double* A = sm ? smem : d.A;
+    const int lda = sm ? N : d.lda;
+    if (sm)
+      for (long long e = threadIdx.x; e < (long long)N * N; e += blockDim.x)
+        smem[e] = d.A[(size_t)(e / N) * d.lda + (e % N)];
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int j = 0; j < N; ++j) {
+      double bv = -1.0;
+      long long bi = (1LL << 62);
+      for (int i = j + threadIdx.x; i < N; i += blockDim.x) {
+        const double v = fabs(A[(size_t)i * lda + j]);
+        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+      }
+      // NaN pivots: treat as bad
+      block_argmax(bv, bi, red, redi);
+      if (threadIdx.x == 0) {
+        int p = (bi >= N || bi < j) ? j : (int)bi;
+        s_p = p;
+        d.piv[j] = p;
+        const double pv = A[(size_t)p * lda + j];
+        if (pv == 0.0 || !isfinite(pv)) s_bad = 1;
+      }
+      __syncthreads();
+      const int p = s_p;
+      if (p != j)
+        for (int c = threadIdx.x; c < N; c += blockDim.x) {
+          const double t = A[(size_t)j * lda + c];
+          A[(size_t)j * lda + c] = A[(size_t)p * lda + c];
+          A[(size_t)p * lda + c] = t;
+        }
+      __syncthreads();
+      const double pv = A[(size_t)j * lda + j];
+      if (pv != 0.0)
+        for (int i = j + 1 + threadIdx.x; i < N; i += blockDim.x) A[(size_t)i * lda + j] /= pv;
+      __syncthreads();
+      const int rem = N - j - 1;
+      if (rem > 0)
+        for (long long e = threadIdx.x; e < (long long)rem * rem; e += blockDim.x) {
+          const int i = j + 1 + (int)(e / rem), c = j + 1 + (int)(e % rem);
+          A[(size_t)i * lda + c] -= A[(size_t)i * lda + j] * A[(size_t)j * lda + c];
+        }
+      __syncthreads();
+    }
+    // final finiteness scan (factor.py:171)
+    int bad = 0;
+    for (long long e = threadIdx.x; e < (long long)N * N; e += blockDim.x)
+      if (!isfinite(A[(size_t)(e / N) * lda + (e % N)])) bad = 1;
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (s_bad && threadIdx.x == 0) atomicCAS(status, 0, d.tag + 1);
+    if (sm)
+      for (long long e = threadIdx.x; e < (long long)N * N; e += blockDim.x)
+        d.A[(size_t)(e / N) * d.lda + (e % N)] = smem[e];
+    __syncthreads();
+  }
+}
+
+// Warp-per-32-columns LU solve: lane owns one RHS column.
+__global__ void __launch_bounds__(256)
+lusolve_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks_per_desc) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int di = gw / chunks_per_desc, ch = gw % chunks_per_desc;
+  if (di >= ndesc) return;
+  const LuSolveDesc d = descs[di];
+  const int c = ch * 32 + lane;
+  if (c >= d.nrhs) return;
+  const int N = d.n;
+  double* x = d.X + c;
+  const size_t ld = d.ldx;
+  for (int j = 0; j < N; ++j) {
+    const int p = d.piv[j];
+    if (p != j) { const double t = x[j * ld]; x[j * ld] = x[p * ld]; x[p * ld] = t; }
+  }
+  for (int i = 1; i < N; ++i) {
+    const double* L = d.LU + (size_t)i * d.lda;
+    double s0 = x[i * ld], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = 0;
+    for (; j + 3 < i; j += 4) {
+      s0 = fma(-L[j], x[j * ld], s0);
+      s1 = fma(-L[j + 1], x[(j + 1) * ld], s1);
+      s2 = fma(-L[j + 2], x[(j + 2) * ld], s2);
+      s3 = fma(-L[j + 3], x[(j + 3) * ld], s3);
+    }
+    for (; j < i; ++j) s0 = fma(-L[j], x[j * ld], s0);
+    x[i * ld] = (s0 + s1) + (s2 + s3);
+  }
+  for (int i = N - 1; i >= 0; --i) {
+    const double* U = d.LU + (size_t)i * d.lda;
+    double s0 = x[i * ld], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = i + 1;
+    for (; j + 3 < N; j += 4) {
+      s0 = fma(-U[j], x[j * ld], s0);
+      s1 = fma(-U[j + 1], x[(j + 1) * ld], s1);
+      s2 = fma(-U[j + 2], x[(j + 2) * ld], s2);
+      s3 = fma(-U[j + 3], x[(j + 3) * ld], s3);
+    }
+    for (; j < N; ++j) s0 = fma(-U[j], x[j * ld], s0);
+    x[i * ld] = ((s0 + s1) + (s2 + s3)) / U[i];
+  }
+}
+}  // namespace
+
+void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
+  if (n <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  const int smem = 200 * 1024;
+  lu_kernel<<<n < 4096 ? n : 4096, 512, smem, s>>>(d_descs, n, d_status, smem / 8);
+}
+
+void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs, cudaStream_t s) {
+  if (ndesc <= 0 || max_nrhs <= 0) return;
+  const int chunks = (max_nrhs + 31) / 32;
+  const long long warps = (long long)ndesc * chunks;
+  const int blocks = (int)((warps + 7) / 8);
+  lusolve_kernel<<<blocks, 256, 0, s>>>(d_descs, ndesc, chunks);
+}
+
+}  // namespace ifmm
+
+// ============================================================================
+// Basis weights (initialize_weights) and tall-skinny QR helpers
+// ============================================================================
+namespace ifmm {
+
+size_t weights_work_doubles(int k, int W) {
+  return 4 * (size_t)k * k + (size_t)k * (W < k ? W : k) + 6 * (size_t)k + 16;
+}
+
+namespace {
+
+// Replace exactly-zero columns of P (k x k col-major, first `good` valid
+// columns orthonormal) by an orthonormal completion from unit vectors.
+__device__ void cta_complete_zero_cols(double* P, int k, const double* sig, double* red) {
+  __shared__ int s_ok;
+  for (int pos = 0; pos < k; ++pos) {
+    if (sig[pos] > 0.0) continue;
+    for (int e = 0; e < k; ++e) {
+      double* v = P + (size_t)pos * k;
+      for (int i = threadIdx.x; i < k; i += blockDim.x) v[i] = (i == e) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int q = 0; q < k; ++q) {
+        if (q == pos || (q > pos && sig[q] <= 0.0)) continue;
+        const double* u = P + (size_t)q * k;
+        double d = 0.0;
+        for (int i = threadIdx.x; i < k; i += blockDim.x) d = fma(u[i], v[i], d);
+        d = block_sum(d, red);
+        for (int i = threadIdx.x; i < k; i += blockDim.x) v[i] -= d * u[i];
+        __syncthreads();
+      }
+      double nn = 0.0;
+      for (int i = threadIdx.x; i < k; i += blockDim.x) nn = fma(v[i], v[i], nn);
+      nn = block_sum(nn, red);
+      if (threadIdx.x == 0) s_ok = nn > 0.25;
+      __syncthreads();
+      if (s_ok) {
+        const double inv = 1.0 / sqrt(nn);
+        for (int i = threadIdx.x; i < k; i += blockDim.x) v[i] *= inv;
+        __syncthreads();
+        break;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) weights_kernel(const WeightDesc* __restrict__ descs, int n) {
+  __shared__ double red[32];
+  __shared__ int sflag;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const WeightDesc d = descs[b];
+    const int k = d.k, W = d.W;
+    double* M = d.work;              // k x k (or k x W)
+    double* V = M + (size_t)k * k;   // k x k
+    double* Pc = V + (size_t)k * k;  // k x k col-major result
+    double* tau = Pc + (size_t)k * k;
+    double* sig = tau + k;           // sorted sigma (k)
+    int* order = (int*)(sig + k);
+    double* sraw = sig + 3 * k;      // unsorted norms
+    if (W >= k) {
+      // H row-major k x W == H^T col-major W x k
+      cta_geqrf(d.H, W, k, W, tau, red);
+      for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int l = e / k, i = e % k;  // M(i,l) = R(l,i)
+        M[e] = (l <= i) ? d.H[(size_t)i * W + l] : 0.0;
+      }
+      __syncthreads();
+      cta_jacobi(M, k, k, k, V, &sflag);
+      cta_sv_order(M, k, k, k, sraw, order);
+      for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int pos = e / k, i = e % k;
+        const int j = order[pos];
+        const double s = sraw[j];
+        Pc[e] = s > 0.0 ? M[(size_t)j * k + i] / s : 0.0;
+      }
+      for (int pos = threadIdx.x; pos < k; pos += blockDim.x) sig[pos] = sraw[order[pos]];
+      __syncthreads();
+      cta_complete_zero_cols(Pc, k, sig, red);
+      // weights = sigma (len k), floor
+      for (int a = threadIdx.x; a < k; a += blockDim.x) {
+        const double scale = sig[0] > 0.0 ? sig[0] : 1.0;
+        d.w[a] = fmax(sig[a], 1e-14 * scale);
+      }
+    } else {
+      // H col-major k x W
+      for (int e = threadIdx.x; e < k * W; e += blockDim.x) {
+        const int w = e / k, a = e % k;
+        M[e] = d.H[(size_t)a * W + w];
+      }
+      __syncthreads();
+      cta_jacobi(M, k, W, k, V, &sflag);
+      cta_sv_order(M, k, W, k, sraw, order);
+      // B = [U (k x W) | e_0 .. e_{k-W-1}]  (k x k col-major) in V-space
+      double* B = V;  // reuse (k x k)
+      for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int pos = e / k, i = e % k;
+        double v;
+        if (pos < W) {
+          const int j = order[pos];
+          v = sraw[j] > 0.0 ? M[(size_t)j * k + i] / sraw[j] : 0.0;
+        } else {
+          v = (i == pos - W) ? 1.0 : 0.0;
+        }
+        B[e] = v;
+      }
+      for (int pos = threadIdx.x; pos < W; pos += blockDim.x) sig[pos] = sraw[order[pos]];
+      __syncthreads();
+      cta_geqrf(B, k, k, k, tau, red);
+      cta_orgqr(B, k, k, k, tau, Pc, k);
+      for (int a = threadIdx.x; a < k; a += blockDim.x) {
+        double v = a < W ? sig[a] : sig[W - 1];
+        const double scale = sig[0] > 0.0 ? sig[0] : 1.0;
+        d.w[a] = fmax(v, 1e-14 * scale);
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      const int i = e / k, pos = e % k;  // P row-major: P[i][pos]
+      d.P[e] = Pc[(size_t)pos * k + i];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+tall_orth_kernel(const double* Y, int n, int w, double* Q, double* work, int mode,
+                 double* out) {
+  __shared__ double red[32];
+  __shared__ int sflag;
+  double* A = work;                 // col-major n x w
+  double* QQ = A + (size_t)n * w;   // col-major n x w
+  double* tau = QQ + (size_t)n * w;
+  for (long long e = threadIdx.x; e < (long long)n * w; e += blockDim.x) {
+    const int c = (int)(e / n), i = (int)(e % n);
+    A[e] = Y[(size_t)i * w + c];
+  }
+  __syncthreads();
+  cta_geqrf(A, n, w, n, tau, red);
+  if (mode == 0) {
+    cta_orgqr(A, n, w, n, tau, QQ, n);
+    __syncthreads();
+    for (long long e = threadIdx.x; e < (long long)n * w; e += blockDim.x) {
+      const int i = (int)(e / w), c = (int)(e % w);
+      Q[e] = QQ[(size_t)c * n + i];
+    }
+  } else {
+    // sigma_max of R (w x w)
+    double* R = QQ;
+    double* V = R + (size_t)w * w;
+    double* sg = V + (size_t)w * w;
+    int* order = (int*)(sg + w);
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+      const int l = e / w, i = e % w;
+      R[e] = (i <= l) ? A[(size_t)l * n + i] : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(R, w, w, w, V, &sflag);
+    cta_sv_order(R, w, w, w, sg, order);
+    if (threadIdx.x == 0) *out = sg[order[0]];
+  }
+}
+
+}  // namespace
+
+void launch_weights(const WeightDesc* d_descs, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  weights_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d_descs, n);
+}
+
+void launch_tall_orth(const double* Y, int n, int w, double* Q, double* work, cudaStream_t s) {
+  tall_orth_kernel<<<1, 1024, 0, s>>>(Y, n, w, Q, work, 0, nullptr);
+}
+
+void launch_tall_sigmax(const double* Y, int n, int w, double* out, double* work,
+                        cudaStream_t s) {
+  tall_orth_kernel<<<1, 1024, 0, s>>>(Y, n, w, nullptr, work, 1, out);
+}
+
+}  // namespace ifmm
+
+// ============================================================================
+// Blocked LU pieces, triangular solve, extension
+// ============================================================================
+namespace ifmm {
+namespace {
+
+__global__ void __launch_bounds__(1024)
+panel_lu_kernel(double* A, int n, int lda, int j0, int jb, int* piv, int* status, int tag) {
+  __shared__ double red[32];
+  __shared__ long long redi[32];
+  __shared__ int s_p;
+  for (int j = j0; j < j0 + jb; ++j) {
+    double bv = -1.0;
+    long long bi = (1LL << 62);
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+      const double v = fabs(A[(size_t)i * lda + j]);
+      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    block_argmax(bv, bi, red, redi);
+    if (threadIdx.x == 0) {
+      const int p = (bi >= n || bi < j) ? j : (int)bi;
+      s_p = p;
+      piv[j] = p;
+      const double pv = A[(size_t)p * lda + j];
+      if (pv == 0.0 || !isfinite(pv)) atomicCAS(status, 0, tag + 1);
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != j)
+      for (int c = j0 + threadIdx.x; c < j0 + jb; c += blockDim.x) {
+        const double t = A[(size_t)j * lda + c];
+        A[(size_t)j * lda + c] = A[(size_t)p * lda + c];
+        A[(size_t)p * lda + c] = t;
+      }
+    __syncthreads();
+    const double pv = A[(size_t)j * lda + j];
+    const int rem_c = j0 + jb - j - 1;
+    if (pv != 0.0)
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+        double* row = A + (size_t)i * lda;
+        const double l = row[j] / pv;
+        row[j] = l;
+        const double* prow = A + (size_t)j * lda;
+        for (int c = 1; c <= rem_c; ++c) row[j + c] -= l * prow[j + c];
+      }
+    __syncthreads();
+  }
+}
+
+__global__ void laswp_kernel(double* A, int n, int lda, int j0, int jb, const int* piv) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ncols = n - jb;
+  if (t >= ncols) return;
+  const int c = t < j0 ? t : t + jb;
+  for (int j = j0; j < j0 + jb; ++j) {
+    const int p = piv[j];
+    if (p != j) {
+      const double x = A[(size_t)j * lda + c];
+      A[(size_t)j * lda + c] = A[(size_t)p * lda + c];
+      A[(size_t)p * lda + c] = x;
+    }
+  }
+}
+
+__global__ void trsm_lunit_kernel(const double* L, int ldl, int nb, double* X, int ldx,
+                                  int ncols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  for (int i = 1; i < nb; ++i) {
+    double s = X[(size_t)i * ldx + c];
+    const double* l = L + (size_t)i * ldl;
+    for (int j = 0; j < i; ++j) s = fma(-l[j], X[(size_t)j * ldx + c], s);
+    X[(size_t)i * ldx + c] = s;
+  }
+}
+
+__global__ void finite_kernel(const double* A, int n, int lda, int* status, int tag) {
+  const long long tot = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double v = A[(size_t)(e / n) * lda + (e % n)];
+    if (!isfinite(v)) atomicCAS(status, 0, tag + 1);
+  }
+}
+
+__global__ void __launch_bounds__(512)
+extend_kernel(double* NB, int m, int k, const double* G, int extra, double* NW, double thr,
+              double* work) {
+  __shared__ double red[32];
+  __shared__ double s_w;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* A = work;                      // col-major m x extra
+  double* tau = A + (size_t)m * extra;
+  double* Q = tau + extra;
+  for (long long e = threadIdx.x; e < (long long)m * extra; e += blockDim.x) A[e] = G[e];
+  double mx = 0.0;
+  for (int a = threadIdx.x; a < k; a += blockDim.x) mx = fmax(mx, NW[a]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t = fmax(t, red[w]);
+    s_w = fmax(thr, 1e-14 * (k ? t : 1.0));
+  }
+  __syncthreads();
+  // G -= B (B^T G), column by column (warp per column)
+  for (int c = warp; c < extra; c += nw) {
+    double* g = A + (size_t)c * m;
+    for (int a = 0; a < k; ++a) {
+      const double* b = NB + (size_t)a * m;
+      double d = 0.0;
+      for (int i = lane; i < m; i += 32) d = fma(b[i], G[(size_t)c * m + i], d);
+      d = warp_sum(d);
+      for (int i = lane; i < m; i += 32) g[i] -= d * b[i];
+    }
+  }
+  __syncthreads();
+  cta_geqrf(A, m, extra, m, tau, red);
+  cta_orgqr(A, m, extra, m, tau, Q, m);
+  __syncthreads();
+  for (long long e = threadIdx.x; e < (long long)m * extra; e += blockDim.x)
+    NB[(size_t)k * m + e] = Q[e];
+  for (int a = threadIdx.x; a < extra; a += blockDim.x) NW[k + a] = s_w;
+}
+
+}  // namespace
+
+void launch_panel_lu(double* A, int n, int lda, int j0, int jb, int* piv, int* status, int tag,
+                     cudaStream_t s) {
+  panel_lu_kernel<<<1, 1024, 0, s>>>(A, n, lda, j0, jb, piv, status, tag);
+}
+void launch_laswp(double* A, int n, int lda, int j0, int jb, const int* piv, cudaStream_t s) {
+  const int nc = n - jb;
+  if (nc <= 0) return;
+  laswp_kernel<<<(nc + 127) / 128, 128, 0, s>>>(A, n, lda, j0, jb, piv);
+}
+void launch_trsm_lunit(const double* L, int ldl, int nb, double* X, int ldx, int ncols,
+                       cudaStream_t s) {
+  if (ncols <= 0) return;
+  trsm_lunit_kernel<<<(ncols + 127) / 128, 128, 0, s>>>(L, ldl, nb, X, ldx, ncols);
+}
+void launch_finite_check(const double* A, int n, int lda, int* status, int tag, cudaStream_t s) {
+  finite_kernel<<<592, 256, 0, s>>>(A, n, lda, status, tag);
+}
+void launch_extend(double* NB, int m, int k, const double* G, int extra, double* NW, double thr,
+                   double* work, cudaStream_t s) {
+  extend_kernel<<<1, 512, 0, s>>>(NB, m, k, G, extra, NW, thr, work);
+}
+
+}  // namespace ifmm

@@ -1,0 +1,155 @@
+// Extended sparse graph assembly (graph.py:30-229) and sigma0 estimation
+// (graph.py:232-241 -> lowrank.py:79-119 with start_rank = max_rank = 1).
+#include <algorithm>
+
+#include "engine.h"
+#include "spmv.cuh"
+
+namespace ifmm {
+
+Graph::~Graph() {
+  if (!ctx) return;
+  for (auto& kv : E) ctx->free(kv.second);
+  for (auto& b : su) ctx->free(b);
+  for (auto& b : sv) ctx->free(b);
+  ctx->sync();
+  ctx->flush();
+}
+
+void Graph::build(H2* h) {
+  ops = h;
+  tree = h->tree;
+  ctx = h->ctx;
+  Ctx& C = *ctx;
+  Tree& T = *tree;
+  nx.assign(T.nc, -1); nz.assign(T.nc, -1); ny.assign(T.nc, -1);
+  dead.assign(T.nc, 0);
+  su.assign(T.nc, Blk()); sv.assign(T.nc, Blk());
+  for (int c : T.leaves()) nx[c] = new_node(T.stop[c] - T.start[c], NK_X, c);
+  for (int l = 2; l <= T.depth; ++l)
+    for (int c : T.levels[l]) {
+      nz[c] = new_node(h->rank[c], NK_Z, c);
+      ny[c] = new_node(h->rank[c], NK_Y, c);
+    }
+  CopyBatch cb;
+  auto dup = [&](const Blk& s) {
+    Blk b = C.alloc(s.r, s.c);
+    cb.add(s.p, s.c, 1, b.p, b.c, 1, s.r, s.c, 0);
+    return b;
+  };
+  auto dupT = [&](const Blk& s) {
+    Blk b = C.alloc(s.c, s.r);
+    cb.add(s.p, 1, s.c, b.p, b.c, 1, s.c, s.r, 0);
+    return b;
+  };
+  // graph.py:63-84
+  for (auto& kv : h->near) {
+    const int i = (int)(kv.first >> 32), j = (int)(kv.first & 0xffffffffu);
+    set(nx[i], nx[j], dup(kv.second));
+  }
+  if (T.depth >= 2)
+    for (int c : T.leaves()) {
+      set(nx[c], nz[c], dup(h->leaf_u[c]));
+      set(nz[c], nx[c], dupT(h->leaf_v[c]));
+    }
+  for (int l = 2; l <= T.depth; ++l)
+    for (int c : T.levels[l]) {
+      const int k = h->rank[c];
+      Blk a = C.alloc(k, k), b = C.alloc(k, k);
+      cb.eye(a, -1.0);
+      cb.eye(b, -1.0);
+      set(nz[c], ny[c], a);
+      set(ny[c], nz[c], b);
+      su[c] = dup(h->su[c]);
+      sv[c] = dup(h->sv[c]);
+    }
+  for (auto& kv : h->coupling) {
+    const int i = (int)(kv.first >> 32), j = (int)(kv.first & 0xffffffffu);
+    set(ny[i], ny[j], dup(kv.second));
+  }
+  for (int c = 0; c < T.nc; ++c)
+    if (h->tu[c].p) {
+      const int p = T.parent[c];
+      set(ny[c], nz[p], dup(h->tu[c]));
+      set(nz[p], ny[c], dup(h->tvt[c]));
+    }
+  cb.run(C);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// sigma0 = leading singular value of the extended matrix by the reference's
+// randomized SVD with one probe rank: Y = E omega; 2x Y = E E^T orth(Y);
+// Q = orth(Y); sigma_max((E^T Q)^T).
+// ---------------------------------------------------------------------------
+double Graph::sigma0(const double* omega, int width, int power_iters) {
+  Ctx& C = *ctx;
+  const int nn = (int)size.size();
+  std::vector<long long> off(nn + 1, 0);
+  for (int i = 0; i < nn; ++i) off[i + 1] = off[i] + size[i];
+  const long long dim = off[nn];
+  IFMM_ASSERT(dim < (1LL << 31), "extended dimension too large");
+  const int w = width;
+  Blk Om = C.alloc((int)dim, w), Y = C.alloc((int)dim, w), Z = C.alloc((int)dim, w);
+  Blk Q = C.alloc((int)dim, w);
+  Blk work = C.alloc(1, (int)(2 * dim * w + 4 * w * w + 64));
+  Blk out = C.alloc(1, 1);
+  CUDA_CHECK(cudaMemcpyAsync(Om.p, omega, sizeof(double) * dim * w, cudaMemcpyHostToDevice, C.st));
+  // row tasks for E and E^T (terms in sorted node order -> deterministic)
+  std::vector<SpmvRow> rE, rT;
+  std::vector<SpmvTerm> tE, tT;
+  auto build = [&](const double* in, double* outp) {
+    rE.clear(); tE.clear(); rT.clear(); tT.clear();
+    for (int t = 0; t < nn; ++t) {
+      SpmvRow r{outp + off[t] * w, size[t], (int)tE.size(), 0, 0};
+      for (int s : rows[t]) {
+        const Blk& B = E.at(key2(t, s));
+        tE.push_back({B.p, B.r, B.c, B.c, 0, in + off[s] * w});
+        r.nt++;
+      }
+      rE.push_back(r);
+    }
+  };
+  auto buildT = [&](const double* in, double* outp) {
+    rT.clear(); tT.clear();
+    for (int s = 0; s < nn; ++s) {
+      SpmvRow r{outp + off[s] * w, size[s], (int)tT.size(), 0, 0};
+      for (int t : cols[s]) {
+        const Blk& B = E.at(key2(t, s));
+        tT.push_back({B.p, B.r, B.c, B.c, 1, in + off[t] * w});
+        r.nt++;
+      }
+      rT.push_back(r);
+    }
+  };
+  auto applyE = [&](const double* in, double* outp) {
+    build(in, outp);
+    SpmvTerm* dt = C.stage.push_vec(C, tE);
+    SpmvRow* dr = C.stage.push_vec(C, rE);
+    launch_spmv(dr, (int)rE.size(), dt, w, w, C.st);
+  };
+  auto applyET = [&](const double* in, double* outp) {
+    buildT(in, outp);
+    SpmvTerm* dt = C.stage.push_vec(C, tT);
+    SpmvRow* dr = C.stage.push_vec(C, rT);
+    launch_spmv(dr, (int)rT.size(), dt, w, w, C.st);
+  };
+  applyE(Om.p, Y.p);
+  for (int it = 0; it < power_iters; ++it) {
+    launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
+    applyET(Q.p, Z.p);
+    applyE(Z.p, Y.p);
+  }
+  launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
+  applyET(Q.p, Z.p);
+  launch_tall_sigmax(Z.p, (int)dim, w, out.p, work.p, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  double s0 = 0.0;
+  CUDA_CHECK(cudaMemcpyAsync(&s0, out.p, sizeof(double), cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  for (Blk* b : {&Om, &Y, &Z, &Q, &work, &out}) C.free(*b);
+  C.flush();
+  return s0;
+}
+
+}  // namespace ifmm

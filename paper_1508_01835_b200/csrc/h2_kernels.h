@@ -1,0 +1,42 @@
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ifmm {
+
+enum KernelKind { KERNEL_EXP = 1, KERNEL_IMQ = 2, KERNEL_BENCH = 3, KERNEL_ZERO = 4 };
+constexpr int MAX_CHEB = 12;
+
+struct KernelSpec {
+  int kind;
+  double p0;  // IMQ: h, BENCH: d
+};
+
+// out(i,j) = K(|P_i - Q_j|), P: m x 3, Q: n x 3 (row-major), out ld ldo
+struct EvalDesc {
+  const double* P;
+  const double* Q;
+  int m, n;
+  double* out;
+  int ldo;
+};
+
+// out (count x nc^3, ld ldo) = interpolation matrix of pts in cell (c, hw)
+struct InterpDesc {
+  const double* pts;
+  int count;
+  double cx, cy, cz, hw;
+  double* out;
+  int ldo;
+};
+
+// out (nc^3 x 3) = Chebyshev grid of cell (c, hw)
+struct GridDesc {
+  double cx, cy, cz, hw;
+  double* out;
+};
+
+void launch_eval(const EvalDesc* d_descs, int n, const KernelSpec& k, cudaStream_t s);
+void launch_interp(const InterpDesc* d_descs, int n, int nc, cudaStream_t s);
+void launch_grid(const GridDesc* d_descs, int n, int nc, cudaStream_t s);
+
+}  // namespace ifmm

@@ -1,0 +1,169 @@
+// Host runtime of the IFMM engine: device arena, descriptor staging,
+// batched-launch helpers, error plumbing.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dense.h"
+#include "h2_kernels.h"
+
+namespace ifmm {
+
+// ---- errors ------------------------------------------------------------
+enum Status { OK = 0, E_VALUE = 1, E_SINGULAR = 2, E_CUDA = 3, E_OOM = 4, E_ASSERT = 5 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& s);
+
+#define CUDA_CHECK(x)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess)                                                             \
+      throw ::ifmm::Error(::ifmm::E_CUDA, std::string("CUDA error: ") +               \
+                                              cudaGetErrorString(_e) + " at " __FILE__); \
+  } while (0)
+
+#define IFMM_ASSERT(c, msg)                                              \
+  do {                                                                   \
+    if (!(c)) throw ::ifmm::Error(::ifmm::E_ASSERT, std::string(msg)); \
+  } while (0)
+
+// ---- device arena: size-class free lists over one cudaMalloc slab -------
+class Arena {
+ public:
+  void init(size_t bytes);
+  void release();
+  double* alloc(size_t ndoubles, int* cls);
+  int* alloc_int(size_t n, int* cls) { return reinterpret_cast<int*>(alloc((n + 1) / 2, cls)); }
+  void free(void* p, int cls);
+  size_t in_use() const { return in_use_; }
+  size_t peak() const { return peak_; }
+  size_t capacity() const { return cap_; }
+
+ private:
+  static int class_of(size_t bytes);
+  static size_t class_bytes(int cls);
+  char* base_ = nullptr;
+  size_t cap_ = 0, top_ = 0, in_use_ = 0, peak_ = 0;
+  std::vector<std::vector<char*>> bins_;
+};
+
+// ---- dense block handle (row-major r x c, ld = c) ------------------------
+struct Blk {
+  double* p = nullptr;
+  int r = 0, c = 0;
+  int cls = -1;
+  bool valid() const { return p != nullptr || (r * c == 0 && cls == -2); }
+};
+
+struct Ctx;
+
+// ---- pinned-host -> device descriptor ring --------------------------------
+class Staging {
+ public:
+  void init(size_t bytes);
+  void release();
+  // copy `bytes` from host memory into the ring; returns the device address
+  void* push(Ctx& ctx, const void* src, size_t bytes);
+  template <class T>
+  T* push_vec(Ctx& ctx, const std::vector<T>& v) {
+    return reinterpret_cast<T*>(push(ctx, v.data(), v.size() * sizeof(T)));
+  }
+
+ private:
+  char* h_ = nullptr;
+  char* d_ = nullptr;
+  size_t cap_ = 0, off_ = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  Arena arena;
+  Staging stage;
+  int* d_status = nullptr;   // singular-pivot flag (tag+1)
+  int* h_pinned_i = nullptr; // small pinned readback buffer
+  size_t h_pinned_n = 0;
+  long long launches = 0;
+
+  Blk alloc(int r, int c) {
+    Blk b;
+    b.r = r;
+    b.c = c;
+    size_t n = (size_t)r * c;
+    b.p = arena.alloc(n ? n : 1, &b.cls);
+    return b;
+  }
+  // Frees are deferred: a block released while a batch that references it
+  // is still being built must not be handed out again before that batch is
+  // enqueued.  flush() returns them to the arena at points where no batch
+  // is under construction (stream order then protects in-flight readers).
+  std::vector<std::pair<void*, int>> pending;
+  void free(Blk& b) {
+    if (b.p && b.cls >= 0) pending.emplace_back(b.p, b.cls);
+    b.p = nullptr;
+    b.cls = -1;
+  }
+  void free_raw(void* p, int cls) {
+    if (p && cls >= 0) pending.emplace_back(p, cls);
+  }
+  void flush() {
+    for (auto& q : pending) arena.free(q.first, q.second);
+    pending.clear();
+  }
+  void sync() { CUDA_CHECK(cudaStreamSynchronize(st)); }
+  // read back n ints from device (synchronizes)
+  const int* readback_ints(const int* d, size_t n);
+  void check_status(const char* what_prefix);
+};
+
+// ---- batched launch builders ---------------------------------------------
+struct GemmBatch {
+  std::vector<GemmDesc> d;
+  double flops = 0.0;
+  void add(const double* A, int lda, int ta, const double* B, int ldb, int tb, double* C,
+           int ldc, int M, int N, int K, double alpha, double beta,
+           const double* dscale = nullptr) {
+    if (M <= 0 || N <= 0) return;
+    GemmDesc g;
+    g.A = A; g.B = B; g.C = C; g.dscale = dscale;
+    g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
+    g.ta = ta; g.tb = tb; g.alpha = alpha; g.beta = beta;
+    d.push_back(g);
+    flops += 2.0 * M * N * (double)K;
+  }
+  void run(Ctx& ctx);
+  bool empty() const { return d.empty(); }
+};
+
+struct CopyBatch {
+  std::vector<CopyDesc> d;
+  void add(const double* src, int ss_r, int ss_c, double* dst, int ds_r, int ds_c, int rows,
+           int cols, int mode, double alpha = 1.0, const double* rscale = nullptr) {
+    if (rows <= 0 || cols <= 0) return;
+    CopyDesc c;
+    c.src = src; c.dst = dst; c.rows = rows; c.cols = cols;
+    c.ss_r = ss_r; c.ss_c = ss_c; c.ds_r = ds_r; c.ds_c = ds_c;
+    c.mode = mode; c.alpha = alpha; c.rscale = rscale;
+    d.push_back(c);
+  }
+  // convenience: row-major blocks
+  void copy(const Blk& s, Blk& t, int r0 = 0, int c0 = 0) {
+    add(s.p, s.c, 1, t.p + (size_t)r0 * t.c + c0, t.c, 1, s.r, s.c, 0);
+  }
+  void zero(Blk& t) { add(nullptr, 0, 0, t.p, t.c, 1, t.r, t.c, 3); }
+  void eye(Blk& t, double a) { add(nullptr, 0, 0, t.p, t.c, 1, t.r, t.c, 2, a); }
+  void run(Ctx& ctx);
+  bool empty() const { return d.empty(); }
+};
+
+}  // namespace ifmm

@@ -1,0 +1,474 @@
+// IFMMFactorization.solve (factor.py:99-157) as a device program.
+//
+// The event log (elim / rebase / merge) is compiled once, after the
+// factorization, into SSA "slots" in one workspace vector:
+//   * every rhs version of a node gets its own slot (a rebase writes a new
+//     version instead of overwriting), so only true dependencies remain;
+//   * merge events cost nothing: the final y versions of the children are
+//     allocated *inside* the parent's x slot (factor.py:123-126), and the
+//     final level-2 y versions inside the top-level rhs;
+//   * the backward solution slots alias the same way (factor.py:147-152).
+// Ops are levelled into dependency waves (read-after-write, write-after-
+// write, write-after-read on slots); each wave is one launch with one CTA
+// per op.  Updates to one slot stay in event order, so solves are bitwise
+// reproducible (reference test_factor.py:95-106).
+#include <algorithm>
+#include <map>
+
+#include "common.cuh"
+#include "engine.h"
+
+namespace ifmm {
+
+enum OpType { OP_FWD_ELIM = 0, OP_REBASE = 1, OP_BWD_ELIM = 2 };
+
+struct SolveOp {
+  int type;
+  int n, m, k;
+  const double* LU;
+  const int* piv;
+  const double* M;  // Tstk (fwd), Scat (bwd), r (rebase)
+  int ldm;
+  int list0, nlist;
+  long long a;      // fwd: rhs_x slot | rebase: in | bwd: rhs_x slot
+  long long b;      // fwd: rhs_y slot | rebase: out | bwd: sol_y slot
+  long long c;      // bwd: sol_x slot
+  long long d;      // bwd: sol_z slot
+  long long e;      // bwd: gather scratch
+  int rows;         // rebase: k_new ; fwd: total target rows
+  int cols;         // rebase: k_old ; bwd: Csrc
+};
+struct ListEnt {
+  long long slot;
+  int off, len;  // fwd: row offset in Tstk, height | bwd: col offset in Scat, width
+};
+
+struct Factor::Program {
+  Blk ops_d, list_d, work, perm_d;
+  std::vector<int> fwd_wave_start, bwd_wave_start;  // op index ranges per wave
+  int n_fwd = 0, n_bwd = 0;
+  long long top_rhs = 0, top_sol = 0;
+  int top_n = 0;
+  long long sol0 = 0;  // sol region of leaf x (N)
+  int max_n = 0;
+  int fwd_waves = 0, bwd_waves = 0;
+  std::vector<int> perm;
+};
+
+Factor::~Factor() {
+  if (!ctx) return;
+  for (auto& e : elims) {
+    ctx->free(e.LU); ctx->free(e.Scat); ctx->free(e.Tstk);
+    ctx->free_raw(e.piv, e.piv_cls);
+  }
+  for (auto& r : rebases) ctx->free(r.r);
+  ctx->free(top_lu);
+  if (top_piv) ctx->free_raw(top_piv, top_piv_cls);
+  if (prog) {
+    ctx->free(prog->ops_d); ctx->free(prog->list_d); ctx->free(prog->work);
+    ctx->free(prog->perm_d);
+    delete prog;
+  }
+  ctx->sync();
+  ctx->flush();
+}
+
+// ---------------------------------------------------------------------------
+// device side
+// ---------------------------------------------------------------------------
+namespace {
+
+// In-place LU solve of v (smem, length n) by one warp (warp 0 does the
+// serial pivots, lanes split every row dot product).
+__device__ void warp_lu_solve(const double* __restrict__ LU, const int* __restrict__ piv, int n,
+                              double* v) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  if (lane == 0)
+    for (int j = 0; j < n; ++j) {
+      const int p = piv[j];
+      if (p != j) { const double t = v[j]; v[j] = v[p]; v[p] = t; }
+    }
+  __syncwarp();
+  for (int i = 1; i < n; ++i) {
+    const double* L = LU + (size_t)i * n;
+    double s = 0.0;
+    for (int j = lane; j < i; j += 32) s = fma(L[j], v[j], s);
+    s = warp_sum(s);
+    if (lane == 0) v[i] -= s;
+    __syncwarp();
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    const double* U = LU + (size_t)i * n;
+    double s = 0.0;
+    for (int j = i + 1 + lane; j < n; j += 32) s = fma(U[j], v[j], s);
+    s = warp_sum(s);
+    if (lane == 0) v[i] = (v[i] - s) / U[i];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256)
+solve_wave_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists, int first,
+                  int count, double* __restrict__ W) {
+  extern __shared__ double v[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int oi = blockIdx.x; oi < count; oi += gridDim.x) {
+    const SolveOp op = ops[first + oi];
+    if (op.type == OP_REBASE) {
+      const double* in = W + op.a;
+      for (int i = warp; i < op.rows; i += nw) {
+        const double* r = op.M + (size_t)i * op.cols;
+        double s = 0.0;
+        for (int j = lane; j < op.cols; j += 32) s = fma(r[j], in[j], s);
+        s = warp_sum(s);
+        if (lane == 0) W[op.b + i] = s;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (op.type == OP_FWD_ELIM) {
+      // g = P^{-1} [rhs_x; 0]
+      for (int i = threadIdx.x; i < op.n; i += blockDim.x) v[i] = i < op.m ? W[op.a + i] : 0.0;
+      __syncthreads();
+      warp_lu_solve(op.LU, op.piv, op.n, v);
+      __syncthreads();
+      // rhs[a] -= T_a g[:m]  over all target rows
+      for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+        const ListEnt t = lists[l];
+        for (int i = warp; i < t.len; i += nw) {
+          const double* row = op.M + (size_t)(t.off + i) * op.ldm;
+          double s = 0.0;
+          for (int j = lane; j < op.m; j += 32) s = fma(row[j], v[j], s);
+          s = warp_sum(s);
+          if (lane == 0) W[t.slot + i] = W[t.slot + i] - s;
+        }
+      }
+      // rhs[ny] += g[m:]
+      for (int i = threadIdx.x; i < op.k; i += blockDim.x) W[op.b + i] = W[op.b + i] + v[op.m + i];
+      __syncthreads();
+      continue;
+    }
+    // OP_BWD_ELIM: gather sources' solutions into scratch
+    for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+      const ListEnt s = lists[l];
+      for (int j = threadIdx.x; j < s.len; j += blockDim.x) W[op.e + s.off + j] = W[s.slot + j];
+    }
+    __syncthreads();
+    const double* gsol = W + op.e;
+    for (int i = warp; i < op.m; i += nw) {
+      const double* row = op.M + (size_t)i * op.ldm;
+      double s = 0.0;
+      for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
+      s = warp_sum(s);
+      if (lane == 0) v[i] = W[op.a + i] - s;
+    }
+    for (int i = threadIdx.x; i < op.k; i += blockDim.x) v[op.m + i] = W[op.b + i];
+    __syncthreads();
+    warp_lu_solve(op.LU, op.piv, op.n, v);
+    __syncthreads();
+    for (int i = threadIdx.x; i < op.n; i += blockDim.x) {
+      if (i < op.m) W[op.c + i] = v[i];
+      else W[op.d + i - op.m] = v[i];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+top_solve_kernel(const double* LU, const int* piv, int n, const double* rhs, double* out) {
+  extern __shared__ double v[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = rhs[i];
+  __syncthreads();
+  warp_lu_solve(LU, piv, n, v);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v[i];
+}
+
+__global__ void gather_perm_kernel(const double* b, const int* perm, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = b[perm[i]];
+}
+__global__ void scatter_perm_kernel(const double* in, const int* perm, int n, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[perm[i]] = in[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side: compile the event log
+// ---------------------------------------------------------------------------
+void Factor::build_program(const std::vector<int>& final_size) {
+  (void)final_size;
+  Ctx& C = *ctx;
+  prog = new Program;
+  Program& P = *prog;
+  const int nnodes = (int)std::max(init_sizes.size(), final_size.size());
+  std::vector<int> nsize(nnodes, 0);
+  for (size_t i = 0; i < init_sizes.size(); ++i) nsize[i] = init_sizes[i];
+  for (auto& mv : merges) {
+    int s = 0;
+    for (int q : mv.psize) s += q;
+    nsize[mv.px] = s;
+  }
+  // ---- versions of y nodes ----
+  std::vector<int> nver(nnodes, 1);
+  for (auto& ev : events)
+    if (ev.type == 1) nver[rebases[ev.idx].ny]++;
+  // final-version alias targets
+  std::vector<long long> final_slot(nnodes, -1);
+  long long top = n_points;  // [0, N) leaf x slots
+  auto alloc = [&](long long n) { long long o = top; top += n; return o; };
+  // merged parents: region per px; parts alias final versions
+  std::vector<long long> xslot(nnodes, -1);
+  for (int t = 0; t < (int)leaf_nodes.size(); ++t) xslot[leaf_nodes[t]] = leaf_start[t];
+  for (auto& mv : merges) {
+    const long long o = alloc(nsize[mv.px]);
+    xslot[mv.px] = o;
+    long long off = 0;
+    for (size_t q = 0; q < mv.parts.size(); ++q) {
+      final_slot[mv.parts[q]] = o + off;
+      off += mv.psize[q];
+    }
+  }
+  P.top_n = 0;
+  for (int s : top_sizes) P.top_n += s;
+  // a top node is an x node only for depth < 2 (no elimination at all): the
+  // top system is then the leaf region itself
+  const bool top_is_x = !top_nodes.empty() && xslot[top_nodes[0]] >= 0;
+  P.top_rhs = top_is_x ? 0 : alloc(P.top_n);
+  if (!top_is_x) {
+    long long off = 0;
+    for (size_t q = 0; q < top_nodes.size(); ++q) {
+      final_slot[top_nodes[q]] = P.top_rhs + off;
+      off += top_sizes[q];
+    }
+  }
+  // version slots
+  std::vector<std::vector<long long>> vslot(nnodes);
+  std::vector<std::vector<int>> vsize(nnodes);
+  {
+    // sizes per version: v0 = init size; after each rebase = r rows
+    for (int i = 0; i < nnodes; ++i) vsize[i].push_back(nsize[i]);
+    for (auto& ev : events)
+      if (ev.type == 1) vsize[rebases[ev.idx].ny].push_back(rebases[ev.idx].r.r);
+    for (int i = 0; i < nnodes; ++i) {
+      if (xslot[i] >= 0) { vslot[i].push_back(xslot[i]); continue; }
+      for (int v = 0; v < nver[i]; ++v) {
+        const bool last = v == nver[i] - 1;
+        vslot[i].push_back(last && final_slot[i] >= 0 ? final_slot[i] : alloc(vsize[i][v]));
+      }
+    }
+  }
+  // ---- solution slots ----
+  std::vector<long long> sslot(nnodes, -1);
+  P.sol0 = alloc(n_points);
+  for (int t = 0; t < (int)leaf_nodes.size(); ++t) sslot[leaf_nodes[t]] = P.sol0 + leaf_start[t];
+  P.top_sol = top_is_x ? P.sol0 : alloc(P.top_n);
+  if (!top_is_x) {
+    long long off = 0;
+    for (size_t q = 0; q < top_nodes.size(); ++q) {
+      sslot[top_nodes[q]] = P.top_sol + off;
+      off += top_sizes[q];
+    }
+  }
+  // merged parents' sol regions (top-down so children alias inside)
+  for (int mi = (int)merges.size() - 1; mi >= 0; --mi) {
+    auto& mv = merges[mi];
+    if (sslot[mv.px] < 0) sslot[mv.px] = alloc(nsize[mv.px]);
+    long long off = 0;
+    for (size_t q = 0; q < mv.parts.size(); ++q) {
+      sslot[mv.parts[q]] = sslot[mv.px] + off;
+      off += mv.psize[q];
+    }
+  }
+  for (auto& E : elims) {
+    if (sslot[E.nz] < 0) sslot[E.nz] = alloc(E.k);
+    if (sslot[E.nx] < 0) sslot[E.nx] = alloc(E.m);
+  }
+
+  // ---- ops + dependency waves ----
+  std::vector<SolveOp> fops, bops;
+  std::vector<ListEnt> lists;
+  std::vector<int> fwave, bwave;
+  // resources: slot start offsets identify atomic slots; composite px slots
+  // are expanded to their parts via the merge table.
+  std::map<int, std::vector<long long>> comp;  // px -> child final slots
+  for (auto& mv : merges) {
+    std::vector<long long> v;
+    for (int q : mv.parts) v.push_back(final_slot[q]);
+    comp[mv.px] = v;
+  }
+  std::unordered_map<long long, int> lw, lr;  // last write wave / max read wave
+  auto res_of = [&](int node, long long slot, std::vector<long long>& out) {
+    auto it = comp.find(node);
+    if (it != comp.end()) { for (long long s : it->second) out.push_back(s); }
+    else out.push_back(slot);
+  };
+  auto wave_for = [&](const std::vector<long long>& rd, const std::vector<long long>& wr) {
+    int w = 0;
+    for (long long r : rd) { auto it = lw.find(r); if (it != lw.end()) w = std::max(w, it->second); }
+    for (long long r : wr) {
+      auto it = lw.find(r); if (it != lw.end()) w = std::max(w, it->second);
+      auto jt = lr.find(r); if (jt != lr.end()) w = std::max(w, jt->second);
+    }
+    w += 1;
+    for (long long r : rd) { int& x = lr[r]; x = std::max(x, w); }
+    for (long long r : wr) lw[r] = w;
+    return w;
+  };
+  std::vector<int> cur(nnodes, 0);
+  P.max_n = 0;
+  for (auto& ev : events) {
+    if (ev.type == 0) {
+      const ElimEv& E = elims[ev.idx];
+      SolveOp o{};
+      o.type = OP_FWD_ELIM;
+      o.n = E.m + E.k; o.m = E.m; o.k = E.k;
+      o.LU = E.LU.p; o.piv = E.piv; o.M = E.Tstk.p; o.ldm = E.m;
+      o.a = vslot[E.nx][cur[E.nx]];
+      o.b = vslot[E.ny][cur[E.ny]];
+      o.list0 = (int)lists.size(); o.nlist = (int)E.tgt.size();
+      std::vector<long long> rd, wr;
+      res_of(E.nx, o.a, rd);
+      wr.push_back(o.b);
+      for (size_t t = 0; t < E.tgt.size(); ++t) {
+        const int a = E.tgt[t];
+        const long long s = vslot[a][cur[a]];
+        lists.push_back({s, E.tgt_off[t], E.tgt_h[t]});
+        res_of(a, s, wr);
+      }
+      P.max_n = std::max(P.max_n, o.n);
+      fops.push_back(o);
+      fwave.push_back(wave_for(rd, wr));
+    } else if (ev.type == 1) {
+      const RebaseEv& R = rebases[ev.idx];
+      SolveOp o{};
+      o.type = OP_REBASE;
+      o.M = R.r.p; o.rows = R.r.r; o.cols = R.r.c;
+      o.a = vslot[R.ny][cur[R.ny]];
+      cur[R.ny]++;
+      o.b = vslot[R.ny][cur[R.ny]];
+      fops.push_back(o);
+      fwave.push_back(wave_for({o.a}, {o.b}));
+    }
+  }
+  // sanity: final versions reached the aliased slots
+  for (auto& mv : merges)
+    for (int q : mv.parts) IFMM_ASSERT(vslot[q][cur[q]] == final_slot[q], "merge alias broken");
+  lw.clear(); lr.clear();
+  std::map<int, std::vector<long long>> comp_sol;
+  for (auto& mv : merges) {
+    std::vector<long long> v;
+    for (int q : mv.parts) v.push_back(sslot[q]);
+    comp_sol[mv.px] = v;
+  }
+  auto res_sol = [&](int node, std::vector<long long>& out) {
+    auto it = comp_sol.find(node);
+    if (it != comp_sol.end()) { for (long long s : it->second) out.push_back(s); }
+    else out.push_back(sslot[node]);
+  };
+  long long scratch = 0;
+  std::vector<long long> bscr;
+  for (int ei = (int)events.size() - 1; ei >= 0; --ei) {
+    const Event& ev = events[ei];
+    if (ev.type != 0) continue;
+    const ElimEv& E = elims[ev.idx];
+    SolveOp o{};
+    o.type = OP_BWD_ELIM;
+    o.n = E.m + E.k; o.m = E.m; o.k = E.k;
+    o.LU = E.LU.p; o.piv = E.piv; o.M = E.Scat.p; o.ldm = E.Scat.c;
+    o.a = vslot[E.nx][0];
+    o.b = sslot[E.ny];
+    o.c = sslot[E.nx];
+    o.d = sslot[E.nz];
+    int csrc = 0;
+    for (int w : E.src_w) csrc += w;
+    o.cols = csrc;
+    o.list0 = (int)lists.size(); o.nlist = (int)E.src.size();
+    std::vector<long long> rd, wr;
+    rd.push_back(o.b);
+    for (size_t t = 0; t < E.src.size(); ++t) {
+      const int b = E.src[t];
+      lists.push_back({sslot[b], E.src_off[t], E.src_w[t]});
+      res_sol(b, rd);
+    }
+    res_sol(E.nx, wr);  // a px's solution slots are its children's y slots
+    wr.push_back(o.d);
+    o.e = -1;
+    bscr.push_back(csrc);
+    bops.push_back(o);
+    bwave.push_back(wave_for(rd, wr));
+    scratch = std::max<long long>(scratch, csrc);
+  }
+  // gather scratch: one region per op (ops of one wave run concurrently)
+  for (size_t i = 0; i < bops.size(); ++i) bops[i].e = alloc(std::max<long long>(bscr[i], 1));
+  const long long wtot = top;
+
+  // ---- sort ops by wave ----
+  auto order_by = [](const std::vector<int>& wv, std::vector<int>& starts) {
+    std::vector<int> idx(wv.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return wv[a] < wv[b]; });
+    starts.clear();
+    int last = -1;
+    for (size_t i = 0; i < idx.size(); ++i)
+      if (wv[idx[i]] != last) { starts.push_back((int)i); last = wv[idx[i]]; }
+    starts.push_back((int)idx.size());
+    return idx;
+  };
+  auto fi = order_by(fwave, P.fwd_wave_start);
+  auto bi = order_by(bwave, P.bwd_wave_start);
+  std::vector<SolveOp> all;
+  for (int i : fi) all.push_back(fops[i]);
+  for (int i : bi) all.push_back(bops[i]);
+  P.n_fwd = (int)fops.size();
+  P.n_bwd = (int)bops.size();
+  P.fwd_waves = (int)P.fwd_wave_start.size() - 1;
+  P.bwd_waves = (int)P.bwd_wave_start.size() - 1;
+  const size_t ob = all.size() * sizeof(SolveOp), lb = lists.size() * sizeof(ListEnt);
+  P.ops_d = C.alloc(1, (int)(ob / 8 + 1));
+  P.list_d = C.alloc(1, (int)(lb / 8 + 1));
+  if (ob) CUDA_CHECK(cudaMemcpyAsync(P.ops_d.p, all.data(), ob, cudaMemcpyHostToDevice, C.st));
+  if (lb) CUDA_CHECK(cudaMemcpyAsync(P.list_d.p, lists.data(), lb, cudaMemcpyHostToDevice, C.st));
+  P.work = C.alloc(1, (int)std::max<long long>(wtot, 1));
+  C.sync();  // host vectors die here
+}
+
+void Factor::solve(const double* d_b, double* d_x) {
+  Ctx& C = *ctx;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(solve_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(top_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  IFMM_ASSERT(prog->top_n <= 25000 && prog->max_n <= 25000, "solve vector exceeds shared memory");
+  Program& P = *prog;
+  const int N = n_points;
+  double* W = P.work.p;
+  const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
+  CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, C.st));
+  gather_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(d_b, d_perm, N, W);
+  const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
+  const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
+  const size_t smem = (size_t)std::max(P.max_n, 1) * sizeof(double);
+  for (int w = 0; w < P.fwd_waves; ++w) {
+    const int a = P.fwd_wave_start[w], b = P.fwd_wave_start[w + 1];
+    solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
+  }
+  if (P.top_n > 0) {
+    top_solve_kernel<<<1, 1024, (size_t)P.top_n * sizeof(double), C.st>>>(
+        top_lu.p, top_piv, P.top_n, W + P.top_rhs, W + P.top_sol);
+  }
+  for (int w = 0; w < P.bwd_waves; ++w) {
+    const int a = P.n_fwd + P.bwd_wave_start[w], b = P.n_fwd + P.bwd_wave_start[w + 1];
+    solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
+  }
+  scatter_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(W + P.sol0, d_perm, N, d_x);
+  C.launches += 3 + P.fwd_waves + P.bwd_waves;
+  CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace ifmm

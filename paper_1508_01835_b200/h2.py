@@ -1,0 +1,149 @@
+"""H2 operators on the device (mirror of ``ifmm.h2``).
+
+``chebyshev_operators`` (h2.py:104-182) and ``initialize_weights``
+(h2.py:185-231, rigorous mode) run entirely in the CUDA engine; the
+returned ``H2Operators`` holds the device handle.  The dict-of-blocks
+attributes of the reference (``leaf_u``, ``coupling``, ``near`` ...) are
+read-only views that copy one block to the host on access (tests and
+inspection only).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections.abc import Mapping
+
+import numpy as np
+
+from . import _native as N
+from .kernels import Kernel
+from .tree import ClusterTopology, Octree
+
+_WHICH = {"leaf_u": 0, "leaf_v": 1, "transfer_u": 2, "transfer_vt": 3, "coupling": 4,
+          "near": 5, "sigma_u": 6, "sigma_v": 7}
+
+
+class _BlockView(Mapping):
+    def __init__(self, ops, which, keys):
+        self._ops, self._w, self._keys = ops, which, keys
+
+    def _fetch(self, key):
+        i, j = key if isinstance(key, tuple) else (key, 0)
+        r, c = C.c_int(), C.c_int()
+        h = self._ops._h
+        N.check(N.lib().ifmm_h2_block(h, self._w, int(i), int(j), None, C.byref(r), C.byref(c)))
+        if r.value < 0:
+            raise KeyError(key)
+        out = np.empty((r.value, c.value))
+        N.check(N.lib().ifmm_h2_block(h, self._w, int(i), int(j), N.as_dp(out), C.byref(r),
+                                      C.byref(c)))
+        return out[0] if self._w in (6, 7) else out
+
+    def __getitem__(self, key):
+        if key not in self._keys:
+            raise KeyError(key)
+        return self._fetch(key)
+
+    def __iter__(self):
+        return iter(self._keys)
+
+    def __len__(self):
+        return len(self._keys)
+
+    def __contains__(self, key):
+        return key in self._keys
+
+
+class H2Operators:
+    """Device-resident operators; attribute views mirror h2.py:76-101."""
+
+    def __init__(self, tree: Octree, topology: ClusterTopology, kernel: Kernel, n_cheb: int,
+                 handle):
+        self.tree, self.topology, self.kernel, self.n_cheb = tree, topology, kernel, n_cheb
+        self._h = handle
+        self._tree_handle = tree.handle()  # keep the device tree alive
+        nc = tree.n_clusters
+        r = np.zeros(nc, dtype=np.int32)
+        N.check(N.lib().ifmm_h2_ranks(handle, N.as_ip(r)))
+        self.rank = {c: int(r[c]) for c in range(nc) if r[c] >= 0}
+        self._weighted = False
+
+    def __del__(self):
+        try:
+            N.lib().ifmm_h2_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def block_dim(self):
+        return self.kernel.block_dim
+
+    @property
+    def dim(self):
+        return self.tree.n_points * self.kernel.block_dim
+
+    def max_rank(self):
+        return max(self.rank.values()) if self.rank else 0
+
+    # ---- reference-shaped read-only views ----
+    def _leaf_keys(self):
+        return self.tree.leaves() if self.tree.depth >= 2 else []
+
+    @property
+    def leaf_u(self):
+        return _BlockView(self, 0, set(self._leaf_keys()))
+
+    @property
+    def leaf_v(self):
+        return _BlockView(self, 1, set(self._leaf_keys()))
+
+    @property
+    def transfer_u(self):
+        cl = self.tree.clusters
+        return _BlockView(self, 2, {c for c in range(len(cl)) if cl[c].level >= 3})
+
+    @property
+    def transfer_vt(self):
+        cl = self.tree.clusters
+        return _BlockView(self, 3, {c for c in range(len(cl)) if cl[c].level >= 3})
+
+    @property
+    def coupling(self):
+        keys = {(i, j) for lv in range(2, self.tree.depth + 1) for i in self.tree.levels[lv]
+                for j in self.topology.interactions[i]}
+        return _BlockView(self, 4, keys)
+
+    @property
+    def near(self):
+        keys = {(i, j) for i in self.tree.leaves() for j in self.topology.neighbors[i]}
+        return _BlockView(self, 5, keys)
+
+    @property
+    def sigma_u(self):
+        return _BlockView(self, 6, set(self.rank) if self._weighted else set())
+
+    @property
+    def sigma_v(self):
+        return _BlockView(self, 7, set(self.rank) if self._weighted else set())
+
+
+def chebyshev_operators(tree: Octree, topology: ClusterTopology, kernel: Kernel, n: int,
+                        epsilon: float = 0.0) -> H2Operators:
+    """h2.py:104-182 on the device."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    kind, p0 = kernel.device_spec()
+    h = N.lib().ifmm_h2_build(tree.handle().h, kind, p0, int(n), float(epsilon))
+    return H2Operators(tree, topology, kernel, n, N.check_handle(h))
+
+
+def initialize_weights(ops: H2Operators, topology: ClusterTopology, mode: str = "rigorous",
+                       sample_size: int = 64, seed: int = 0) -> H2Operators:
+    """h2.py:185-231 (rigorous mode) on the device, in place."""
+    if mode not in ("rigorous", "sampled"):
+        raise ValueError("mode must be 'rigorous' or 'sampled'")
+    if mode == "sampled":
+        raise ValueError("sampled weights are not implemented by the engine (rigorous only)")
+    N.check(N.lib().ifmm_h2_weights(ops._h))
+    ops._weighted = True
+    return ops

@@ -1,0 +1,136 @@
+"""FMM matvec and GMRES (mirror of ``ifmm.krylov``).
+
+``h2_matvec`` (krylov.py:119-159) runs on the device (deterministic
+block-sparse products).  ``gmres`` (krylov.py:32-116) is the reference's
+non-restarted MGS/Givens loop written against an array namespace, so it
+runs on numpy arrays or on CUDA torch tensors (``apply_A`` / ``precond``
+decide where the vectors live).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .h2 import H2Operators
+
+
+@dataclass
+class IterationTrace:
+    residual_history: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    side: str = "none"
+
+
+def h2_matvec(ops: H2Operators, x):
+    """krylov.py:119-159 on the device; numpy or CUDA torch in, same out."""
+    try:
+        import torch
+        is_t = isinstance(x, torch.Tensor)
+    except Exception:
+        is_t = False
+    if is_t:
+        if x.shape != (ops.dim,):
+            raise ValueError("vector length mismatch")
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        torch.cuda.current_stream().synchronize()
+        N.check(N.lib().ifmm_h2_matvec(ops._h, C.c_void_p(x.data_ptr()),
+                                       C.c_void_p(y.data_ptr()), 1))
+        return y
+    x = np.ascontiguousarray(np.asarray(x, dtype=float))
+    if len(x) != ops.dim:
+        raise ValueError("vector length mismatch")
+    y = np.empty_like(x)
+    N.check(N.lib().ifmm_h2_matvec(ops._h, x.ctypes.data_as(C.c_void_p),
+                                   y.ctypes.data_as(C.c_void_p), 0))
+    return y
+
+
+def gmres(apply_A, b, tol: float = 1e-10, max_iters: int = 500, precond=None,
+          side: str = "right"):
+    """krylov.py:32-116 (MGS Arnoldi + Givens least squares)."""
+    if tol <= 0 or max_iters < 1:
+        raise ValueError("tol must be > 0 and max_iters >= 1")
+    if precond is None:
+        side = "none"
+    if side not in ("left", "right", "none"):
+        raise ValueError("side must be 'left', 'right', or 'none'")
+    trace = IterationTrace(side=side)
+    try:
+        import torch
+        is_t = isinstance(b, torch.Tensor)
+    except Exception:
+        is_t = False
+    if is_t:
+        def dot(u, v): return float(torch.dot(u, v))
+        def norm(u): return float(torch.linalg.vector_norm(u))
+        zeros = lambda n: torch.zeros(n, dtype=b.dtype, device=b.device)  # noqa: E731
+    else:
+        b = np.asarray(b, dtype=float)
+        def dot(u, v): return float(u @ v)
+        def norm(u): return float(np.linalg.norm(u))
+        zeros = lambda n: np.zeros(n)  # noqa: E731
+    n = len(b)
+    r0 = precond(b) if side == "left" else b
+    beta = norm(r0)
+    if beta == 0.0:
+        trace.converged = True
+        return zeros(n), trace
+    V = [r0 / beta]
+    H = np.zeros((max_iters + 1, max_iters))
+    cs, sn = np.zeros(max_iters), np.zeros(max_iters)
+    g = np.zeros(max_iters + 1)
+    g[0] = beta
+    k_done, breakdown = 0, False
+    for k in range(max_iters):
+        if side == "right":
+            w = apply_A(precond(V[k]))
+        elif side == "left":
+            w = precond(apply_A(V[k]))
+        else:
+            w = apply_A(V[k])
+        for i in range(k + 1):
+            H[i, k] = dot(V[i], w)
+            w = w - H[i, k] * V[i]
+        h_sub = norm(w)
+        H[k + 1, k] = h_sub
+        for i in range(k):
+            h0 = cs[i] * H[i, k] + sn[i] * H[i + 1, k]
+            H[i + 1, k] = -sn[i] * H[i, k] + cs[i] * H[i + 1, k]
+            H[i, k] = h0
+        nu = np.hypot(H[k, k], H[k + 1, k])
+        if nu == 0.0:
+            k_done, breakdown = k, True
+            break
+        cs[k], sn[k] = H[k, k] / nu, H[k + 1, k] / nu
+        H[k, k], H[k + 1, k] = nu, 0.0
+        g[k + 1] = -sn[k] * g[k]
+        g[k] = cs[k] * g[k]
+        rel = abs(g[k + 1]) / beta
+        trace.residual_history.append(float(rel))
+        k_done = k + 1
+        if rel <= tol:
+            trace.converged = True
+            break
+        if h_sub == 0.0:
+            breakdown = True
+            break
+        V.append(w / h_sub)
+    if breakdown and trace.residual_history:
+        trace.converged = trace.residual_history[-1] <= tol
+    k = k_done
+    x = zeros(n)
+    if k > 0:
+        import scipy.linalg as sla
+        y = sla.solve_triangular(H[:k, :k], g[:k])
+        u = zeros(n)
+        for i in range(k):
+            u = u + float(y[i]) * V[i]
+        x = precond(u) if side == "right" else u
+    trace.iterations = k
+    return x, trace
