@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""IFMM factorize+solve benchmark (BASELINE.json metric: unknowns/s).
+
+A "step" = one pass of the hot path over the synthetic problem: sigma0
+estimation + factorize (factor.py:176-230) + one solve (factor.py:99-157),
+exactly what the reference's unknowns/s covers.  Setup --
+points, octree, H2 operators, weights, and the per-step extended-graph
+assembly (factorize consumes its graph) -- is outside the timed region.
+
+  value  : N * K / (device time of K steps), rhs and solution resident on
+           the GPU (CUDA events on the engine stream, max over ranks)
+  e2e    : same, but every step's solve goes through the public API with a
+           HOST numpy rhs (h2d of b and d2h of x inside the timed region)
+  roofline : dominant device kernel category of one extra instrumented step
+  cpu_baseline : the numpy oracle port on a bounded same-recipe sample
+
+`--impl reference` times the CPU reference path (the oracle port of the
+reference; the unmodified reference is Python and not installable on the
+GPU box) on a bounded sample, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# SURVEY.md 8d pinned recipes: (N, dim, seed, kernel, leaf, n_cheb, eps)
+CONFIGS = {
+    "c1": (4096, 2, 0, "exp", 32, 4, 1e-8),
+    "c2": (65536, 2, 1, "exp", 64, 6, 1e-10),
+    "c3": (262144, 3, 2, "imq", 64, 4, 1e-6),
+    "c4": (1048576, 3, 3, "imq", 64, 4, 1e-6),
+}
+DEFAULT_CONFIG = "c2"
+METRIC = "IFMM factorize+solve unknowns/s"
+# CPU sample sizes for the oracle leg (about 10-30 s of single-core work)
+CPU_SAMPLE_N = {"c1": 4096, "c2": 8192, "c3": 4096, "c4": 4096}
+
+
+def inputs(cfg, n=None):
+    N, dim, seed, kern, leaf, nc, eps = CONFIGS[cfg]
+    N = n or N
+    g = np.random.Generator(np.random.PCG64(seed))
+    if dim == 2:
+        pts = np.column_stack([g.uniform(0.0, 1.0, size=(N, 2)), np.zeros(N)])
+    else:
+        pts = g.uniform(0.0, 1.0, size=(N, 3))
+    gb = np.random.Generator(np.random.PCG64(seed + 1))
+    b = gb.uniform(-1.0, 1.0, N) if dim == 2 else gb.standard_normal(N)
+    h = N ** (-1.0 / 3.0)
+    return dict(N=N, pts=pts, b=b, kern=kern, h=h, leaf=leaf, nc=nc, eps=eps, dim=dim)
+
+
+def workload_desc(cfg, inp):
+    return {"workload": f"{cfg}: {inp['dim']}D N={inp['N']} {inp['kern']}"
+                        f"{' h=N^-1/3' if inp['kern'] == 'imq' else ''}, leaf<= {inp['leaf']}, "
+                        f"{inp['nc']}^3 Chebyshev, eps={inp['eps']:g}, fp64",
+            "N": inp["N"], "epsilon": inp["eps"], "l2": "inputs >> L2 (graph blocks GBs)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = checker / reported baseline only)
+# ---------------------------------------------------------------------------
+def cpu_oracle_rate(cfg, threads):
+    from threadpoolctl import threadpool_limits
+    from oracle import ifmm_np as O
+    n = CPU_SAMPLE_N[cfg]
+    inp = inputs(cfg, n)
+    block = O.exp_block if inp["kern"] == "exp" else O.imq_block(inp["h"])
+    with threadpool_limits(limits=threads):
+        tree, topo, ops = O.pipeline(inp["pts"], block, inp["leaf"], inp["nc"], inp["eps"])
+        g = O.Graph(ops)
+        t0 = time.perf_counter()
+        f = O.factorize(g, inp["eps"], seed=0)
+        x = f.solve(inp["b"])
+        dt = time.perf_counter() - t0
+    del x
+    sample = (f"oracle numpy port of the reference path, {cfg} recipe at N={n} "
+              f"(sigma0+factorize+solve {dt:.2f} s)")
+    return n / dt, dt, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = args.config
+    threads = os.cpu_count() or 1
+    times = []
+    n = CPU_SAMPLE_N[cfg]
+    for i in range(args.warmup + args.steps):
+        rate, dt, sample = cpu_oracle_rate(cfg, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    val = n * len(times) / tot
+    inp = inputs(cfg)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / max(len(times), 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(cfg, inp),
+            "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, dev):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for ln in open(self.f.name):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) >= 7 and parts[0].isdigit():
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [int(r[0]) for r in rows]
+        load = [s for s in sm if s > 500] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": int(rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def fp64_peak_tflops():
+    """cuBLAS DGEMM 8192^3 best of 5 (MEASURED_PEAKS.json has no fp64 entry)."""
+    import torch
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) * 1e-3)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * 8192 ** 3 / best / 1e12
+
+
+def run_ours(args, rank, world):
+    import torch
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    import paper_1508_01835_b200 as P
+    from paper_1508_01835_b200 import _native as NN
+
+    fp64_peak = fp64_peak_tflops() if rank == 0 else None
+    cfg = args.config
+    inp = inputs(cfg, args.n)
+    N = inp["N"]
+    K = P.exp_kernel() if inp["kern"] == "exp" else P.imq_kernel(inp["h"])
+    t0 = time.perf_counter()
+    tree, _ = P.build_octree(inp["pts"], inp["leaf"])
+    topo = P.compute_topology(tree)
+    ops = P.chebyshev_operators(tree, topo, K, inp["nc"], epsilon=inp["eps"])
+    P.initialize_weights(ops, topo)
+    t_setup = time.perf_counter() - t0
+    b_host = np.ascontiguousarray(inp["b"])
+    b_dev = torch.from_numpy(b_host).cuda()
+
+    def one_step(host_rhs: bool, timed: bool):
+        graph = P.assemble_extended_graph(ops)
+        NN.lib().ifmm_dev_sync(NN.ctx())
+        NN.event(0)
+        s0 = P.estimate_sigma0(graph, seed=0)
+        fct = P.factorize(graph, inp["eps"], seed=0, sigma0=s0)
+        NN.event(1)
+        x = fct.solve(b_host if host_rhs else b_dev)
+        NN.event(2)
+        t_f = NN.elapsed_ms(0, 1) * 1e-3
+        t_s = NN.elapsed_ms(1, 2) * 1e-3
+        return t_f, t_s, fct, x
+
+    for _ in range(args.warmup):
+        one_step(False, False)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(torch.cuda.current_device()) if rank == 0 else None
+    l0 = NN.launches()
+    tf, ts, tsh = [], [], []
+    for _ in range(args.steps):
+        a, b_, fct, x = one_step(False, True)
+        # e2e: the same factorization's solve through the public API on host
+        NN.event(3)
+        xh = fct.solve(b_host)
+        NN.event(4)
+        tf.append(a)
+        ts.append(b_)
+        tsh.append(NN.elapsed_ms(3, 4) * 1e-3)
+        del fct, x, xh
+    launches = NN.launches() - l0
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    tot_dev = sum(tf) + sum(ts)
+    tot_e2e = sum(tf) + sum(tsh)
+    if world > 1:
+        t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_dev, tot_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    # ---- instrumented step for the kernel roofline ----
+    NN.ktime(1)
+    _, _, fct, x = one_step(False, False)
+    kt = NN.ktime(0)
+    res = float(np.linalg.norm(P.h2_matvec(ops, x.cpu().numpy()) - b_host) /
+                np.linalg.norm(b_host))
+    del fct, x
+    dom = max(kt.items(), key=lambda kv: kv[1][0])
+    cat, (ksec, kwork, kcnt) = dom
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    if cat in ("solve", "copy", "spmv"):
+        ach = kwork / ksec / 1e9 if ksec > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": cat, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        ach = kwork / ksec / 1e12 if ksec > 0 else 0.0
+        roof = {"bound": "tensor", "kernel": cat, "achieved": ach, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured in this run"}
+    roof["launches"] = kcnt
+    roof["avg_launch_ms"] = 1e3 * ksec / max(kcnt, 1)
+    roof["categories"] = {k: {"s": round(v[0], 4), "work": v[1], "n": v[2]}
+                          for k, v in kt.items() if v[2]}
+    # ---- CPU baseline (oracle port, bounded sample) ----
+    cpu_rate, cpu_dt, sample = cpu_oracle_rate(cfg, 1)
+    value = N * args.steps * world / tot_dev
+    e2e = N * args.steps * world / tot_e2e
+    line = {"metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_dev / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md 8d seeded recipe)",
+            "config": dict(workload_desc(cfg, inp), parallelism=f"replicas{world}"),
+            "e2e": {"value": e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": {"value": cpu_rate, "unit": "unknowns/s", "cores": 1,
+                             "kind": "port", "sample": sample},
+            "clocks": clk,
+            "detail": {"t_factorize_s": statistics.mean(tf), "t_solve_dev_s": statistics.mean(ts),
+                       "t_solve_host_s": statistics.mean(tsh), "t_setup_s": t_setup,
+                       "rel_residual_h2": res,
+                       "fp64_dgemm_tflops": fp64_peak}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override N (diagnostics)")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

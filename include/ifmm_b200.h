@@ -107,6 +107,19 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
                    const double* F, const double* wf, double thr, int min_rank,
                    double* NB, double* NW, double* OM, double* FM, int* rank);
 int ifmm_dev_sync(void* ctx);
+/* Device timing on the engine stream: record event `slot` (0..63); elapsed
+ * milliseconds between two recorded slots (waits for the second). */
+int ifmm_ctx_event(void* ctx, int slot);
+int ifmm_ctx_elapsed(void* ctx, int a, int b, double* ms);
+/* Number of engine kernel launches issued on the context so far. */
+long long ifmm_ctx_launches(void* ctx);
+/* Per-category kernel timing (categories: gemm, copy, svd, union, lu,
+ * lusolve, spmv, solve, other).  Reads the accumulated totals (seconds,
+ * algorithmic work = flops or bytes, launch count); enable >= 0 also resets
+ * and switches timing on (1) or off (0). */
+int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* count, int n);
+/* Diagnostics: phase times (s) of the last factorize when IFMM_PROFILE=1. */
+int ifmm_profile(double* out, int n);
 
 #ifdef __cplusplus
 }

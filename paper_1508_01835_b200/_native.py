@@ -51,6 +51,11 @@ _SIGS = {
     "ifmm_factor_level_ranks": (C.c_int, [vp, C.c_int, ip]),
     "ifmm_factor_timings": (C.c_int, [vp, dp, C.c_int]),
     "ifmm_solve": (C.c_int, [vp, vp, vp, C.c_int]),
+    "ifmm_profile": (C.c_int, [dp, C.c_int]),
+    "ifmm_ctx_event": (C.c_int, [vp, C.c_int]),
+    "ifmm_ctx_elapsed": (C.c_int, [vp, C.c_int, C.c_int, dp]),
+    "ifmm_ctx_launches": (C.c_longlong, [vp]),
+    "ifmm_ktime": (C.c_int, [vp, C.c_int, dp, dp, lp, C.c_int]),
     "ifmm_dev_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                 C.c_int, vp, C.c_int, C.c_double, C.c_double]),
     "ifmm_dev_svd": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_double, vp, vp, vp, vp]),
@@ -169,3 +174,39 @@ def as_ip(a: np.ndarray):
 
 def as_lp(a: np.ndarray):
     return a.ctypes.data_as(lp)
+
+
+PROFILE_PHASES = ("lu", "xsolve", "schur", "add", "fillsvd", "union", "rebase", "newk", "merge",
+                  "top", "host")
+
+
+def profile():
+    """Phase times of the last factorize (only populated with IFMM_PROFILE=1)."""
+    out = np.zeros(len(PROFILE_PHASES))
+    lib().ifmm_profile(as_dp(out), len(out))
+    return dict(zip(PROFILE_PHASES, out.tolist()))
+
+
+KCATS = ("gemm", "copy", "svd", "union", "lu", "lusolve", "spmv", "solve", "other")
+
+
+def event(slot: int):
+    check(lib().ifmm_ctx_event(ctx(), slot))
+
+
+def elapsed_ms(a: int, b: int) -> float:
+    out = C.c_double()
+    check(lib().ifmm_ctx_elapsed(ctx(), a, b, C.byref(out)))
+    return out.value
+
+
+def launches() -> int:
+    return int(lib().ifmm_ctx_launches(ctx()))
+
+
+def ktime(enable: int = -1):
+    """Per-category device kernel time / work / count; enable>=0 resets."""
+    t, w = np.zeros(16), np.zeros(16)
+    n = np.zeros(16, dtype=np.int64)
+    lib().ifmm_ktime(ctx(), enable, as_dp(t), as_dp(w), as_lp(n), 16)
+    return {k: (float(t[i]), float(w[i]), int(n[i])) for i, k in enumerate(KCATS)}

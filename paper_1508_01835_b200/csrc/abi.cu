@@ -10,6 +10,7 @@ using namespace ifmm;
 
 namespace ifmm {
 const char* last_error_cstr();
+extern double g_prof[];
 }
 
 #define ABI_TRY try {
@@ -363,6 +364,49 @@ int ifmm_factor_timings(void* p, double* out, int n) {
   return 0;
 }
 
+int ifmm_ctx_event(void* ctx, int slot) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  if (slot < 0 || slot >= 64) throw Error(E_VALUE, "event slot out of range");
+  if (!C.ev[slot]) CUDA_CHECK(cudaEventCreate(&C.ev[slot]));
+  CUDA_CHECK(cudaEventRecord(C.ev[slot], C.st));
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_ctx_elapsed(void* ctx, int a, int b, double* ms) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  CUDA_CHECK(cudaEventSynchronize(C.ev[b]));
+  float f = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&f, C.ev[a], C.ev[b]));
+  *ms = f;
+  return 0;
+  ABI_CATCH
+}
+
+long long ifmm_ctx_launches(void* ctx) { return ((Ctx*)ctx)->launches; }
+
+int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* count, int n) {
+  Ctx& C = *(Ctx*)ctx;
+  C.kt_collect();
+  for (int i = 0; i < n && i < 16; ++i) {
+    if (time_s) time_s[i] = C.ktime[i];
+    if (work) work[i] = C.kwork[i];
+    if (count) count[i] = C.kcount[i];
+  }
+  if (enable >= 0) {
+    C.ktime_on = enable != 0;
+    for (int i = 0; i < 16; ++i) { C.ktime[i] = 0; C.kwork[i] = 0; C.kcount[i] = 0; }
+  }
+  return 0;
+}
+
+int ifmm_profile(double* out, int n) {
+  for (int i = 0; i < n && i < 11; ++i) out[i] = ifmm::g_prof[i];
+  return 0;
+}
+
 int ifmm_solve(void* p, const double* b, double* x, int on_device) {
   ABI_TRY
   Factor* f = (Factor*)p;
@@ -422,7 +466,7 @@ int ifmm_dev_lu_solve(void* ctx, int n, double* A, int* piv, double* X, int nrhs
   std::vector<LuSolveDesc> d(1);
   d[0].LU = A; d[0].piv = piv; d[0].n = n; d[0].lda = n; d[0].X = X; d[0].nrhs = nrhs;
   d[0].ldx = nrhs;
-  if (nrhs > 0) launch_lusolve(C.stage.push_vec(C, d), 1, nrhs, C.st);
+  if (nrhs > 0) launch_lusolve(C.stage.push_vec(C, d), 1, nrhs, C.st, n);
   CUDA_CHECK(cudaGetLastError());
   C.sync();
   C.check_status("test ");

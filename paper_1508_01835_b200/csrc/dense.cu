@@ -183,11 +183,15 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int e = threadIdx.x; e < cols * cols; e += blockDim.x)
     V[e] = (e % (cols + 1) == 0) ? 1.0 : 0.0;
-  const double tol = kEps * sqrt((double)(rows > 1 ? rows : 1));
+  // rotate whenever the pair is not orthogonal to working precision, but
+  // only rotations above the dot-product rounding level (rows * eps) keep
+  // the sweep loop alive -- otherwise rounding noise never converges.
+  const double tol_rot = kEps;
+  const double tol_conv = kEps * (double)(rows > 4 ? rows : 4);
   const int cp = cols + (cols & 1);
   __syncthreads();
   if (cols < 2) return;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *sflag = 0;
     __syncthreads();
     for (int r = 0; r < cp - 1; ++r) {
@@ -205,7 +209,8 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
           a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
         }
         a = warp_sum(a); b = warp_sum(b); g = warp_sum(g);
-        if (g != 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
+        const double sab = sqrt(a) * sqrt(b);
+        if (g != 0.0 && fabs(g) > tol_rot * sab) {
           const double zeta = (b - a) / (2.0 * g);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -221,7 +226,7 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
             vx[i] = c * u - s * v;
             vy[i] = s * u + c * v;
           }
-          if (lane == 0) *sflag = 1;
+          if (lane == 0 && fabs(g) > tol_conv * sab) *sflag = 1;
         }
       }
       __syncthreads();
@@ -663,6 +668,45 @@ lusolve_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks_per_
     x[i * ld] = ((s0 + s1) + (s2 + s3)) / U[i];
   }
 }
+// One CTA per (system, 32-column chunk): the chunk lives in shared memory
+// (n x 33 padded), lane = column, 8 warps split the rows of each rank-1
+// column sweep; one barrier per pivot.  Final backward values go straight
+// to global memory so no thread ever overwrites a value another may read.
+__global__ void __launch_bounds__(256)
+lusolve_smem_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks_per_desc) {
+  extern __shared__ double xs[];
+  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  const int di = blockIdx.x / chunks_per_desc, ch = blockIdx.x % chunks_per_desc;
+  if (di >= ndesc) return;
+  const LuSolveDesc d = descs[di];
+  const int c0 = ch * 32;
+  if (c0 >= d.nrhs) return;
+  const int nc = min(32, d.nrhs - c0);
+  const int N = d.n;
+  const size_t ld = d.ldx;
+  for (int e = threadIdx.x; e < N * 32; e += blockDim.x) {
+    const int i = e >> 5, cc = e & 31;
+    xs[i * 33 + cc] = cc < nc ? d.X[(size_t)i * ld + c0 + cc] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32)
+    for (int j = 0; j < N; ++j) {
+      const int p = d.piv[j];
+      if (p != j) { const double t = xs[j * 33 + c]; xs[j * 33 + c] = xs[p * 33 + c]; xs[p * 33 + c] = t; }
+    }
+  __syncthreads();
+  for (int j = 0; j < N - 1; ++j) {
+    const double xj = xs[j * 33 + c];
+    for (int i = j + 1 + r0; i < N; i += 8) xs[i * 33 + c] -= d.LU[(size_t)i * d.lda + j] * xj;
+    __syncthreads();
+  }
+  for (int j = N - 1; j >= 0; --j) {
+    const double xj = xs[j * 33 + c] / d.LU[(size_t)j * d.lda + j];
+    if (r0 == (j & 7) && c < nc) d.X[(size_t)j * ld + c0 + c] = xj;
+    for (int i = r0; i < j; i += 8) xs[i * 33 + c] -= d.LU[(size_t)i * d.lda + j] * xj;
+    __syncthreads();
+  }
+}
 }  // namespace
 
 void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
@@ -676,8 +720,21 @@ void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
   lu_kernel<<<n < 4096 ? n : 4096, 512, smem, s>>>(d_descs, n, d_status, smem / 8);
 }
 
-void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs, cudaStream_t s) {
+void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs, cudaStream_t s,
+                    int max_n) {
   if (ndesc <= 0 || max_nrhs <= 0) return;
+  if (max_n > 0 && max_n <= 800) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(lusolve_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           220 * 1024);
+      attr = true;
+    }
+    const int chunks = (max_nrhs + 31) / 32;
+    lusolve_smem_kernel<<<ndesc * chunks, 256, (size_t)max_n * 33 * sizeof(double), s>>>(
+        d_descs, ndesc, chunks);
+    return;
+  }
   const int chunks = (max_nrhs + 31) / 32;
   const long long warps = (long long)ndesc * chunks;
   const int blocks = (int)((warps + 7) / 8);

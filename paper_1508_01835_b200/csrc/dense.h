@@ -103,8 +103,9 @@ struct LuSolveDesc {
   double* X;
   int nrhs, ldx;
 };
+// max_n (largest system) <= 800 selects the shared-memory kernel.
 void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs,
-                    cudaStream_t s);
+                    cudaStream_t s, int max_n = 0);
 
 }  // namespace ifmm
 

@@ -30,6 +30,31 @@ namespace ifmm {
 static constexpr int TOP_TAG = 0x7fffffff - 1;
 
 // IFMM_TRACE=<file>: per-pair decision trace (debug / parity triage)
+// IFMM_PROFILE=1: stream-synchronised phase timers (diagnostics; perturbs
+// overlap, never used for reported numbers)
+enum { PH_LU = 0, PH_XSOLVE, PH_SCHUR, PH_ADD, PH_FILLSVD, PH_UNION, PH_REBASE, PH_NEWK, PH_MERGE,
+       PH_TOP, PH_HOST, PH_N };
+double g_prof[PH_N];
+static bool prof_on() {
+  static int on = -1;
+  if (on < 0) { const char* p = getenv("IFMM_PROFILE"); on = (p && *p == '1') ? 1 : 0; }
+  return on == 1;
+}
+struct Phase {
+  Ctx& C;
+  int id;
+  std::chrono::steady_clock::time_point t0;
+  Phase(Ctx& c, int i) : C(c), id(i) {
+    if (prof_on()) { C.sync(); t0 = std::chrono::steady_clock::now(); }
+  }
+  ~Phase() {
+    if (prof_on()) {
+      C.sync();
+      g_prof[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+};
+
 static FILE* trace_file() {
   static FILE* f = nullptr;
   static bool init = false;
@@ -49,7 +74,12 @@ void lu_any(Ctx& C, double* A, int n, int* piv, int tag) {
   if (n <= 160) {
     std::vector<LuDesc> d(1);
     d[0].A = A; d[0].n = n; d[0].lda = n; d[0].piv = piv; d[0].tag = tag;
-    launch_lu(C.stage.push_vec(C, d), 1, C.d_status, C.st);
+    LuDesc* dd = C.stage.push_vec(C, d);
+    cudaEvent_t ka = nullptr;
+    const double fl = 2.0 / 3.0 * (double)n * n * n;
+    C.kt_begin(K_LU, fl, &ka);
+    launch_lu(dd, 1, C.d_status, C.st);
+    C.kt_end(K_LU, fl, ka);
     C.launches++;
   } else {
     lu_blocked(C, A, n, n, piv, tag);
@@ -62,7 +92,12 @@ static void lusolve(Ctx& C, const double* LU, const int* piv, int n, double* X, 
   std::vector<LuSolveDesc> d(1);
   d[0].LU = LU; d[0].piv = piv; d[0].n = n; d[0].lda = n; d[0].X = X; d[0].nrhs = nrhs;
   d[0].ldx = nrhs;
-  launch_lusolve(C.stage.push_vec(C, d), 1, nrhs, C.st);
+  LuSolveDesc* dd = C.stage.push_vec(C, d);
+  cudaEvent_t ka = nullptr;
+  const double fl = 2.0 * n * n * (double)nrhs;
+  C.kt_begin(K_LUSOLVE, fl, &ka);
+  launch_lusolve(dd, 1, nrhs, C.st, n);
+  C.kt_end(K_LUSOLVE, fl, ka);
   C.launches++;
   CUDA_CHECK(cudaGetLastError());
 }
@@ -114,8 +149,8 @@ struct Eliminator {
   void run_gemm(GemmBatch& gb) {
     flops_gemm += gb.flops;
     flops_all += gb.flops;
-    gb.flops = 0;
     gb.run(C);
+    gb.flops = 0;
   }
 
   // -------------------------------------------------------------------------
@@ -134,6 +169,7 @@ struct Eliminator {
     if (reqs.empty()) return;
     int* dr = ranks_buf((int)reqs.size());
     std::vector<UnionDesc> ud;
+    double uflops = 0;
     for (size_t i = 0; i < reqs.size(); ++i) {
       UReq& q = reqs[i];
       BU& b = *q.bu;
@@ -157,9 +193,16 @@ struct Eliminator {
       ud.push_back(d);
       // flop estimate: ACA 2mn per step (<= cap steps) + QR/SVD of cap
       const double mm = b.m, nn = b.k_old + b.k_f, s = b.cap;
-      flops_all += 2 * mm * nn * s + 2 * mm * s * s + 2 * nn * s * s + 4 * s * s * s + 22 * s * s * s;
+      const double fl = 2 * mm * nn * s + 2 * mm * s * s + 2 * nn * s * s + 4 * s * s * s + 22 * s * s * s;
+      flops_all += fl;
+      uflops += fl;
     }
-    launch_union(C.stage.push_vec(C, ud), (int)ud.size(), thr, C.st);
+    Phase ph(C, PH_UNION);
+    UnionDesc* dud = C.stage.push_vec(C, ud);
+    cudaEvent_t ka = nullptr;
+    C.kt_begin(K_UNION, uflops, &ka);
+    launch_union(dud, (int)ud.size(), thr, C.st);
+    C.kt_end(K_UNION, uflops, ka);
     C.launches++;
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(dr, reqs.size());
@@ -312,6 +355,7 @@ void Eliminator::finish_unions(int c, BU& bu, BU& bv, const double* fu, int fu_r
 
 // _apply_rebase (factor.py:395-430)
 void Eliminator::rebase(int c, BU& bu, BU& bv, int partner) {
+  Phase ph(C, PH_REBASE);
   if (FILE* tf = trace_file()) fprintf(tf, "R %d %d %d %d\n", c, bu.k_old, bu.rank, bv.rank);
   const int nxn = g.nx[c], nzn = g.nz[c], nyn = g.ny[c];
   const int py = g.ny[partner];
@@ -450,6 +494,7 @@ void Eliminator::redirect(int cj, int ck, const FillFac* f_kj, const FillFac* f_
     if (r2 > 0)
       gc.add(uj.FM.p, uj.k_f, 0, vk.FM.p, vk.k_f, 1, njk.p, kkn, kjn, kkn, r2, 1.0,
              has_jk ? 1.0 : 0.0, sjk);
+    Phase ph(C, PH_NEWK);
     CopyBatch z;
     if (!has_kj && r1 == 0) z.zero(nkj);
     if (!has_jk && r2 == 0) z.zero(njk);
@@ -496,6 +541,7 @@ void Eliminator::redirect(int cj, int ck, const FillFac* f_kj, const FillFac* f_
     if (rv > 0)
       gb2.add(Ud, nd, 1, bv.FM.p, bv.k_f, 1, ndl.p, kln, nd, kln, rv, 1.0, has_dl ? 1.0 : 0.0,
               sd);
+    Phase ph(C, PH_NEWK);
     CopyBatch z;
     if (!has_ld && ru == 0) z.zero(nld);
     if (!has_dl && rv == 0) z.zero(ndl);
@@ -520,6 +566,7 @@ void Eliminator::eliminate(int c, LevelStats& st) {
   Blk e1 = g.take(nzn, nyn), e2 = g.take(nyn, nzn);
   C.free(e1); C.free(e2);
   Blk P = C.alloc(n, n);
+  Phase* ph = new Phase(C, PH_LU);
   {
     CopyBatch cb;
     cb.copy(D, P, 0, 0);
@@ -534,6 +581,8 @@ void Eliminator::eliminate(int c, LevelStats& st) {
   lu_any(C, P.p, n, piv, c);
   flops_gemm += 2.0 / 3.0 * (double)n * n * n;
   flops_all += 2.0 / 3.0 * (double)n * n * n;
+  delete ph;
+  ph = new Phase(C, PH_XSOLVE);
 
   ElimEv ev;
   ev.nx = nxn; ev.nz = nzn; ev.ny = nyn; ev.m = m; ev.k = k;
@@ -579,6 +628,8 @@ void Eliminator::eliminate(int c, LevelStats& st) {
   lusolve(C, P.p, piv, n, X.p, NC);
   flops_gemm += 2.0 * n * n * (double)NC;
   flops_all += 2.0 * n * n * (double)NC;
+  delete ph;
+  ph = new Phase(C, PH_SCHUR);
 
   // Schur fill: F = [-Tstk X[:m] ; X[m:]]   (NR x NC)
   Blk Fm = C.alloc(NR, NC);
@@ -592,6 +643,8 @@ void Eliminator::eliminate(int c, LevelStats& st) {
   }
   C.free(X);
 
+  delete ph;
+  ph = new Phase(C, PH_ADD);
   F.elims.push_back(std::move(ev));
   F.events.push_back({0, (int)F.elims.size() - 1});
   const ElimEv& E = F.elims.back();
@@ -626,8 +679,11 @@ void Eliminator::eliminate(int c, LevelStats& st) {
     }
   }
   adds.run(C);
+  delete ph;
+  ph = nullptr;
 
   if (!stash.empty()) {
+    Phase* ps = new Phase(C, PH_FILLSVD);
     // compress every stashed fill in one batched Jacobi SVD launch
     std::vector<std::pair<std::pair<int, int>, Stash>> items(stash.begin(), stash.end());
     const int ns = (int)items.size();
@@ -648,6 +704,12 @@ void Eliminator::eliminate(int c, LevelStats& st) {
       const double mm = std::max(s.h, s.w), nn = std::min(s.h, s.w);
       flops_all += 4 * mm * nn * nn + 22 * nn * nn * nn;
     }
+    double sflops = 0;
+    for (int i = 0; i < ns; ++i) {
+      const double mm = std::max(items[i].second.h, items[i].second.w);
+      const double nn = std::min(items[i].second.h, items[i].second.w);
+      sflops += 4 * mm * nn * nn + 22 * nn * nn * nn;
+    }
     Blk ws = C.alloc(1, (int)std::max<size_t>(tot, 1));
     int* dr = ranks_buf(ns);
     std::vector<SvdDesc> sd(ns);
@@ -659,7 +721,11 @@ void Eliminator::eliminate(int c, LevelStats& st) {
       sd[i].rank = dr + i;
       sd[i].work = ws.p + wo[i];
     }
-    launch_svd(C.stage.push_vec(C, sd), ns, thr, smem_dim, C.st, 0);
+    SvdDesc* dsd = C.stage.push_vec(C, sd);
+    cudaEvent_t ka = nullptr;
+    C.kt_begin(K_SVD, sflops, &ka);
+    launch_svd(dsd, ns, thr, smem_dim, C.st, 0);
+    C.kt_end(K_SVD, sflops, ka);
     C.launches++;
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(dr, ns);
@@ -670,6 +736,7 @@ void Eliminator::eliminate(int c, LevelStats& st) {
       f.m = sd[i].m; f.n = sd[i].n; f.rank = hr[i];
       fac[items[i].first] = f;
     }
+    delete ps;
     std::set<std::pair<int, int>> pairs;
     for (auto& it : items)
       pairs.insert({std::min(it.first.first, it.first.second),
@@ -690,6 +757,7 @@ void Eliminator::eliminate(int c, LevelStats& st) {
 
 // merge_to_parent (factor.py:525-578)
 void Eliminator::merge(int level) {
+  Phase ph(C, PH_MERGE);
   Tree& T = *g.tree;
   std::map<int, int> owner, offs;  // child y node -> parent cluster / offset
   std::map<int, int> px_of;
@@ -748,6 +816,7 @@ void Eliminator::merge(int level) {
 
 // _assemble_top (factor.py:233-246)
 void Eliminator::top() {
+  Phase ph(C, PH_TOP);
   Tree& T = *g.tree;
   std::vector<int> tn;
   if (T.depth >= 2)
@@ -803,6 +872,7 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
     F->leaf_stop.push_back(T.stop[c]);
   }
   Eliminator el(C, g, *F, eps * sigma0, 0x1f2e3d4c5b6a7988ULL);
+  for (double& v : g_prof) v = 0.0;
   try {
     for (int l = T.depth; l >= 2; --l) {
       LevelStats st;

@@ -11,79 +11,74 @@ void set_last_error(const std::string& s) { g_last_error = s; }
 const char* last_error_cstr() { return g_last_error.c_str(); }
 
 // ---------------------------------------------------------------------------
-// Arena: classes of 256 B up to 4 KiB, then geometric with 8 steps / octave.
-// Frees go to per-class free lists; reuse is safe because every kernel runs
-// on the one context stream (a freed block is only handed to work enqueued
-// after the last reader).
+// Arena: best-fit with coalescing.  Reuse is safe because every kernel runs
+// on the one context stream and frees are deferred (Ctx::free/flush).
 // ---------------------------------------------------------------------------
-static std::vector<size_t>& class_table() {
-  static std::vector<size_t> t;
-  if (t.empty()) {
-    size_t s = 256;
-    while (s < (size_t)1 << 41) {
-      t.push_back(s);
-      size_t nx = s + 256;
-      if (s >= 4096) {
-        size_t g = s / 8;
-        g = (g + 255) / 256 * 256;
-        nx = s + g;
-      }
-      s = nx;
-    }
-  }
-  return t;
-}
-
-int Arena::class_of(size_t bytes) {
-  auto& t = class_table();
-  auto it = std::lower_bound(t.begin(), t.end(), bytes);
-  return (int)(it - t.begin());
-}
-size_t Arena::class_bytes(int cls) { return class_table()[cls]; }
-
 void Arena::init(size_t bytes) {
   bytes = bytes / 4096 * 4096;
   CUDA_CHECK(cudaMalloc(&base_, bytes));
   cap_ = bytes;
-  top_ = in_use_ = peak_ = 0;
-  bins_.assign(class_table().size(), {});
+  in_use_ = peak_ = 0;
+  by_addr_.clear();
+  by_size_.clear();
+  insert_free(0, bytes);
 }
 
 void Arena::release() {
   if (base_) cudaFree(base_);
   base_ = nullptr;
-  cap_ = top_ = 0;
-  bins_.clear();
+  cap_ = 0;
+  by_addr_.clear();
+  by_size_.clear();
+}
+
+void Arena::insert_free(size_t off, size_t len) {
+  by_addr_[off] = len;
+  by_size_.insert({len, off});
 }
 
 double* Arena::alloc(size_t ndoubles, int* cls) {
-  const size_t bytes = ndoubles * sizeof(double);
-  const int c = class_of(bytes);
-  const size_t cb = class_bytes(c);
-  char* p;
-  if (!bins_[c].empty()) {
-    p = bins_[c].back();
-    bins_[c].pop_back();
-  } else {
-    if (top_ + cb > cap_) {
-      char msg[160];
-      snprintf(msg, sizeof msg, "device arena exhausted: need %zu B, %zu of %zu B used", cb,
-               in_use_, cap_);
-      throw Error(E_OOM, msg);
-    }
-    p = base_ + top_;
-    top_ += cb;
+  size_t bytes = ndoubles * sizeof(double);
+  bytes = (bytes + 255) / 256 * 256;
+  if (bytes == 0) bytes = 256;
+  auto it = by_size_.lower_bound({bytes, 0});
+  if (it == by_size_.end()) {
+    char msg[200];
+    snprintf(msg, sizeof msg, "device arena exhausted: need %zu B, %zu of %zu B in use", bytes,
+             in_use_, cap_);
+    throw Error(E_OOM, msg);
   }
-  in_use_ += cb;
+  const size_t len = it->first, off = it->second;
+  by_size_.erase(it);
+  by_addr_.erase(off);
+  if (len > bytes) insert_free(off + bytes, len - bytes);
+  in_use_ += bytes;
   peak_ = std::max(peak_, in_use_);
-  *cls = c;
-  return reinterpret_cast<double*>(p);
+  *cls = (int)(bytes / 256);
+  return reinterpret_cast<double*>(base_ + off);
 }
 
 void Arena::free(void* p, int cls) {
-  if (!p || cls < 0) return;
-  bins_[cls].push_back(reinterpret_cast<char*>(p));
-  in_use_ -= class_bytes(cls);
+  if (!p || cls <= 0) return;
+  size_t off = (size_t)(reinterpret_cast<char*>(p) - base_);
+  size_t len = (size_t)cls * 256;
+  in_use_ -= len;
+  auto nx = by_addr_.lower_bound(off);
+  if (nx != by_addr_.end() && nx->first == off + len) {  // merge with next
+    len += nx->second;
+    by_size_.erase({nx->second, nx->first});
+    nx = by_addr_.erase(nx);
+  }
+  if (nx != by_addr_.begin()) {
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == off) {  // merge with previous
+      off = pv->first;
+      len += pv->second;
+      by_size_.erase({pv->second, pv->first});
+      by_addr_.erase(pv);
+    }
+  }
+  insert_free(off, len);
 }
 
 // ---------------------------------------------------------------------------
@@ -149,7 +144,10 @@ void GemmBatch::run(Ctx& ctx) {
   ts[d.size()] = tot;
   GemmDesc* dd = ctx.stage.push_vec(ctx, d);
   int* dt = ctx.stage.push_vec(ctx, ts);
+  cudaEvent_t ka = nullptr;
+  ctx.kt_begin(K_GEMM, flops, &ka);
   launch_gemm(dd, dt, (int)d.size(), tot, ctx.st);
+  ctx.kt_end(K_GEMM, flops, ka);
   ctx.launches++;
   CUDA_CHECK(cudaGetLastError());
   d.clear();
@@ -158,7 +156,12 @@ void GemmBatch::run(Ctx& ctx) {
 void CopyBatch::run(Ctx& ctx) {
   if (d.empty()) return;
   CopyDesc* dd = ctx.stage.push_vec(ctx, d);
+  double bytes = 0;
+  for (auto& x : d) bytes += 16.0 * x.rows * x.cols;
+  cudaEvent_t ka = nullptr;
+  ctx.kt_begin(K_COPY, bytes, &ka);
   launch_copy(dd, (int)d.size(), ctx.st);
+  ctx.kt_end(K_COPY, bytes, ka);
   ctx.launches++;
   CUDA_CHECK(cudaGetLastError());
   d.clear();

@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,7 +39,8 @@ void set_last_error(const std::string& s);
     if (!(c)) throw ::ifmm::Error(::ifmm::E_ASSERT, std::string(msg)); \
   } while (0)
 
-// ---- device arena: size-class free lists over one cudaMalloc slab -------
+// ---- device arena: best-fit, coalescing free list over one cudaMalloc ----
+// Blocks are multiples of 256 B; `cls` carries the length in 256-B units.
 class Arena {
  public:
   void init(size_t bytes);
@@ -50,11 +53,11 @@ class Arena {
   size_t capacity() const { return cap_; }
 
  private:
-  static int class_of(size_t bytes);
-  static size_t class_bytes(int cls);
+  void insert_free(size_t off, size_t len);
   char* base_ = nullptr;
-  size_t cap_ = 0, top_ = 0, in_use_ = 0, peak_ = 0;
-  std::vector<std::vector<char*>> bins_;
+  size_t cap_ = 0, in_use_ = 0, peak_ = 0;
+  std::map<size_t, size_t> by_addr_;              // offset -> length
+  std::set<std::pair<size_t, size_t>> by_size_;   // (length, offset)
 };
 
 // ---- dense block handle (row-major r x c, ld = c) ------------------------
@@ -94,6 +97,42 @@ struct Ctx {
   int* h_pinned_i = nullptr; // small pinned readback buffer
   size_t h_pinned_n = 0;
   long long launches = 0;
+  cudaEvent_t ev[64] = {};
+  // per-category kernel timing (IFMM_KTIME=1 or ktime_on): event pairs
+  bool ktime_on = false;
+  struct KRec { int cat; cudaEvent_t a, b; double work; };
+  std::vector<KRec> krec;
+  std::vector<cudaEvent_t> kpool;
+  double ktime[16] = {}, kwork[16] = {};
+  long long kcount[16] = {};
+  void kt_begin(int cat, double work, cudaEvent_t* a) {
+    if (!ktime_on) return;
+    if (kpool.size() < 2) for (int i = 0; i < 256; ++i) { cudaEvent_t e; cudaEventCreate(&e); kpool.push_back(e); }
+    *a = kpool.back(); kpool.pop_back();
+    cudaEventRecord(*a, st);
+    (void)cat; (void)work;
+  }
+  void kt_end(int cat, double work, cudaEvent_t a) {
+    if (!ktime_on) return;
+    cudaEvent_t b = kpool.back(); kpool.pop_back();
+    cudaEventRecord(b, st);
+    krec.push_back({cat, a, b, work});
+    if (krec.size() > 4096) kt_collect();
+  }
+  void kt_collect() {
+    if (krec.empty()) return;
+    cudaStreamSynchronize(st);
+    for (auto& k : krec) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, k.a, k.b);
+      ktime[k.cat] += ms * 1e-3;
+      kwork[k.cat] += k.work;
+      kcount[k.cat]++;
+      kpool.push_back(k.a);
+      kpool.push_back(k.b);
+    }
+    krec.clear();
+  }
 
   Blk alloc(int r, int c) {
     Blk b;
@@ -127,6 +166,8 @@ struct Ctx {
 };
 
 // ---- batched launch builders ---------------------------------------------
+enum KCat { K_GEMM = 0, K_COPY, K_SVD, K_UNION, K_LU, K_LUSOLVE, K_SPMV, K_SOLVE, K_OTHER, K_NCAT };
+
 struct GemmBatch {
   std::vector<GemmDesc> d;
   double flops = 0.0;

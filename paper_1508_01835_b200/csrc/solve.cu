@@ -448,12 +448,19 @@ void Factor::solve(const double* d_b, double* d_x) {
   Program& P = *prog;
   const int N = n_points;
   double* W = P.work.p;
+  double solve_bytes = 0;  // algorithmic bytes: every stored factor block read twice
+  for (auto& e : elims)
+    solve_bytes += 8.0 * (2.0 * (double)(e.m + e.k) * (e.m + e.k) + (double)e.m * e.Scat.c +
+                          (double)e.Tstk.r * e.m);
+  for (auto& r : rebases) solve_bytes += 8.0 * r.r.r * r.r.c;
   const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
   CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, C.st));
   gather_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(d_b, d_perm, N, W);
   const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
   const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
   const size_t smem = (size_t)std::max(P.max_n, 1) * sizeof(double);
+  cudaEvent_t ka = nullptr;
+  C.kt_begin(K_SOLVE, 0, &ka);
   for (int w = 0; w < P.fwd_waves; ++w) {
     const int a = P.fwd_wave_start[w], b = P.fwd_wave_start[w + 1];
     solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
@@ -467,6 +474,7 @@ void Factor::solve(const double* d_b, double* d_x) {
     solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
   }
   scatter_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(W + P.sol0, d_perm, N, d_x);
+  C.kt_end(K_SOLVE, solve_bytes, ka);
   C.launches += 3 + P.fwd_waves + P.bwd_waves;
   CUDA_CHECK(cudaGetLastError());
 }

@@ -1,0 +1,27 @@
+"""Scale probe: time each stage of the pipeline at a given N (c3/c4 recipe)."""
+import sys, time, numpy as np
+sys.path.insert(0, ".")
+import paper_1508_01835_b200 as P
+from paper_1508_01835_b200 import _native as NN
+N = int(sys.argv[1]); leaf = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+seed = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+g = np.random.Generator(np.random.PCG64(seed))
+pts = g.uniform(0.0, 1.0, size=(N, 3))
+b = np.random.Generator(np.random.PCG64(seed + 1)).standard_normal(N)
+h = N ** (-1.0 / 3.0)
+t = time.perf_counter(); tree, _ = P.build_octree(pts, leaf); topo = P.compute_topology(tree)
+print(f"N={N} depth={tree.depth} leaves={len(tree.leaves())} tree {time.perf_counter()-t:.2f}s", flush=True)
+t = time.perf_counter(); ops = P.chebyshev_operators(tree, topo, P.imq_kernel(h), 4, epsilon=1e-6)
+print(f"h2 build {time.perf_counter()-t:.2f}s max rank {ops.max_rank()}", flush=True)
+t = time.perf_counter(); P.initialize_weights(ops, topo); print(f"weights {time.perf_counter()-t:.2f}s", flush=True)
+t = time.perf_counter(); gr = P.assemble_extended_graph(ops); print(f"graph {time.perf_counter()-t:.2f}s dim {gr.dim} edges {gr.num_edges}", flush=True)
+t = time.perf_counter(); s0 = P.estimate_sigma0(gr); print(f"sigma0 {s0:.10g} {time.perf_counter()-t:.2f}s", flush=True)
+t = time.perf_counter(); f = P.factorize(gr, 1e-6, sigma0=s0); tf = time.perf_counter() - t
+print(f"factorize {tf:.2f}s stats peak_edges={f.stats.peak_edges} events={f.event_counts} flops={f.flops}", flush=True)
+print("profile", {k: round(v, 3) for k, v in NN.profile().items()}, flush=True)
+print("levels", [(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in f.stats.levels], flush=True)
+t = time.perf_counter(); x = f.solve(b); ts = time.perf_counter() - t
+t = time.perf_counter(); x = f.solve(b); ts2 = time.perf_counter() - t
+y = P.h2_matvec(ops, x)
+print(f"solve {ts:.3f}s / {ts2:.3f}s  rel res (H2) {np.linalg.norm(y-b)/np.linalg.norm(b):.3e}  unknowns/s {N/(tf+ts2):.1f}")
+print("arena in_use/peak GB", [v / 2**30 for v in NN.memory()])
