@@ -18,6 +18,10 @@
 
 namespace ifmm {
 
+__device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
+__device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
+                          double* Q, int ldq);
+
 // ============================================================================
 // Grouped GEMM (DMMA)
 // ============================================================================
@@ -179,13 +183,68 @@ void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s) {
 // W: col-major rows x cols (ld ldw, rows >= cols); V: col-major cols x cols
 // (ld cols) initialised here to I.  On exit W's columns are sigma_j u_j
 // (unsorted) and V holds the accumulated rotations.
+template <int T>
+__device__ __forceinline__ double team_sum(double v) {
+#pragma unroll
+  for (int o = T / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One round-robin sweep pass with teams of T lanes per column pair.
+template <int T>
+__device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int ldw, double* V,
+                                             int cp, int r, double tol_rot, double tol_conv,
+                                             int* sflag) {
+  const int tl = threadIdx.x & (T - 1);
+  const int team = threadIdx.x / T, nteam = blockDim.x / T;
+  for (int pi0 = 0; pi0 < cp / 2; pi0 += nteam) {
+    const int pi = pi0 + team;
+    int p = 0, q = cols;
+    if (pi < cp / 2) {
+      if (pi == 0) { p = r; q = cp - 1; }
+      else { p = (r + pi) % (cp - 1); q = (r - pi + cp - 1) % (cp - 1); }
+      if (p > q) { int t = p; p = q; q = t; }
+    }
+    const bool act = pi < cp / 2 && q < cols;
+    double a = 0.0, b = 0.0, g = 0.0;
+    double* x = W + (size_t)p * ldw;
+    double* y = W + (size_t)(act ? q : p) * ldw;
+    if (act)
+      for (int i = tl; i < rows; i += T) {
+        const double u = x[i], v = y[i];
+        a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
+      }
+    // all lanes of the warp take part in the shuffles (teams never straddle)
+    a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
+    if (!act) continue;
+    const double sab = sqrt(a) * sqrt(b);
+    if (g != 0.0 && fabs(g) > tol_rot * sab) {
+      const double zeta = (b - a) / (2.0 * g);
+      const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+      const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+      for (int i = tl; i < rows; i += T) {
+        const double u = x[i], v = y[i];
+        x[i] = c * u - s * v;
+        y[i] = s * u + c * v;
+      }
+      double* vx = V + (size_t)p * cols;
+      double* vy = V + (size_t)q * cols;
+      for (int i = tl; i < cols; i += T) {
+        const double u = vx[i], v = vy[i];
+        vx[i] = c * u - s * v;
+        vy[i] = s * u + c * v;
+      }
+      if (tl == 0 && fabs(g) > tol_conv * sab) *sflag = 1;
+    }
+  }
+}
+
+// One-sided Jacobi (Hestenes), round-robin ordering.  Rotations are applied
+// whenever a pair is not orthogonal to working precision; only rotations
+// above the dot-product rounding level (rows * eps) keep the sweeps going.
 __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, int* sflag) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int e = threadIdx.x; e < cols * cols; e += blockDim.x)
     V[e] = (e % (cols + 1) == 0) ? 1.0 : 0.0;
-  // rotate whenever the pair is not orthogonal to working precision, but
-  // only rotations above the dot-product rounding level (rows * eps) keep
-  // the sweep loop alive -- otherwise rounding noise never converges.
   const double tol_rot = kEps;
   const double tol_conv = kEps * (double)(rows > 4 ? rows : 4);
   const int cp = cols + (cols & 1);
@@ -195,40 +254,9 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
     if (threadIdx.x == 0) *sflag = 0;
     __syncthreads();
     for (int r = 0; r < cp - 1; ++r) {
-      for (int pi = warp; pi < cp / 2; pi += nw) {
-        int p, q;
-        if (pi == 0) { p = r; q = cp - 1; }
-        else { p = (r + pi) % (cp - 1); q = (r - pi + cp - 1) % (cp - 1); }
-        if (p > q) { int t = p; p = q; q = t; }
-        if (q >= cols) continue;
-        double* x = W + (size_t)p * ldw;
-        double* y = W + (size_t)q * ldw;
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < rows; i += 32) {
-          const double u = x[i], v = y[i];
-          a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
-        }
-        a = warp_sum(a); b = warp_sum(b); g = warp_sum(g);
-        const double sab = sqrt(a) * sqrt(b);
-        if (g != 0.0 && fabs(g) > tol_rot * sab) {
-          const double zeta = (b - a) / (2.0 * g);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = lane; i < rows; i += 32) {
-            const double u = x[i], v = y[i];
-            x[i] = c * u - s * v;
-            y[i] = s * u + c * v;
-          }
-          double* vx = V + (size_t)p * cols;
-          double* vy = V + (size_t)q * cols;
-          for (int i = lane; i < cols; i += 32) {
-            const double u = vx[i], v = vy[i];
-            vx[i] = c * u - s * v;
-            vy[i] = s * u + c * v;
-          }
-          if (lane == 0 && fabs(g) > tol_conv * sab) *sflag = 1;
-        }
-      }
+      if (rows <= 64) jacobi_round<8>(W, rows, cols, ldw, V, cp, r, tol_rot, tol_conv, sflag);
+      else if (rows <= 192) jacobi_round<16>(W, rows, cols, ldw, V, cp, r, tol_rot, tol_conv, sflag);
+      else jacobi_round<32>(W, rows, cols, ldw, V, cp, r, tol_rot, tol_conv, sflag);
       __syncthreads();
     }
     const int again = *sflag;
@@ -261,7 +289,11 @@ __device__ void cta_sv_order(const double* W, int rows, int cols, int ldw, doubl
 
 __host__ __device__ size_t svd_work_doubles(int m, int n) {
   const int rows = m > n ? m : n, cols = m > n ? n : m;
-  return (size_t)rows * cols + (size_t)cols * cols + 2 * (size_t)cols + 8;
+  const size_t jac = (size_t)rows * cols + (size_t)cols * cols + 2 * (size_t)cols + 8;
+  // QRCP path: A (m n) + Q0 (m k) + W2 (n k) + Vacc (k k) + norms/perm/tau/sig/order
+  const size_t k = cols;
+  const size_t qr = (size_t)m * n + (size_t)m * k + (size_t)n * k + k * k + 2 * (size_t)n + 4 * k + 16;
+  return jac > qr ? jac : qr;
 }
 
 namespace {
@@ -331,8 +363,173 @@ size_t svd_smem_doubles(int max_smem_dim) {
   return need * sizeof(double) > 200 * 1024 ? 0 : need;
 }
 
+namespace {
+// Truncated SVD through a rank-revealing pivoted QR (fill compression).
+// F P = Q R; stop at step r0 once ||R22||_F <= delta, delta = max(1e-9 thr,
+// rounding level of F).  Then one-sided Jacobi on M^T = (R0 P^T)^T
+// (n x r0):  F ~= Q0 M = (Q0 Vacc) S (W2 Vacc / S)^T.  Weyl: every
+// singular value moves by <= delta, so `sigma > thr` only differs from an
+// exact SVD for sigma within delta of thr.
+__global__ void __launch_bounds__(512)
+fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ long long redi[32];
+  __shared__ int sflag;
+  __shared__ double s_beta, s_tau, s_scale, s_tot;
+  __shared__ int s_p, s_stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
+    const SvdDesc d = descs[bb];
+    const int m = d.m, nn = d.n;
+    const int kmax = m < nn ? m : nn;
+    if (kmax == 0) { if (threadIdx.x == 0) *d.rank = 0; continue; }
+    const size_t need = svd_work_doubles(m, nn);
+    double* A = (need <= (size_t)smem_doubles) ? smem : d.work;
+    double* Q0 = A + (size_t)m * nn;
+    double* W2 = Q0 + (size_t)m * kmax;
+    double* Vc = W2 + (size_t)nn * kmax;
+    double* nrm = Vc + (size_t)kmax * kmax;
+    double* tau = nrm + nn;
+    double* sig = tau + kmax;
+    int* perm = (int*)(sig + kmax);
+    int* order = perm + nn;
+    // load col-major + column norms
+    for (long long e = threadIdx.x; e < (long long)m * nn; e += blockDim.x) {
+      const int j = (int)(e / m), i = (int)(e % m);
+      A[e] = d.src[(size_t)i * d.s_r + (size_t)j * d.s_c];
+    }
+    for (int j = threadIdx.x; j < nn; j += blockDim.x) perm[j] = j;
+    __syncthreads();
+    for (int j = warp; j < nn; j += nw) {
+      double s = 0.0;
+      for (int i = lane; i < m; i += 32) { const double u = A[(size_t)j * m + i]; s = fma(u, u, s); }
+      s = warp_sum(s);
+      if (lane == 0) nrm[j] = s;
+    }
+    __syncthreads();
+    double fro = 0.0;
+    for (int j = threadIdx.x; j < nn; j += blockDim.x) fro += nrm[j];
+    fro = block_sum(fro, red);
+    if (sqrt(fro) <= thr * (1.0 - 1e-12)) {  // sigma_1 <= ||F||_F <= thr
+      if (threadIdx.x == 0) *d.rank = 0;
+      __syncthreads();
+      continue;
+    }
+    const double delta = fmax(1e-9 * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
+    const double delta2 = delta * delta;
+    int r0 = 0;
+    for (int j = 0; j < kmax; ++j) {
+      // remaining Frobenius mass and pivot column
+      double t = 0.0, bv = -1.0;
+      long long bi = (1LL << 62);
+      for (int c2 = j + threadIdx.x; c2 < nn; c2 += blockDim.x) {
+        const double v = nrm[c2];
+        t += v;
+        if (v > bv || (v == bv && c2 < bi)) { bv = v; bi = c2; }
+      }
+      t = block_sum(t, red);
+      block_argmax(bv, bi, red, redi);
+      if (threadIdx.x == 0) { s_stop = t <= delta2; s_p = (int)bi; }
+      __syncthreads();
+      if (s_stop) break;
+      const int p = s_p;
+      if (p != j) {
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const double u = A[(size_t)j * m + i];
+          A[(size_t)j * m + i] = A[(size_t)p * m + i];
+          A[(size_t)p * m + i] = u;
+        }
+        if (threadIdx.x == 0) {
+          const double u = nrm[j]; nrm[j] = nrm[p]; nrm[p] = u;
+          const int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
+        }
+      }
+      __syncthreads();
+      // Householder on A[j:, j]
+      double* a = A + (size_t)j * m;
+      double nx = 0.0;
+      for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) nx = fma(a[i], a[i], nx);
+      nx = block_sum(nx, red);
+      if (threadIdx.x == 0) {
+        const double alpha = a[j];
+        if (nx == 0.0) { s_tau = 0.0; s_beta = alpha; s_scale = 0.0; }
+        else {
+          const double beta = -copysign(sqrt(alpha * alpha + nx), alpha);
+          s_tau = (beta - alpha) / beta;
+          s_scale = 1.0 / (alpha - beta);
+          s_beta = beta;
+        }
+        tau[j] = s_tau;
+      }
+      __syncthreads();
+      const double sc = s_scale, tj = s_tau;
+      if (tj != 0.0)
+        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[i] *= sc;
+      __syncthreads();
+      if (threadIdx.x == 0) a[j] = s_beta;
+      for (int c2 = j + 1 + warp; c2 < nn; c2 += nw) {
+        double* ac = A + (size_t)c2 * m;
+        if (tj != 0.0) {
+          double w = (lane == 0) ? ac[j] : 0.0;
+          for (int i = j + 1 + lane; i < m; i += 32) w = fma(a[i], ac[i], w);
+          w = warp_sum(w) * tj;
+          if (lane == 0) ac[j] -= w;
+          for (int i = j + 1 + lane; i < m; i += 32) ac[i] -= w * a[i];
+        }
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
+        s = warp_sum(s);
+        if (lane == 0) nrm[c2] = s;
+      }
+      r0 = j + 1;
+      __syncthreads();
+    }
+    if (r0 == 0) { if (threadIdx.x == 0) *d.rank = 0; __syncthreads(); continue; }
+    // Q0 (m x r0) and W2 = (R0 P^T)^T (n x r0)
+    cta_orgqr(A, m, r0, m, tau, Q0, m);
+    for (long long e = threadIdx.x; e < (long long)nn * r0; e += blockDim.x) {
+      const int aa = (int)(e / nn), jj = (int)(e % nn);  // row aa of R, column position jj
+      W2[(size_t)aa * nn + perm[jj]] = (aa <= jj) ? A[(size_t)jj * m + aa] : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi(W2, nn, r0, nn, Vc, &sflag);
+    cta_sv_order(W2, nn, r0, nn, sig, order);
+    int k = 0;
+    for (int j = 0; j < r0; ++j) k += sig[order[j]] > thr;
+    // U = Q0 Vc[:, order] (m x k); V = W2[:, order] / sig (n x k)
+    for (long long e = threadIdx.x; e < (long long)m * k; e += blockDim.x) {
+      const int pos = (int)(e / m), i = (int)(e % m);
+      const double* v = Vc + (size_t)order[pos] * r0;
+      double acc = 0.0;
+      for (int l = 0; l < r0; ++l) acc = fma(Q0[(size_t)l * m + i], v[l], acc);
+      d.U[(size_t)pos * m + i] = acc;
+    }
+    for (long long e = threadIdx.x; e < (long long)nn * k; e += blockDim.x) {
+      const int pos = (int)(e / nn), i = (int)(e % nn);
+      const int j = order[pos];
+      d.V[(size_t)pos * nn + i] = W2[(size_t)j * nn + i] / sig[j];
+    }
+    for (int pos = threadIdx.x; pos < k; pos += blockDim.x) d.S[pos] = sig[order[pos]];
+    if (threadIdx.x == 0) *d.rank = k;
+    __syncthreads();
+  }
+}
+}  // namespace
+
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim, cudaStream_t s,
                 int rel_mode) {
+  if (n > 0 && !rel_mode) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(fill_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr2 = true;
+    }
+    const size_t bytes = svd_smem_doubles(max_smem_dim) * sizeof(double);
+    fill_svd_kernel<<<n < 4096 ? n : 4096, 512, bytes, s>>>(d_descs, n, thr,
+                                                           (int)(bytes / sizeof(double)));
+    return;
+  }
   if (n <= 0) return;
   // shared-memory workspace for blocks up to max_smem_dim^2 (fits 200 KB)
   size_t bytes = svd_smem_doubles(max_smem_dim) * sizeof(double);

@@ -35,21 +35,24 @@ static constexpr int TOP_TAG = 0x7fffffff - 1;
 enum { PH_LU = 0, PH_XSOLVE, PH_SCHUR, PH_ADD, PH_FILLSVD, PH_UNION, PH_REBASE, PH_NEWK, PH_MERGE,
        PH_TOP, PH_HOST, PH_N };
 double g_prof[PH_N];
-static bool prof_on() {
+// IFMM_PROFILE=2: host-only phase timers (no synchronisation): host
+// enqueue/bookkeeping cost per phase.
+static int prof_mode() {
   static int on = -1;
-  if (on < 0) { const char* p = getenv("IFMM_PROFILE"); on = (p && *p == '1') ? 1 : 0; }
-  return on == 1;
+  if (on < 0) { const char* p = getenv("IFMM_PROFILE"); on = (p && *p) ? (*p - '0') : 0; }
+  return on;
 }
+static bool prof_on() { return prof_mode() != 0; }
 struct Phase {
   Ctx& C;
   int id;
   std::chrono::steady_clock::time_point t0;
   Phase(Ctx& c, int i) : C(c), id(i) {
-    if (prof_on()) { C.sync(); t0 = std::chrono::steady_clock::now(); }
+    if (prof_on()) { if (prof_mode() == 1) C.sync(); t0 = std::chrono::steady_clock::now(); }
   }
   ~Phase() {
     if (prof_on()) {
-      C.sync();
+      if (prof_mode() == 1) C.sync();
       g_prof[id] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   }
@@ -87,21 +90,6 @@ void lu_any(Ctx& C, double* A, int n, int* piv, int tag) {
   CUDA_CHECK(cudaGetLastError());
 }
 
-static void lusolve(Ctx& C, const double* LU, const int* piv, int n, double* X, int nrhs) {
-  if (n <= 0 || nrhs <= 0) return;
-  std::vector<LuSolveDesc> d(1);
-  d[0].LU = LU; d[0].piv = piv; d[0].n = n; d[0].lda = n; d[0].X = X; d[0].nrhs = nrhs;
-  d[0].ldx = nrhs;
-  LuSolveDesc* dd = C.stage.push_vec(C, d);
-  cudaEvent_t ka = nullptr;
-  const double fl = 2.0 * n * n * (double)nrhs;
-  C.kt_begin(K_LUSOLVE, fl, &ka);
-  launch_lusolve(dd, 1, nrhs, C.st, n);
-  C.kt_end(K_LUSOLVE, fl, ka);
-  C.launches++;
-  CUDA_CHECK(cudaGetLastError());
-}
-
 // ---------------------------------------------------------------------------
 // fill factors and basis updates
 // ---------------------------------------------------------------------------
@@ -123,6 +111,7 @@ struct BU {  // BasisUpdate (lowrank.py:22-51)
 };
 
 struct PairCtx;
+std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact);
 
 struct Eliminator {
   Ctx& C;
@@ -238,9 +227,26 @@ struct Eliminator {
   void finish_unions(int c, BU& bu, BU& bv, const double* fu, int fu_r, int fu_c, int kfu,
                      const double* wu, const double* fv, int fv_r, int fv_c, int kfv,
                      const double* wv, LevelStats& st);
-  void rebase(int c, BU& bu, BU& bv, int partner);
-  void redirect(int cj, int ck, const FillFac* f_kj, const FillFac* f_jk, LevelStats& st);
-  void eliminate(int c, LevelStats& st);
+  struct RebaseReq {
+    int c, partner;
+    BU* bu;
+    BU* bv;
+  };
+  void rebase_many(std::vector<RebaseReq>& reqs);
+  struct PairJob {
+    int cj, ck;
+    const FillFac* f_kj;
+    const FillFac* f_jk;
+    bool ej = false, ek = false;
+    int r1 = 0, r2 = 0;
+    BU uj, vj, uk, vk;  // live-dead: (uj, vj) belong to the live cluster
+    Blk old_kj, old_jk;
+    bool has_kj = false, has_jk = false;
+  };
+  bool exact_order = false;
+  void process_pairs(std::vector<PairJob>& pairs, LevelStats& st);
+  void run_wave(std::vector<PairJob*>& jobs, LevelStats& st);
+  void eliminate_wave(const std::vector<int>& cs, LevelStats& st);
   void merge(int level);
   void top();
 };
@@ -353,339 +359,498 @@ void Eliminator::finish_unions(int c, BU& bu, BU& bv, const double* fu, int fu_r
   }
 }
 
-// _apply_rebase (factor.py:395-430)
-void Eliminator::rebase(int c, BU& bu, BU& bv, int partner) {
+// _apply_rebase (factor.py:395-430) for every cluster of one pair wave.
+// Row-side updates r E of all clusters run first, then column-side updates
+// E t^T read the already row-updated blocks, so an edge between two clusters
+// of the wave receives r_j E t_l^T (the reference applies the same two
+// products in pair order; matrix products associate).
+void Eliminator::rebase_many(std::vector<RebaseReq>& reqs) {
   Phase ph(C, PH_REBASE);
-  if (FILE* tf = trace_file()) fprintf(tf, "R %d %d %d %d\n", c, bu.k_old, bu.rank, bv.rank);
-  const int nxn = g.nx[c], nzn = g.nz[c], nyn = g.ny[c];
-  const int py = g.ny[partner];
-  const int m = g.size[nxn];
-  const int kn = bu.rank, ko = bu.k_old;
-  IFMM_ASSERT(bu.rank == bv.rank, "unequal U/V ranks in rebase");
   CopyBatch cb;
-  GemmBatch gb;
-  // new U (m x kn row-major) and V^T (kn x m row-major)
-  if (!bu.identity || kn != ko) {
-    Blk nu = C.alloc(m, kn);
-    cb.add(bu.NB.p, 1, m, nu.p, kn, 1, m, kn, 0);
-    g.set(nxn, nzn, nu);
-  }
-  if (!bv.identity || kn != ko) {
-    Blk nv = C.alloc(kn, m);
-    cb.add(bv.NB.p, m, 1, nv.p, m, 1, kn, m, 0);
-    g.set(nzn, nxn, nv);
-  }
-  if (!bu.identity || kn != ko) {
-    Blk w = C.alloc(1, kn);
-    cb.add(bu.NW.p, 1, 1, w.p, 1, 1, 1, kn, 0);
-    C.free(g.su[c]);
-    g.su[c] = w;
-  }
-  if (!bv.identity || kn != ko) {
-    Blk w = C.alloc(1, kn);
-    cb.add(bv.NW.p, 1, 1, w.p, 1, 1, 1, kn, 0);
-    C.free(g.sv[c]);
-    g.sv[c] = w;
-  }
-  IFMM_ASSERT(!g.get(nyn, nyn), "live cluster with a y-y self edge");
-  const bool rid = bu.identity && kn == ko, tid = bv.identity && kn == ko;
-  if (!rid) {
-    std::vector<int> rs(g.rows[nyn].begin(), g.rows[nyn].end());
-    for (int b : rs) {
-      if (b == nzn || b == py) continue;
-      const Blk E = *g.get(nyn, b);
-      Blk nb = C.alloc(kn, E.c);
-      gb.add(bu.OM.p, ko, 0, E.p, E.c, 0, nb.p, E.c, kn, E.c, ko, 1.0, 0.0);
-      g.set(nyn, b, nb);
+  GemmBatch rowg, colg;
+  for (auto& q : reqs) {
+    const int c = q.c;
+    BU& bu = *q.bu;
+    BU& bv = *q.bv;
+    const int nxn = g.nx[c], nzn = g.nz[c], nyn = g.ny[c];
+    const int py = g.ny[q.partner];
+    const int m = g.size[nxn];
+    const int kn = bu.rank, ko = bu.k_old;
+    IFMM_ASSERT(bu.rank == bv.rank, "unequal U/V ranks in rebase");
+    if (FILE* tf = trace_file()) fprintf(tf, "R %d %d %d %d\n", c, ko, bu.rank, bv.rank);
+    if (!bu.identity || kn != ko) {
+      Blk nu = C.alloc(m, kn);
+      cb.add(bu.NB.p, 1, m, nu.p, kn, 1, m, kn, 0);
+      g.set(nxn, nzn, nu);
+      Blk w = C.alloc(1, kn);
+      cb.add(bu.NW.p, 1, 1, w.p, 1, 1, 1, kn, 0);
+      C.free(g.su[c]);
+      g.su[c] = w;
     }
-  }
-  if (!tid) {
-    std::vector<int> cs(g.cols[nyn].begin(), g.cols[nyn].end());
-    for (int a : cs) {
-      if (a == nzn || a == py) continue;
-      const Blk E = *g.get(a, nyn);
-      Blk nb = C.alloc(E.r, kn);
-      gb.add(E.p, E.c, 0, bv.OM.p, ko, 1, nb.p, kn, E.r, kn, ko, 1.0, 0.0);
-      g.set(a, nyn, nb);
+    if (!bv.identity || kn != ko) {
+      Blk nv = C.alloc(kn, m);
+      cb.add(bv.NB.p, m, 1, nv.p, m, 1, kn, m, 0);
+      g.set(nzn, nxn, nv);
+      Blk w = C.alloc(1, kn);
+      cb.add(bv.NW.p, 1, 1, w.p, 1, 1, 1, kn, 0);
+      C.free(g.sv[c]);
+      g.sv[c] = w;
     }
-  }
-  cb.run(C);
-  run_gemm(gb);
-  Blk e1 = g.take(nzn, nyn), e2 = g.take(nyn, nzn);
-  C.free(e1); C.free(e2);
-  g.size[nzn] = kn;
-  g.size[nyn] = kn;
-  Blk a = C.alloc(kn, kn), b2 = C.alloc(kn, kn);
-  CopyBatch ce;
-  ce.eye(a, -1.0);
-  ce.eye(b2, -1.0);
-  ce.run(C);
-  g.set(nzn, nyn, a);
-  g.set(nyn, nzn, b2);
-  if (!rid) {
-    // keep r (kn x ko) for the solve replay
-    Blk r = C.alloc(kn, ko);
-    CopyBatch cr;
-    cr.add(bu.OM.p, ko, 1, r.p, ko, 1, kn, ko, 0);
-    cr.run(C);
-    F.rebases.push_back({nyn, r});
-    F.events.push_back({1, (int)F.rebases.size() - 1});
-  }
-}
-
-// redirect_fillin (factor.py:433-522)
-void Eliminator::redirect(int cj, int ck, const FillFac* f_kj, const FillFac* f_jk,
-                          LevelStats& st) {
-  const bool ej = g.dead[cj], ek = g.dead[ck];
-  IFMM_ASSERT(!(ej && ek), "both-eliminated fills are added, not redirected");
-  const int r1 = f_kj ? f_kj->rank : 0;
-  const int r2 = f_jk ? f_jk->rank : 0;
-  if (r1 == 0 && r2 == 0) {
-    st.dropped++;
-    if (FILE* tf = trace_file()) fprintf(tf, "D %d %d\n", cj, ck);
-    return;
-  }
-  st.compressed++;
-  st.ranks.push_back(std::max(r1, r2));
-  if (FILE* tf = trace_file()) fprintf(tf, "P %d %d %d %d %d %d\n", cj, ck, r1, r2, (int)ej, (int)ek);
-  const int yj = g.ny[cj], yk = g.ny[ck];
-  Blk* pkj = g.get(yk, yj);
-  Blk* pjk = g.get(yj, yk);
-  Blk old_kj = pkj ? *pkj : Blk();
-  Blk old_jk = pjk ? *pjk : Blk();
-  const bool has_kj = pkj != nullptr, has_jk = pjk != nullptr;
-  // keep old blocks alive through the rebases (set() on partner edges
-  // happens only below)
-  if (!ej && !ek) {
-    BU uj, vj, uk, vk;
-    std::vector<UReq> pend;
-    // j: U-fill = U(F_jk) (m_j x r2, w s_jk); V-fill = V(F_kj) (m_j x r1, w s_kj)
-    const double* Ujk = r2 ? f_jk->U : nullptr; const int ldUjk = r2 ? f_jk->m : 0;
-    const double* Vkj = r1 ? f_kj->V : nullptr; const int ldVkj = r1 ? f_kj->n : 0;
-    const double* Ukj = r1 ? f_kj->U : nullptr; const int ldUkj = r1 ? f_kj->m : 0;
-    const double* Vjk = r2 ? f_jk->V : nullptr; const int ldVjk = r2 ? f_jk->n : 0;
-    const double* sjk = r2 ? f_jk->S : nullptr;
-    const double* skj = r1 ? f_kj->S : nullptr;
-    cluster_unions(cj, Ujk, 1, ldUjk, r2, sjk, Vkj, 1, ldVkj, r1, skj, uj, vj, st, pend);
-    cluster_unions(ck, Ukj, 1, ldUkj, r1, skj, Vjk, 1, ldVjk, r2, sjk, uk, vk, st, pend);
-    launch_unions(pend);
-    finish_unions(cj, uj, vj, Ujk, 1, ldUjk, r2, sjk, Vkj, 1, ldVkj, r1, skj, st);
-    finish_unions(ck, uk, vk, Ukj, 1, ldUkj, r1, skj, Vjk, 1, ldVjk, r2, sjk, st);
-    const int kjo = g.size[yj], kko = g.size[yk];
-    rebase(cj, uj, vj, ck);
-    rebase(ck, uk, vk, cj);
-    const int kjn = uj.rank, kkn = uk.rank;
-    // new_kj = rk old_kj tj^T + (rk' s_kj) tj'^T   (kkn x kjn)
-    // new_jk = rj old_jk tk^T + (rj' s_jk) tk'^T   (kjn x kkn)
-    Blk nkj = C.alloc(kkn, kjn), njk = C.alloc(kjn, kkn);
-    Blk t1 = has_kj ? C.alloc(kko, kjn) : Blk(), t2 = has_jk ? C.alloc(kjo, kkn) : Blk();
-    GemmBatch ga, gb2, gc;
-    if (has_kj) {
-      ga.add(old_kj.p, kjo, 0, vj.OM.p, kjo, 1, t1.p, kjn, kko, kjn, kjo, 1.0, 0.0);
-      gb2.add(uk.OM.p, kko, 0, t1.p, kjn, 0, nkj.p, kjn, kkn, kjn, kko, 1.0, 0.0);
-    }
-    if (has_jk) {
-      ga.add(old_jk.p, kko, 0, vk.OM.p, kko, 1, t2.p, kkn, kjo, kkn, kko, 1.0, 0.0);
-      gb2.add(uj.OM.p, kjo, 0, t2.p, kkn, 0, njk.p, kkn, kjn, kkn, kjo, 1.0, 0.0);
-    }
-    if (r1 > 0)
-      gc.add(uk.FM.p, uk.k_f, 0, vj.FM.p, vj.k_f, 1, nkj.p, kjn, kkn, kjn, r1, 1.0,
-             has_kj ? 1.0 : 0.0, skj);
-    if (r2 > 0)
-      gc.add(uj.FM.p, uj.k_f, 0, vk.FM.p, vk.k_f, 1, njk.p, kkn, kjn, kkn, r2, 1.0,
-             has_jk ? 1.0 : 0.0, sjk);
-    Phase ph(C, PH_NEWK);
-    CopyBatch z;
-    if (!has_kj && r1 == 0) z.zero(nkj);
-    if (!has_jk && r2 == 0) z.zero(njk);
-    z.run(C);
-    run_gemm(ga);
-    run_gemm(gb2);
-    run_gemm(gc);
-    g.set(yk, yj, nkj);
-    g.set(yj, yk, njk);
-    C.free(t1); C.free(t2);
-    for (BU* b : {&uj, &vj, &uk, &vk}) free_bu(*b);
-  } else {
-    const int live = ej ? ck : cj, deadc = ej ? cj : ck;
-    const FillFac* fu = ej ? f_kj : f_jk;  // rows on x_live, cols on y_dead
-    const FillFac* fv = ej ? f_jk : f_kj;  // rows on y_dead, cols on x_live
-    const int ru = fu ? fu->rank : 0, rv = fv ? fv->rank : 0;
-    const int nd = g.size[g.ny[deadc]];
-    BU bu, bv;
-    std::vector<UReq> pend;
-    const double* Ul = ru ? fu->U : nullptr; const int ldUl = ru ? fu->m : 0;
-    const double* sl = ru ? fu->S : nullptr;
-    const double* Wl = ru ? fu->V : nullptr;  // nd x ru col-major (ld fu->n == nd)
-    const double* Ud = rv ? fv->U : nullptr;  // nd x rv col-major (ld fv->m == nd)
-    const double* sd = rv ? fv->S : nullptr;
-    const double* Vl = rv ? fv->V : nullptr; const int ldVl = rv ? fv->n : 0;
-    cluster_unions(live, Ul, 1, ldUl, ru, sl, Vl, 1, ldVl, rv, sd, bu, bv, st, pend);
-    launch_unions(pend);
-    finish_unions(live, bu, bv, Ul, 1, ldUl, ru, sl, Vl, 1, ldVl, rv, sd, st);
-    const int klo = g.size[g.ny[live]];
-    rebase(live, bu, bv, deadc);
-    const int kln = bu.rank;
-    const int ylive = g.ny[live], ydead = g.ny[deadc];
-    const bool live_is_k = live == ck;
-    const Blk old_ld = live_is_k ? old_kj : old_jk;  // (y_live, y_dead): klo x nd
-    const Blk old_dl = live_is_k ? old_jk : old_kj;  // (y_dead, y_live): nd x klo
-    const bool has_ld = live_is_k ? has_kj : has_jk;
-    const bool has_dl = live_is_k ? has_jk : has_kj;
-    Blk nld = C.alloc(kln, nd), ndl = C.alloc(nd, kln);
-    GemmBatch ga, gb2;
-    if (has_ld) ga.add(bu.OM.p, klo, 0, old_ld.p, nd, 0, nld.p, nd, kln, nd, klo, 1.0, 0.0);
-    if (has_dl) ga.add(old_dl.p, klo, 0, bv.OM.p, klo, 1, ndl.p, kln, nd, kln, klo, 1.0, 0.0);
-    if (ru > 0)
-      gb2.add(bu.FM.p, bu.k_f, 0, Wl, nd, 0, nld.p, nd, kln, nd, ru, 1.0, has_ld ? 1.0 : 0.0, sl);
-    if (rv > 0)
-      gb2.add(Ud, nd, 1, bv.FM.p, bv.k_f, 1, ndl.p, kln, nd, kln, rv, 1.0, has_dl ? 1.0 : 0.0,
-              sd);
-    Phase ph(C, PH_NEWK);
-    CopyBatch z;
-    if (!has_ld && ru == 0) z.zero(nld);
-    if (!has_dl && rv == 0) z.zero(ndl);
-    z.run(C);
-    run_gemm(ga);
-    run_gemm(gb2);
-    g.set(ylive, ydead, nld);
-    g.set(ydead, ylive, ndl);
-    free_bu(bu);
-    free_bu(bv);
-  }
-}
-
-// _eliminate_cluster (factor.py:259-326)
-void Eliminator::eliminate(int c, LevelStats& st) {
-  if (FILE* tf = trace_file()) fprintf(tf, "E %d %d %d\n", c, g.size[g.nx[c]], g.size[g.nz[c]]);
-  const int nxn = g.nx[c], nzn = g.nz[c], nyn = g.ny[c];
-  const int m = g.size[nxn], k = g.size[nzn], n = m + k;
-  Blk D = g.take(nxn, nxn);
-  Blk U = g.take(nxn, nzn);
-  Blk Vt = g.take(nzn, nxn);
-  Blk e1 = g.take(nzn, nyn), e2 = g.take(nyn, nzn);
-  C.free(e1); C.free(e2);
-  Blk P = C.alloc(n, n);
-  Phase* ph = new Phase(C, PH_LU);
-  {
-    CopyBatch cb;
-    cb.copy(D, P, 0, 0);
-    cb.copy(U, P, 0, m);
-    cb.copy(Vt, P, m, 0);
-    cb.add(nullptr, 0, 0, P.p + (size_t)m * n + m, n, 1, k, k, 3);
-    cb.run(C);
-  }
-  C.free(D); C.free(U); C.free(Vt);
-  int pc;
-  int* piv = C.arena.alloc_int(n, &pc);
-  lu_any(C, P.p, n, piv, c);
-  flops_gemm += 2.0 / 3.0 * (double)n * n * n;
-  flops_all += 2.0 / 3.0 * (double)n * n * n;
-  delete ph;
-  ph = new Phase(C, PH_XSOLVE);
-
-  ElimEv ev;
-  ev.nx = nxn; ev.nz = nzn; ev.ny = nyn; ev.m = m; ev.k = k;
-  ev.LU = P; ev.piv = piv; ev.piv_cls = pc;
-  std::vector<Blk> srcB, tgtB;
-  int Csrc = 0, Rtgt = 0;
-  for (int b : std::vector<int>(g.rows[nxn].begin(), g.rows[nxn].end())) {
-    Blk E = g.take(nxn, b);
-    ev.src.push_back(b); ev.src_off.push_back(Csrc); ev.src_w.push_back(E.c);
-    Csrc += E.c;
-    srcB.push_back(E);
-  }
-  for (int a : std::vector<int>(g.cols[nxn].begin(), g.cols[nxn].end())) {
-    Blk E = g.take(a, nxn);
-    ev.tgt.push_back(a); ev.tgt_off.push_back(Rtgt); ev.tgt_h.push_back(E.r);
-    Rtgt += E.r;
-    tgtB.push_back(E);
-  }
-  IFMM_ASSERT(g.rows[nzn].empty() && g.cols[nzn].empty(), "z node unexpectedly has extra edges");
-  ev.Scat = C.alloc(m, std::max(Csrc, 1));
-  ev.Tstk = C.alloc(std::max(Rtgt, 1), m);
-  const int NC = Csrc + k, NR = Rtgt + k;
-  Blk X = C.alloc(n, NC);
-  {
-    CopyBatch cb;
-    for (size_t i = 0; i < srcB.size(); ++i) {
-      cb.add(srcB[i].p, srcB[i].c, 1, ev.Scat.p + ev.src_off[i], std::max(Csrc, 1), 1, m,
-             srcB[i].c, 0);
-      cb.add(srcB[i].p, srcB[i].c, 1, X.p + ev.src_off[i], NC, 1, m, srcB[i].c, 0);
-    }
-    for (size_t i = 0; i < tgtB.size(); ++i)
-      cb.add(tgtB[i].p, tgtB[i].c, 1, ev.Tstk.p + (size_t)ev.tgt_off[i] * m, m, 1, tgtB[i].r, m,
-             0);
-    cb.add(nullptr, 0, 0, X.p + (size_t)m * NC, NC, 1, k, Csrc, 3);   // 0 below sources
-    cb.add(nullptr, 0, 0, X.p + Csrc, NC, 1, m, k, 3);                // 0 above -I
-    cb.add(nullptr, 0, 0, X.p + (size_t)m * NC + Csrc, NC, 1, k, k, 2, -1.0);  // -I
-    cb.run(C);
-  }
-  for (auto& b : srcB) C.free(b);
-  for (auto& b : tgtB) C.free(b);
-  g.dead[c] = 1;
-
-  lusolve(C, P.p, piv, n, X.p, NC);
-  flops_gemm += 2.0 * n * n * (double)NC;
-  flops_all += 2.0 * n * n * (double)NC;
-  delete ph;
-  ph = new Phase(C, PH_SCHUR);
-
-  // Schur fill: F = [-Tstk X[:m] ; X[m:]]   (NR x NC)
-  Blk Fm = C.alloc(NR, NC);
-  {
-    GemmBatch gb;
-    gb.add(ev.Tstk.p, m, 0, X.p, NC, 0, Fm.p, NC, Rtgt, NC, m, -1.0, 0.0);
-    run_gemm(gb);
-    CopyBatch cb;
-    cb.add(X.p + (size_t)m * NC, NC, 1, Fm.p + (size_t)Rtgt * NC, NC, 1, k, NC, 0);
-    cb.run(C);
-  }
-  C.free(X);
-
-  delete ph;
-  ph = new Phase(C, PH_ADD);
-  F.elims.push_back(std::move(ev));
-  F.events.push_back({0, (int)F.elims.size() - 1});
-  const ElimEv& E = F.elims.back();
-
-  // classification (factor.py:301-318)
-  std::vector<int> A_nodes(E.tgt), A_off(E.tgt_off), A_h(E.tgt_h);
-  A_nodes.push_back(nyn); A_off.push_back(Rtgt); A_h.push_back(k);
-  std::vector<int> B_nodes(E.src), B_off(E.src_off), B_w(E.src_w);
-  B_nodes.push_back(nyn); B_off.push_back(Csrc); B_w.push_back(k);
-  struct Stash { int ro, co, h, w; };
-  std::map<std::pair<int, int>, Stash> stash;
-  CopyBatch adds;
-  for (size_t ai = 0; ai < A_nodes.size(); ++ai) {
-    const int a = A_nodes[ai], ca = g.owner[a];
-    for (size_t bi = 0; bi < B_nodes.size(); ++bi) {
-      const int b = B_nodes[bi], cbc = g.owner[b];
-      const double* sub = Fm.p + (size_t)A_off[ai] * NC + B_off[bi];
-      if ((g.dead[ca] && g.dead[cbc]) || g.tree->adjacent(ca, cbc)) {
-        Blk* ex = g.get(a, b);
-        if (ex) {
-          IFMM_ASSERT(ex->r == A_h[ai] && ex->c == B_w[bi], "fill shape mismatch");
-          adds.add(sub, NC, 1, ex->p, ex->c, 1, A_h[ai], B_w[bi], 1);
-        } else {
-          Blk nb = C.alloc(A_h[ai], B_w[bi]);
-          adds.add(sub, NC, 1, nb.p, nb.c, 1, A_h[ai], B_w[bi], 0);
-          g.set(a, b, nb);
-        }
-        st.added++;
-      } else {
-        stash[{ca, cbc}] = {A_off[ai], B_off[bi], A_h[ai], B_w[bi]};
+    IFMM_ASSERT(!g.get(nyn, nyn), "live cluster with a y-y self edge");
+    if (!(bu.identity && kn == ko)) {
+      std::vector<int> rs(g.rows[nyn].begin(), g.rows[nyn].end());
+      for (int b : rs) {
+        if (b == nzn || b == py) continue;
+        const Blk E = *g.get(nyn, b);
+        Blk nb = C.alloc(kn, E.c);
+        rowg.add(bu.OM.p, ko, 0, E.p, E.c, 0, nb.p, E.c, kn, E.c, ko, 1.0, 0.0);
+        g.set(nyn, b, nb);
       }
     }
   }
-  adds.run(C);
-  delete ph;
-  ph = nullptr;
+  cb.run(C);
+  run_gemm(rowg);
+  for (auto& q : reqs) {
+    const int c = q.c;
+    BU& bu = *q.bu;
+    BU& bv = *q.bv;
+    const int nzn = g.nz[c], nyn = g.ny[c];
+    const int py = g.ny[q.partner];
+    const int kn = bu.rank, ko = bu.k_old;
+    if (!(bv.identity && kn == ko)) {
+      std::vector<int> cs(g.cols[nyn].begin(), g.cols[nyn].end());
+      for (int a : cs) {
+        if (a == nzn || a == py) continue;
+        const Blk E = *g.get(a, nyn);
+        Blk nb = C.alloc(E.r, kn);
+        colg.add(E.p, E.c, 0, bv.OM.p, ko, 1, nb.p, kn, E.r, kn, ko, 1.0, 0.0);
+        g.set(a, nyn, nb);
+      }
+    }
+  }
+  run_gemm(colg);
+  CopyBatch ce;
+  for (auto& q : reqs) {
+    const int c = q.c;
+    BU& bu = *q.bu;
+    const int nzn = g.nz[c], nyn = g.ny[c];
+    const int kn = bu.rank, ko = bu.k_old;
+    Blk e1 = g.take(nzn, nyn), e2 = g.take(nyn, nzn);
+    C.free(e1); C.free(e2);
+    g.size[nzn] = kn;
+    g.size[nyn] = kn;
+    Blk a = C.alloc(kn, kn), b2 = C.alloc(kn, kn);
+    ce.eye(a, -1.0);
+    ce.eye(b2, -1.0);
+    g.set(nzn, nyn, a);
+    g.set(nyn, nzn, b2);
+    if (!(bu.identity && kn == ko)) {
+      Blk r = C.alloc(kn, ko);  // r (kn x ko) kept for the solve replay
+      ce.add(bu.OM.p, ko, 1, r.p, ko, 1, kn, ko, 0);
+      F.rebases.push_back({nyn, r});
+      F.events.push_back({1, (int)F.rebases.size() - 1});
+    }
+  }
+  ce.run(C);
+}
 
-  if (!stash.empty()) {
-    Phase* ps = new Phase(C, PH_FILLSVD);
-    // compress every stashed fill in one batched Jacobi SVD launch
-    std::vector<std::pair<std::pair<int, int>, Stash>> items(stash.begin(), stash.end());
+// redirect_fillin (factor.py:433-522) for a list of fill pairs in sorted
+// (min, max) order.  Dropped pairs only count; compressed pairs are grouped
+// into waves of cluster-disjoint pairs (a pair's wave is one past the last
+// wave that touched either of its clusters, so pairs sharing a cluster keep
+// the reference order) and each wave is executed with batched launches.
+void Eliminator::process_pairs(std::vector<PairJob>& pairs, LevelStats& st) {
+  std::vector<PairJob*> live;
+  for (auto& p : pairs) {
+    p.ej = g.dead[p.cj];
+    p.ek = g.dead[p.ck];
+    IFMM_ASSERT(!(p.ej && p.ek), "both-eliminated fills are added, not redirected");
+    p.r1 = p.f_kj ? p.f_kj->rank : 0;
+    p.r2 = p.f_jk ? p.f_jk->rank : 0;
+    if (p.r1 == 0 && p.r2 == 0) {
+      st.dropped++;
+      if (FILE* tf = trace_file()) fprintf(tf, "D %d %d\n", p.cj, p.ck);
+      continue;
+    }
+    st.compressed++;
+    st.ranks.push_back(std::max(p.r1, p.r2));
+    if (FILE* tf = trace_file())
+      fprintf(tf, "P %d %d %d %d %d %d\n", p.cj, p.ck, p.r1, p.r2, (int)p.ej, (int)p.ek);
+    live.push_back(&p);
+  }
+  if (live.empty()) return;
+  std::map<int, int> last;
+  std::vector<int> wave(live.size());
+  int maxw = 0;
+  for (size_t i = 0; i < live.size(); ++i) {
+    int w = 0;
+    if (exact_order) w = (int)i + 1;
+    else {
+      auto a = last.find(live[i]->cj), b = last.find(live[i]->ck);
+      if (a != last.end()) w = std::max(w, a->second);
+      if (b != last.end()) w = std::max(w, b->second);
+      w += 1;
+    }
+    last[live[i]->cj] = w;
+    last[live[i]->ck] = w;
+    wave[i] = w;
+    maxw = std::max(maxw, w);
+  }
+  std::vector<std::vector<PairJob*>> waves(maxw + 1);
+  for (size_t i = 0; i < live.size(); ++i) waves[wave[i]].push_back(live[i]);
+  for (int w = 1; w <= maxw; ++w) run_wave(waves[w], st);
+}
+
+void Eliminator::run_wave(std::vector<PairJob*>& jobs, LevelStats& st) {
+  // ---- unions of every cluster of the wave, one launch ----
+  std::vector<UReq> pend;
+  for (PairJob* pj : jobs) {
+    PairJob& p = *pj;
+    const int yj = g.ny[p.cj], yk = g.ny[p.ck];
+    Blk* pkj = g.get(yk, yj);
+    Blk* pjk = g.get(yj, yk);
+    p.has_kj = pkj != nullptr;
+    p.has_jk = pjk != nullptr;
+    if (p.has_kj) p.old_kj = *pkj;
+    if (p.has_jk) p.old_jk = *pjk;
+    const int r1 = p.r1, r2 = p.r2;
+    if (!p.ej && !p.ek) {
+      cluster_unions(p.cj, r2 ? p.f_jk->U : nullptr, 1, r2 ? p.f_jk->m : 0, r2,
+                     r2 ? p.f_jk->S : nullptr, r1 ? p.f_kj->V : nullptr, 1,
+                     r1 ? p.f_kj->n : 0, r1, r1 ? p.f_kj->S : nullptr, p.uj, p.vj, st, pend);
+      cluster_unions(p.ck, r1 ? p.f_kj->U : nullptr, 1, r1 ? p.f_kj->m : 0, r1,
+                     r1 ? p.f_kj->S : nullptr, r2 ? p.f_jk->V : nullptr, 1,
+                     r2 ? p.f_jk->n : 0, r2, r2 ? p.f_jk->S : nullptr, p.uk, p.vk, st, pend);
+    } else {
+      const int live = p.ej ? p.ck : p.cj;
+      const FillFac* fu = p.ej ? p.f_kj : p.f_jk;  // rows on x_live, cols on y_dead
+      const FillFac* fv = p.ej ? p.f_jk : p.f_kj;  // rows on y_dead, cols on x_live
+      const int ru = fu ? fu->rank : 0, rv = fv ? fv->rank : 0;
+      cluster_unions(live, ru ? fu->U : nullptr, 1, ru ? fu->m : 0, ru, ru ? fu->S : nullptr,
+                     rv ? fv->V : nullptr, 1, rv ? fv->n : 0, rv, rv ? fv->S : nullptr, p.uj,
+                     p.vj, st, pend);
+    }
+  }
+  launch_unions(pend);
+  // ---- rank equalisation (rare relaunches) ----
+  for (PairJob* pj : jobs) {
+    PairJob& p = *pj;
+    const int r1 = p.r1, r2 = p.r2;
+    if (!p.ej && !p.ek) {
+      finish_unions(p.cj, p.uj, p.vj, r2 ? p.f_jk->U : nullptr, 1, r2 ? p.f_jk->m : 0, r2,
+                    r2 ? p.f_jk->S : nullptr, r1 ? p.f_kj->V : nullptr, 1, r1 ? p.f_kj->n : 0,
+                    r1, r1 ? p.f_kj->S : nullptr, st);
+      finish_unions(p.ck, p.uk, p.vk, r1 ? p.f_kj->U : nullptr, 1, r1 ? p.f_kj->m : 0, r1,
+                    r1 ? p.f_kj->S : nullptr, r2 ? p.f_jk->V : nullptr, 1, r2 ? p.f_jk->n : 0,
+                    r2, r2 ? p.f_jk->S : nullptr, st);
+    } else {
+      const int live = p.ej ? p.ck : p.cj;
+      const FillFac* fu = p.ej ? p.f_kj : p.f_jk;
+      const FillFac* fv = p.ej ? p.f_jk : p.f_kj;
+      const int ru = fu ? fu->rank : 0, rv = fv ? fv->rank : 0;
+      finish_unions(live, p.uj, p.vj, ru ? fu->U : nullptr, 1, ru ? fu->m : 0, ru,
+                    ru ? fu->S : nullptr, rv ? fv->V : nullptr, 1, rv ? fv->n : 0, rv,
+                    rv ? fv->S : nullptr, st);
+    }
+  }
+  // ---- rebases ----
+  std::vector<int> kjo(jobs.size()), kko(jobs.size());
+  std::vector<RebaseReq> reqs;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    PairJob& p = *jobs[i];
+    kjo[i] = g.size[g.ny[p.cj]];
+    kko[i] = g.size[g.ny[p.ck]];
+    if (!p.ej && !p.ek) {
+      reqs.push_back({p.cj, p.ck, &p.uj, &p.vj});
+      reqs.push_back({p.ck, p.cj, &p.uk, &p.vk});
+    } else {
+      const int live = p.ej ? p.ck : p.cj, deadc = p.ej ? p.cj : p.ck;
+      reqs.push_back({live, deadc, &p.uj, &p.vj});
+    }
+  }
+  rebase_many(reqs);
+  // ---- K-edge rewrite ----
+  Phase ph(C, PH_NEWK);
+  GemmBatch ga, gb2, gc;
+  CopyBatch z;
+  std::vector<Blk> tmp;
+  struct Out { int t, s; Blk b; };
+  std::vector<Out> outs;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    PairJob& p = *jobs[i];
+    const int yj = g.ny[p.cj], yk = g.ny[p.ck];
+    const int r1 = p.r1, r2 = p.r2;
+    if (!p.ej && !p.ek) {
+      BU &uj = p.uj, &vj = p.vj, &uk = p.uk, &vk = p.vk;
+      const int kj0 = kjo[i], kk0 = kko[i];
+      const int kjn = uj.rank, kkn = uk.rank;
+      // new_kj = rk old_kj tj^T + (rk' s_kj) tj'^T ; new_jk = rj old_jk tk^T + (rj' s_jk) tk'^T
+      Blk nkj = C.alloc(kkn, kjn), njk = C.alloc(kjn, kkn);
+      if (p.has_kj) {
+        Blk t1 = C.alloc(kk0, kjn);
+        tmp.push_back(t1);
+        ga.add(p.old_kj.p, kj0, 0, vj.OM.p, kj0, 1, t1.p, kjn, kk0, kjn, kj0, 1.0, 0.0);
+        gb2.add(uk.OM.p, kk0, 0, t1.p, kjn, 0, nkj.p, kjn, kkn, kjn, kk0, 1.0, 0.0);
+      }
+      if (p.has_jk) {
+        Blk t2 = C.alloc(kj0, kkn);
+        tmp.push_back(t2);
+        ga.add(p.old_jk.p, kk0, 0, vk.OM.p, kk0, 1, t2.p, kkn, kj0, kkn, kk0, 1.0, 0.0);
+        gb2.add(uj.OM.p, kj0, 0, t2.p, kkn, 0, njk.p, kkn, kjn, kkn, kj0, 1.0, 0.0);
+      }
+      if (r1 > 0)
+        gc.add(uk.FM.p, uk.k_f, 0, vj.FM.p, vj.k_f, 1, nkj.p, kjn, kkn, kjn, r1, 1.0,
+               p.has_kj ? 1.0 : 0.0, p.f_kj->S);
+      if (r2 > 0)
+        gc.add(uj.FM.p, uj.k_f, 0, vk.FM.p, vk.k_f, 1, njk.p, kkn, kjn, kkn, r2, 1.0,
+               p.has_jk ? 1.0 : 0.0, p.f_jk->S);
+      if (!p.has_kj && r1 == 0) z.zero(nkj);
+      if (!p.has_jk && r2 == 0) z.zero(njk);
+      outs.push_back({yk, yj, nkj});
+      outs.push_back({yj, yk, njk});
+    } else {
+      const int live = p.ej ? p.ck : p.cj, deadc = p.ej ? p.cj : p.ck;
+      const FillFac* fu = p.ej ? p.f_kj : p.f_jk;
+      const FillFac* fv = p.ej ? p.f_jk : p.f_kj;
+      const int ru = fu ? fu->rank : 0, rv = fv ? fv->rank : 0;
+      const int nd = g.size[g.ny[deadc]];
+      BU &bu = p.uj, &bv = p.vj;
+      const int klo = bu.k_old, kln = bu.rank;
+      const bool live_is_k = live == p.ck;
+      const Blk old_ld = live_is_k ? p.old_kj : p.old_jk;  // (y_live, y_dead)
+      const Blk old_dl = live_is_k ? p.old_jk : p.old_kj;  // (y_dead, y_live)
+      const bool has_ld = live_is_k ? p.has_kj : p.has_jk;
+      const bool has_dl = live_is_k ? p.has_jk : p.has_kj;
+      Blk nld = C.alloc(kln, nd), ndl = C.alloc(nd, kln);
+      if (has_ld) ga.add(bu.OM.p, klo, 0, old_ld.p, nd, 0, nld.p, nd, kln, nd, klo, 1.0, 0.0);
+      if (has_dl) ga.add(old_dl.p, klo, 0, bv.OM.p, klo, 1, ndl.p, kln, nd, kln, klo, 1.0, 0.0);
+      if (ru > 0)
+        gb2.add(bu.FM.p, bu.k_f, 0, fu->V, nd, 0, nld.p, nd, kln, nd, ru, 1.0,
+                has_ld ? 1.0 : 0.0, fu->S);
+      if (rv > 0)
+        gb2.add(fv->U, nd, 1, bv.FM.p, bv.k_f, 1, ndl.p, kln, nd, kln, rv, 1.0,
+                has_dl ? 1.0 : 0.0, fv->S);
+      if (!has_ld && ru == 0) z.zero(nld);
+      if (!has_dl && rv == 0) z.zero(ndl);
+      outs.push_back({g.ny[live], g.ny[deadc], nld});
+      outs.push_back({g.ny[deadc], g.ny[live], ndl});
+    }
+  }
+  z.run(C);
+  run_gemm(ga);
+  run_gemm(gb2);
+  run_gemm(gc);
+  for (auto& o : outs) g.set(o.t, o.s, o.b);
+  for (auto& b : tmp) C.free(b);
+  for (PairJob* pj : jobs)
+    for (BU* b : {&pj->uj, &pj->vj, &pj->uk, &pj->vk}) free_bu(*b);
+  C.flush();
+}
+
+// _eliminate_cluster (factor.py:259-326) for a wave of clusters that are
+// pairwise at Chebyshev distance >= 3 (no shared neighbour: their
+// eliminations touch disjoint edges and commute).  Every stage is one
+// batched launch over the wave.
+void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
+  struct W {
+    int c, nx, nz, ny, m, k, n, Csrc, Rtgt, NC, NR;
+    Blk P, X, Fm;
+    int* piv;
+    int pc;
+    std::vector<Blk> srcB, tgtB;
+  };
+  std::vector<W> ws(cs.size());
+  Phase* ph = new Phase(C, PH_LU);
+  // ---- pivot blocks P = [[D, U], [V^T, 0]] and their LU ----
+  {
+    CopyBatch cb;
+    std::vector<Blk> dead_blks;
+    for (size_t i = 0; i < cs.size(); ++i) {
+      W& w = ws[i];
+      w.c = cs[i];
+      if (FILE* tf = trace_file())
+        fprintf(tf, "E %d %d %d\n", w.c, g.size[g.nx[w.c]], g.size[g.nz[w.c]]);
+      w.nx = g.nx[w.c]; w.nz = g.nz[w.c]; w.ny = g.ny[w.c];
+      w.m = g.size[w.nx]; w.k = g.size[w.nz]; w.n = w.m + w.k;
+      Blk D = g.take(w.nx, w.nx), U = g.take(w.nx, w.nz), Vt = g.take(w.nz, w.nx);
+      Blk e1 = g.take(w.nz, w.ny), e2 = g.take(w.ny, w.nz);
+      w.P = C.alloc(w.n, w.n);
+      cb.copy(D, w.P, 0, 0);
+      cb.copy(U, w.P, 0, w.m);
+      cb.copy(Vt, w.P, w.m, 0);
+      cb.add(nullptr, 0, 0, w.P.p + (size_t)w.m * w.n + w.m, w.n, 1, w.k, w.k, 3);
+      for (Blk b : {D, U, Vt, e1, e2}) dead_blks.push_back(b);
+      w.piv = C.arena.alloc_int(w.n, &w.pc);
+    }
+    cb.run(C);
+    for (auto& b : dead_blks) C.free(b);
+    std::vector<LuDesc> small;
+    double fl = 0;
+    for (W& w : ws) {
+      const double f3 = 2.0 / 3.0 * (double)w.n * w.n * w.n;
+      flops_gemm += f3;
+      flops_all += f3;
+      if (w.n <= 160) {
+        LuDesc d;
+        d.A = w.P.p; d.n = w.n; d.lda = w.n; d.piv = w.piv; d.tag = w.c;
+        small.push_back(d);
+        fl += f3;
+      } else {
+        lu_blocked(C, w.P.p, w.n, w.n, w.piv, w.c);
+      }
+    }
+    if (!small.empty()) {
+      LuDesc* dd = C.stage.push_vec(C, small);
+      cudaEvent_t ka = nullptr;
+      C.kt_begin(K_LU, fl, &ka);
+      launch_lu(dd, (int)small.size(), C.d_status, C.st);
+      C.kt_end(K_LU, fl, ka);
+      C.launches++;
+      CUDA_CHECK(cudaGetLastError());
+    }
+  }
+  delete ph;
+  ph = new Phase(C, PH_XSOLVE);
+  // ---- sources / targets, event records, X = P^{-1}[E(x,b);0 | 0;-I] ----
+  {
+    CopyBatch cb;
+    std::vector<LuSolveDesc> sd;
+    int max_nrhs = 0, max_n = 0;
+    double fl = 0;
+    for (W& w : ws) {
+      ElimEv ev;
+      ev.nx = w.nx; ev.nz = w.nz; ev.ny = w.ny; ev.m = w.m; ev.k = w.k;
+      ev.LU = w.P; ev.piv = w.piv; ev.piv_cls = w.pc;
+      w.Csrc = 0; w.Rtgt = 0;
+      for (int b : std::vector<int>(g.rows[w.nx].begin(), g.rows[w.nx].end())) {
+        Blk E = g.take(w.nx, b);
+        ev.src.push_back(b); ev.src_off.push_back(w.Csrc); ev.src_w.push_back(E.c);
+        w.Csrc += E.c;
+        w.srcB.push_back(E);
+      }
+      for (int a : std::vector<int>(g.cols[w.nx].begin(), g.cols[w.nx].end())) {
+        Blk E = g.take(a, w.nx);
+        ev.tgt.push_back(a); ev.tgt_off.push_back(w.Rtgt); ev.tgt_h.push_back(E.r);
+        w.Rtgt += E.r;
+        w.tgtB.push_back(E);
+      }
+      IFMM_ASSERT(g.rows[w.nz].empty() && g.cols[w.nz].empty(),
+                  "z node unexpectedly has extra edges");
+      const int m = w.m, k = w.k, Csrc = w.Csrc;
+      ev.Scat = C.alloc(m, std::max(Csrc, 1));
+      ev.Tstk = C.alloc(std::max(w.Rtgt, 1), m);
+      w.NC = Csrc + k;
+      w.NR = w.Rtgt + k;
+      w.X = C.alloc(w.n, w.NC);
+      const int NC = w.NC;
+      for (size_t i = 0; i < w.srcB.size(); ++i) {
+        cb.add(w.srcB[i].p, w.srcB[i].c, 1, ev.Scat.p + ev.src_off[i], std::max(Csrc, 1), 1, m,
+               w.srcB[i].c, 0);
+        cb.add(w.srcB[i].p, w.srcB[i].c, 1, w.X.p + ev.src_off[i], NC, 1, m, w.srcB[i].c, 0);
+      }
+      for (size_t i = 0; i < w.tgtB.size(); ++i)
+        cb.add(w.tgtB[i].p, w.tgtB[i].c, 1, ev.Tstk.p + (size_t)ev.tgt_off[i] * m, m, 1,
+               w.tgtB[i].r, m, 0);
+      cb.add(nullptr, 0, 0, w.X.p + (size_t)m * NC, NC, 1, k, Csrc, 3);
+      cb.add(nullptr, 0, 0, w.X.p + Csrc, NC, 1, m, k, 3);
+      cb.add(nullptr, 0, 0, w.X.p + (size_t)m * NC + Csrc, NC, 1, k, k, 2, -1.0);
+      g.dead[w.c] = 1;
+      LuSolveDesc d;
+      d.LU = w.P.p; d.piv = w.piv; d.n = w.n; d.lda = w.n; d.X = w.X.p; d.nrhs = NC; d.ldx = NC;
+      sd.push_back(d);
+      max_nrhs = std::max(max_nrhs, NC);
+      max_n = std::max(max_n, w.n);
+      const double f2 = 2.0 * w.n * w.n * (double)NC;
+      flops_gemm += f2;
+      flops_all += f2;
+      fl += f2;
+      F.elims.push_back(std::move(ev));
+      F.events.push_back({0, (int)F.elims.size() - 1});
+    }
+    cb.run(C);
+    for (W& w : ws) {
+      for (auto& b : w.srcB) C.free(b);
+      for (auto& b : w.tgtB) C.free(b);
+    }
+    LuSolveDesc* dd = C.stage.push_vec(C, sd);
+    cudaEvent_t ka = nullptr;
+    C.kt_begin(K_LUSOLVE, fl, &ka);
+    launch_lusolve(dd, (int)sd.size(), max_nrhs, C.st, max_n);
+    C.kt_end(K_LUSOLVE, fl, ka);
+    C.launches++;
+    CUDA_CHECK(cudaGetLastError());
+  }
+  delete ph;
+  ph = new Phase(C, PH_SCHUR);
+  // ---- Schur fill F = [-Tstk X[:m] ; X[m:]]  (NR x NC), one grouped GEMM ----
+  const size_t e0 = F.elims.size() - ws.size();
+  {
+    GemmBatch gb;
+    CopyBatch cb;
+    for (size_t i = 0; i < ws.size(); ++i) {
+      W& w = ws[i];
+      const ElimEv& ev = F.elims[e0 + i];
+      w.Fm = C.alloc(w.NR, w.NC);
+      gb.add(ev.Tstk.p, w.m, 0, w.X.p, w.NC, 0, w.Fm.p, w.NC, w.Rtgt, w.NC, w.m, -1.0, 0.0);
+      cb.add(w.X.p + (size_t)w.m * w.NC, w.NC, 1, w.Fm.p + (size_t)w.Rtgt * w.NC, w.NC, 1, w.k,
+             w.NC, 0);
+    }
+    run_gemm(gb);
+    cb.run(C);
+    for (W& w : ws) C.free(w.X);
+  }
+  delete ph;
+  ph = new Phase(C, PH_ADD);
+  // ---- classification (factor.py:301-318) ----
+  struct Stash { int wi, ro, co, h, w; };
+  std::vector<std::map<std::pair<int, int>, Stash>> stash(ws.size());
+  {
+    CopyBatch adds;
+    for (size_t wi = 0; wi < ws.size(); ++wi) {
+      W& w = ws[wi];
+      const ElimEv& E = F.elims[e0 + wi];
+      std::vector<int> A_nodes(E.tgt), A_off(E.tgt_off), A_h(E.tgt_h);
+      A_nodes.push_back(w.ny); A_off.push_back(w.Rtgt); A_h.push_back(w.k);
+      std::vector<int> B_nodes(E.src), B_off(E.src_off), B_w(E.src_w);
+      B_nodes.push_back(w.ny); B_off.push_back(w.Csrc); B_w.push_back(w.k);
+      const int NC = w.NC;
+      for (size_t ai = 0; ai < A_nodes.size(); ++ai) {
+        const int a = A_nodes[ai], ca = g.owner[a];
+        for (size_t bi = 0; bi < B_nodes.size(); ++bi) {
+          const int b = B_nodes[bi], cbc = g.owner[b];
+          const double* sub = w.Fm.p + (size_t)A_off[ai] * NC + B_off[bi];
+          if ((g.dead[ca] && g.dead[cbc]) || g.tree->adjacent(ca, cbc)) {
+            Blk* ex = g.get(a, b);
+            if (ex) {
+              IFMM_ASSERT(ex->r == A_h[ai] && ex->c == B_w[bi], "fill shape mismatch");
+              adds.add(sub, NC, 1, ex->p, ex->c, 1, A_h[ai], B_w[bi], 1);
+            } else {
+              Blk nb = C.alloc(A_h[ai], B_w[bi]);
+              adds.add(sub, NC, 1, nb.p, nb.c, 1, A_h[ai], B_w[bi], 0);
+              g.set(a, b, nb);
+            }
+            st.added++;
+          } else {
+            stash[wi][{ca, cbc}] = {(int)wi, A_off[ai], B_off[bi], A_h[ai], B_w[bi]};
+          }
+        }
+      }
+    }
+    adds.run(C);
+  }
+  delete ph;
+  // ---- fill compression of every stashed block of the wave, one launch ----
+  std::vector<std::pair<std::pair<int, int>, Stash>> items;
+  std::vector<size_t> first(ws.size() + 1, 0);
+  for (size_t wi = 0; wi < ws.size(); ++wi) {
+    first[wi] = items.size();
+    for (auto& kv : stash[wi]) items.push_back(kv);
+  }
+  first[ws.size()] = items.size();
+  std::vector<FillFac> fac(items.size());
+  Blk wsb;
+  if (!items.empty()) {
+    Phase ps(C, PH_FILLSVD);
     const int ns = (int)items.size();
     int maxdim = 0;
     for (auto& it : items) maxdim = std::max(maxdim, std::max(it.second.h, it.second.w));
@@ -693,6 +858,7 @@ void Eliminator::eliminate(int c, LevelStats& st) {
     const size_t smem_d = svd_smem_doubles(smem_dim);
     size_t tot = 0;
     std::vector<size_t> uo(ns), so(ns), vo(ns), wo(ns);
+    double sflops = 0;
     for (int i = 0; i < ns; ++i) {
       const Stash& s = items[i].second;
       const int mn = std::min(s.h, s.w);
@@ -701,25 +867,21 @@ void Eliminator::eliminate(int c, LevelStats& st) {
       vo[i] = tot; tot += (size_t)s.w * mn;
       wo[i] = tot;
       if (svd_work_doubles(s.h, s.w) > smem_d) tot += svd_work_doubles(s.h, s.w);
-      const double mm = std::max(s.h, s.w), nn = std::min(s.h, s.w);
-      flops_all += 4 * mm * nn * nn + 22 * nn * nn * nn;
-    }
-    double sflops = 0;
-    for (int i = 0; i < ns; ++i) {
-      const double mm = std::max(items[i].second.h, items[i].second.w);
-      const double nn = std::min(items[i].second.h, items[i].second.w);
+      const double mm = std::max(s.h, s.w), nn = mn;
       sflops += 4 * mm * nn * nn + 22 * nn * nn * nn;
     }
-    Blk ws = C.alloc(1, (int)std::max<size_t>(tot, 1));
+    flops_all += sflops;
+    wsb = C.alloc(1, (int)std::max<size_t>(tot, 1));
     int* dr = ranks_buf(ns);
     std::vector<SvdDesc> sd(ns);
     for (int i = 0; i < ns; ++i) {
       const Stash& s = items[i].second;
-      sd[i].src = Fm.p + (size_t)s.ro * NC + s.co;
-      sd[i].m = s.h; sd[i].n = s.w; sd[i].s_r = NC; sd[i].s_c = 1;
-      sd[i].U = ws.p + uo[i]; sd[i].S = ws.p + so[i]; sd[i].V = ws.p + vo[i];
+      const W& w = ws[s.wi];
+      sd[i].src = w.Fm.p + (size_t)s.ro * w.NC + s.co;
+      sd[i].m = s.h; sd[i].n = s.w; sd[i].s_r = w.NC; sd[i].s_c = 1;
+      sd[i].U = wsb.p + uo[i]; sd[i].S = wsb.p + so[i]; sd[i].V = wsb.p + vo[i];
       sd[i].rank = dr + i;
-      sd[i].work = ws.p + wo[i];
+      sd[i].work = wsb.p + wo[i];
     }
     SvdDesc* dsd = C.stage.push_vec(C, sd);
     cudaEvent_t ka = nullptr;
@@ -729,30 +891,66 @@ void Eliminator::eliminate(int c, LevelStats& st) {
     C.launches++;
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(dr, ns);
-    std::map<std::pair<int, int>, FillFac> fac;
     for (int i = 0; i < ns; ++i) {
-      FillFac f;
-      f.U = sd[i].U; f.S = sd[i].S; f.V = sd[i].V;
-      f.m = sd[i].m; f.n = sd[i].n; f.rank = hr[i];
-      fac[items[i].first] = f;
+      fac[i].U = sd[i].U; fac[i].S = sd[i].S; fac[i].V = sd[i].V;
+      fac[i].m = sd[i].m; fac[i].n = sd[i].n; fac[i].rank = hr[i];
     }
-    delete ps;
-    std::set<std::pair<int, int>> pairs;
-    for (auto& it : items)
-      pairs.insert({std::min(it.first.first, it.first.second),
-                    std::max(it.first.first, it.first.second)});
-    for (auto& pr : pairs) {
-      const int cj = pr.first, ck = pr.second;
-      auto a = fac.find({ck, cj});
-      auto b = fac.find({cj, ck});
-      redirect(cj, ck, a == fac.end() ? nullptr : &a->second,
-               b == fac.end() ? nullptr : &b->second, st);
-    }
-    C.flush();
-    C.free(ws);
   }
-  C.free(Fm);
+  // ---- pairs of every cluster (cluster-disjoint across the wave) ----
+  std::vector<PairJob> jobs;
+  for (size_t wi = 0; wi < ws.size(); ++wi) {
+    std::map<std::pair<int, int>, const FillFac*> fm;
+    for (size_t i = first[wi]; i < first[wi + 1]; ++i) fm[items[i].first] = &fac[i];
+    std::set<std::pair<int, int>> pairs;
+    for (auto& kv : fm)
+      pairs.insert({std::min(kv.first.first, kv.first.second),
+                    std::max(kv.first.first, kv.first.second)});
+    for (auto& pr : pairs) {
+      PairJob pj;
+      pj.cj = pr.first;
+      pj.ck = pr.second;
+      auto a = fm.find({pr.second, pr.first});
+      auto b = fm.find({pr.first, pr.second});
+      pj.f_kj = a == fm.end() ? nullptr : a->second;
+      pj.f_jk = b == fm.end() ? nullptr : b->second;
+      jobs.push_back(std::move(pj));
+    }
+  }
+  if (!jobs.empty()) process_pairs(jobs, st);
+  C.free(wsb);
+  for (W& w : ws) C.free(w.Fm);
   C.flush();
+}
+
+// Waves of clusters of one level: Morton order, a cluster joins the first
+// wave after every earlier cluster within Chebyshev distance 2.
+std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact) {
+  const auto& ids = T.levels[level];
+  std::vector<std::vector<int>> out;
+  if (exact) {
+    for (int c : ids) out.push_back({c});
+    return out;
+  }
+  std::unordered_map<uint64_t, int> wave_at;
+  auto key = [](long long x, long long y, long long z) {
+    return ((uint64_t)(x & 0x1fffff) << 42) | ((uint64_t)(y & 0x1fffff) << 21) |
+           (uint64_t)(z & 0x1fffff);
+  };
+  for (int c : ids) {
+    const long long x = T.cell[3 * c], y = T.cell[3 * c + 1], z = T.cell[3 * c + 2];
+    int w = 0;
+    for (int dx = -2; dx <= 2; ++dx)
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dz = -2; dz <= 2; ++dz) {
+          if (x + dx < 0 || y + dy < 0 || z + dz < 0) continue;
+          auto it = wave_at.find(key(x + dx, y + dy, z + dz));
+          if (it != wave_at.end()) w = std::max(w, it->second);
+        }
+    wave_at[key(x, y, z)] = w + 1;
+    if ((int)out.size() < w + 1) out.resize(w + 1);
+    out[w].push_back(c);
+  }
+  return out;
 }
 
 // merge_to_parent (factor.py:525-578)
@@ -872,12 +1070,13 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
     F->leaf_stop.push_back(T.stop[c]);
   }
   Eliminator el(C, g, *F, eps * sigma0, 0x1f2e3d4c5b6a7988ULL);
+  el.exact_order = (flags & 1) != 0;
   for (double& v : g_prof) v = 0.0;
   try {
     for (int l = T.depth; l >= 2; --l) {
       LevelStats st;
       st.level = l;
-      for (int c : T.levels[l]) el.eliminate(c, st);
+      for (auto& wv : cluster_waves(T, l, el.exact_order)) el.eliminate_wave(wv, st);
       C.check_status("cluster ");
       F->levels.push_back(st);
       if (l > 2) el.merge(l);

@@ -37,11 +37,31 @@ void Arena::insert_free(size_t off, size_t len) {
   by_size_.insert({len, off});
 }
 
+bool Arena::drain_cache() {
+  if (cached_ == 0) return false;
+  for (auto& kv : cache_)
+    for (size_t off : kv.second) backend_free(off, kv.first);
+  cache_.clear();
+  cached_ = 0;
+  return true;
+}
+
 double* Arena::alloc(size_t ndoubles, int* cls) {
   size_t bytes = ndoubles * sizeof(double);
   bytes = (bytes + 255) / 256 * 256;
   if (bytes == 0) bytes = 256;
+  *cls = (int)(bytes / 256);
+  auto ci = cache_.find(bytes);
+  if (ci != cache_.end() && !ci->second.empty()) {
+    const size_t off = ci->second.back();
+    ci->second.pop_back();
+    cached_ -= bytes;
+    in_use_ += bytes;
+    peak_ = std::max(peak_, in_use_);
+    return reinterpret_cast<double*>(base_ + off);
+  }
   auto it = by_size_.lower_bound({bytes, 0});
+  if (it == by_size_.end() && drain_cache()) it = by_size_.lower_bound({bytes, 0});
   if (it == by_size_.end()) {
     char msg[200];
     snprintf(msg, sizeof msg, "device arena exhausted: need %zu B, %zu of %zu B in use", bytes,
@@ -60,9 +80,18 @@ double* Arena::alloc(size_t ndoubles, int* cls) {
 
 void Arena::free(void* p, int cls) {
   if (!p || cls <= 0) return;
-  size_t off = (size_t)(reinterpret_cast<char*>(p) - base_);
-  size_t len = (size_t)cls * 256;
+  const size_t off = (size_t)(reinterpret_cast<char*>(p) - base_);
+  const size_t len = (size_t)cls * 256;
   in_use_ -= len;
+  if (len <= ((size_t)1 << 20)) {  // cache blocks up to 1 MiB
+    cache_[len].push_back(off);
+    cached_ += len;
+    return;
+  }
+  backend_free(off, len);
+}
+
+void Arena::backend_free(size_t off, size_t len) {
   auto nx = by_addr_.lower_bound(off);
   if (nx != by_addr_.end() && nx->first == off + len) {  // merge with next
     len += nx->second;

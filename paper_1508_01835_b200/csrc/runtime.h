@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -54,6 +55,13 @@ class Arena {
 
  private:
   void insert_free(size_t off, size_t len);
+  void backend_free(size_t off, size_t len);
+  bool drain_cache();
+  // exact-size cache in front of the best-fit backend: most edge blocks are
+  // re-requested with the same shape, so reuse is an O(1) vector pop.  The
+  // cache is drained back (with coalescing) only when the backend is full.
+  std::unordered_map<size_t, std::vector<size_t>> cache_;
+  size_t cached_ = 0;
   char* base_ = nullptr;
   size_t cap_ = 0, in_use_ = 0, peak_ = 0;
   std::map<size_t, size_t> by_addr_;              // offset -> length

@@ -141,8 +141,17 @@ class IFMMFactorization:
 
 
 def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
-              sigma0: float | None = None) -> IFMMFactorization:
-    """factor.py:176-230.  Consumes the graph (like the reference's pops)."""
+              sigma0: float | None = None, exact_order: bool | None = None
+              ) -> IFMMFactorization:
+    """factor.py:176-230.  Consumes the graph (like the reference's pops).
+
+    ``exact_order`` processes the fill pairs of each elimination strictly in
+    the reference's sorted order (one pair at a time).  The default groups
+    cluster-disjoint pairs into concurrent waves, which commute up to
+    rounding.  IFMM_EXACT_ORDER=1 sets the default."""
+    import os
+    if exact_order is None:
+        exact_order = os.environ.get("IFMM_EXACT_ORDER", "0") == "1"
     if not 0.0 < epsilon < 1.0:
         raise ValueError("epsilon must be in (0, 1)")
     if graph.consumed:
@@ -153,7 +162,7 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
         sigma0 = estimate_sigma0(graph, seed=seed)
         t_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    h = N.lib().ifmm_factorize(graph._h, float(epsilon), float(sigma0), 0)
+    h = N.lib().ifmm_factorize(graph._h, float(epsilon), float(sigma0), 1 if exact_order else 0)
     graph.consumed = True
     h = N.check_handle(h)
     return IFMMFactorization(graph, h, epsilon, sigma0, t_s, time.perf_counter() - t0)

@@ -16,7 +16,13 @@ print(f"h2 build {time.perf_counter()-t:.2f}s max rank {ops.max_rank()}", flush=
 t = time.perf_counter(); P.initialize_weights(ops, topo); print(f"weights {time.perf_counter()-t:.2f}s", flush=True)
 t = time.perf_counter(); gr = P.assemble_extended_graph(ops); print(f"graph {time.perf_counter()-t:.2f}s dim {gr.dim} edges {gr.num_edges}", flush=True)
 t = time.perf_counter(); s0 = P.estimate_sigma0(gr); print(f"sigma0 {s0:.10g} {time.perf_counter()-t:.2f}s", flush=True)
+import os
+if os.environ.get("KT") == "1": NN.ktime(1)
+l0 = NN.launches()
 t = time.perf_counter(); f = P.factorize(gr, 1e-6, sigma0=s0); tf = time.perf_counter() - t
+print("launches", NN.launches() - l0)
+if os.environ.get("KT") == "1":
+    kt = NN.ktime(0); print("ktime", {k: (round(v[0], 3), v[2]) for k, v in kt.items() if v[2]}, "sum", round(sum(v[0] for v in kt.values()), 3))
 print(f"factorize {tf:.2f}s stats peak_edges={f.stats.peak_edges} events={f.event_counts} flops={f.flops}", flush=True)
 print("profile", {k: round(v, 3) for k, v in NN.profile().items()}, flush=True)
 print("levels", [(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in f.stats.levels], flush=True)
