@@ -179,6 +179,17 @@ def fp64_peak_tflops():
     return 2.0 * 8192 ** 3 / best / 1e12
 
 
+def reduce_max(vals, device="cuda"):
+    """Max over ranks of a list of timings (no-op without a process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(vals)
+    t = torch.tensor(list(vals), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 def run_ours(args, rank, world):
     import torch
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
@@ -235,10 +246,7 @@ def run_ours(args, rank, world):
     clk = clocks.stop() if clocks else None
     tot_dev = sum(tf) + sum(ts)
     tot_e2e = sum(tf) + sum(tsh)
-    if world > 1:
-        t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_dev, tot_e2e = float(t[0]), float(t[1])
+    tot_dev, tot_e2e = reduce_max([tot_dev, tot_e2e])
     if rank != 0:
         return
     # ---- instrumented step for the kernel roofline ----

@@ -416,7 +416,7 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
       __syncthreads();
       continue;
     }
-    const double delta = fmax(1e-9 * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
+    const double delta = fmax(1e-6 * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
     const double delta2 = delta * delta;
     int r0 = 0;
     for (int j = 0; j < kmax; ++j) {

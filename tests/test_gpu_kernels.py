@@ -115,3 +115,34 @@ def test_union_matches_oracle(N):
     fm = FM.cpu().numpy()[:r * kf].reshape(r, kf)
     np.testing.assert_allclose(nb @ om, ref.basis @ ref.old_map, atol=1e-10)
     np.testing.assert_allclose(nb @ fm, ref.basis @ ref.fill_map, atol=1e-10)
+
+
+@pytest.mark.parametrize("m,n,decay,r_cut", [(480, 480, 0.5, 12), (480, 100, 0.3, 13),
+                                              (100, 480, 0.3, 13), (200, 300, 0.05, 60),
+                                              (64, 64, 0.2, 40), (500, 450, 0.02, 100),
+                                              (450, 480, 0.01, 300)])
+def test_fill_svd_large(N, m, n, decay, r_cut):
+    """Rank-revealing fill compression vs numpy on large blocks (global path);
+    the threshold sits between two singular values."""
+    rng = np.random.default_rng(m * 3 + n)
+    k = min(m, n)
+    s_true = 10.0 ** (-decay * np.arange(k))
+    thr = float(np.sqrt(s_true[r_cut - 1] * s_true[r_cut]))
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    A = (U * s_true) @ V.T
+    s_ref = np.linalg.svd(A, compute_uv=False)
+    dA = _dev(A)
+    dU = torch.zeros(m * k, dtype=torch.float64, device="cuda")
+    dS = torch.zeros(k, dtype=torch.float64, device="cuda")
+    dV = torch.zeros(n * k, dtype=torch.float64, device="cuda")
+    dr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().ifmm_dev_svd(N.ctx(), m, n, _p(dA), thr, _p(dU), _p(dS), _p(dV), _p(dr)))
+    r = int(dr.item())
+    assert r == int(np.sum(s_ref > thr))
+    S = dS.cpu().numpy()[:r]
+    np.testing.assert_allclose(S, s_ref[:r], rtol=1e-9, atol=1e-6 * thr)
+    Uo = dU.cpu().numpy()[:m * r].reshape(r, m).T
+    Vo = dV.cpu().numpy()[:n * r].reshape(r, n).T
+    Ar = (U[:, :r] * s_true[:r]) @ V[:, :r].T
+    assert np.linalg.norm((Uo * S) @ Vo.T - Ar) <= 1e-8 * np.linalg.norm(Ar) + 1e-5 * thr
