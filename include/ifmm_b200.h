@@ -118,6 +118,9 @@ long long ifmm_ctx_launches(void* ctx);
  * algorithmic work = flops or bytes, launch count); enable >= 0 also resets
  * and switches timing on (1) or off (0). */
 int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* count, int n);
+/* Diagnostics: union-kernel cycle counters (ACA, QR, Q, Jacobi, output,
+ * steps, count, sum m, sum C, smem count, Jacobi sweeps); reset != 0 clears. */
+int ifmm_union_profile(unsigned long long* out, int reset);
 /* Diagnostics: phase times (s) of the last factorize when IFMM_PROFILE=1. */
 int ifmm_profile(double* out, int n);
 

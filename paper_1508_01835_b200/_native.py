@@ -56,6 +56,7 @@ _SIGS = {
     "ifmm_ctx_elapsed": (C.c_int, [vp, C.c_int, C.c_int, dp]),
     "ifmm_ctx_launches": (C.c_longlong, [vp]),
     "ifmm_ktime": (C.c_int, [vp, C.c_int, dp, dp, lp, C.c_int]),
+    "ifmm_union_profile": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     "ifmm_dev_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
                                 C.c_int, vp, C.c_int, C.c_double, C.c_double]),
     "ifmm_dev_svd": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_double, vp, vp, vp, vp]),

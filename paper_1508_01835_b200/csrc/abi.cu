@@ -402,6 +402,11 @@ int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* c
   return 0;
 }
 
+int ifmm_union_profile(unsigned long long* out, int reset) {
+  ifmm::union_profile(out, reset);
+  return 0;
+}
+
 int ifmm_profile(double* out, int n) {
   for (int i = 0; i < n && i < 11; ++i) out[i] = ifmm::g_prof[i];
   return 0;
@@ -487,7 +492,7 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
   d[0].min_rank = min_rank;
   d[0].NB = NB; d[0].nb_r = 1; d[0].nb_c = m;                    // col-major output
   d[0].NW = NW; d[0].OM = OM; d[0].FM = FM; d[0].rank = rank; d[0].work = wk.p;
-  launch_union(C.stage.push_vec(C, d), 1, thr, C.st);
+  launch_union(C.stage.push_vec(C, d), 1, thr, C.st, union_fits_smem(m, k_old, k_f) ? 1 : 0);
   CUDA_CHECK(cudaGetLastError());
   C.sync();
   C.free(wk);

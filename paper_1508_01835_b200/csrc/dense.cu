@@ -18,6 +18,9 @@
 
 namespace ifmm {
 
+// per-phase cycle counters of the union kernel (diagnostics)
+__device__ unsigned long long g_uprof[16];
+
 __device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
 __device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
                           double* Q, int ldq);
@@ -217,11 +220,11 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
     // all lanes of the warp take part in the shuffles (teams never straddle)
     a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
     if (!act) continue;
-    const double sab = sqrt(a) * sqrt(b);
-    if (g != 0.0 && fabs(g) > tol_rot * sab) {
+    const double ab = a * b, g2 = g * g;
+    if (g != 0.0 && g2 > tol_rot * tol_rot * ab) {
       const double zeta = (b - a) / (2.0 * g);
-      const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-      const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+      const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
       for (int i = tl; i < rows; i += T) {
         const double u = x[i], v = y[i];
         x[i] = c * u - s * v;
@@ -234,7 +237,7 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
         vx[i] = c * u - s * v;
         vy[i] = s * u + c * v;
       }
-      if (tl == 0 && fabs(g) > tol_conv * sab) *sflag = 1;
+      if (tl == 0 && g2 > tol_conv * tol_conv * ab) *sflag = 1;
     }
   }
 }
@@ -261,6 +264,7 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
     }
     const int again = *sflag;
     __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&g_uprof[10], 1ull);
     if (!again) break;
   }
 }
@@ -363,6 +367,84 @@ size_t svd_smem_doubles(int max_smem_dim) {
   return need * sizeof(double) > 200 * 1024 ? 0 : need;
 }
 
+
+// Householder QR with column pivoting of col-major A (m x n, ld m), in place
+// (R upper, scaled reflectors below, taus), stopping once the remaining
+// Frobenius mass sum(nrm[j:]) <= stop2.  nrm must hold the squared column
+// norms on entry; perm receives the pivot order.  Returns the step count.
+__device__ int cta_qrcp(double* A, int m, int nn, int kmax, double* nrm, int* perm, double* tau,
+                        double stop2, double* red, long long* redi) {
+  __shared__ double s_beta, s_tau, s_scale;
+  __shared__ int s_p, s_stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int r0 = 0;
+  for (int j = 0; j < kmax; ++j) {
+    double t = 0.0, bv = -1.0;
+    long long bi = (1LL << 62);
+    for (int c2 = j + threadIdx.x; c2 < nn; c2 += blockDim.x) {
+      const double v = nrm[c2];
+      t += v;
+      if (v > bv || (v == bv && c2 < bi)) { bv = v; bi = c2; }
+    }
+    t = block_sum(t, red);
+    block_argmax(bv, bi, red, redi);
+    if (threadIdx.x == 0) { s_stop = t <= stop2; s_p = (int)bi; }
+    __syncthreads();
+    if (s_stop) break;
+    const int p = s_p;
+    if (p != j) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double u = A[(size_t)j * m + i];
+        A[(size_t)j * m + i] = A[(size_t)p * m + i];
+        A[(size_t)p * m + i] = u;
+      }
+      if (threadIdx.x == 0) {
+        const double u = nrm[j]; nrm[j] = nrm[p]; nrm[p] = u;
+        const int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
+      }
+    }
+    __syncthreads();
+    double* a = A + (size_t)j * m;
+    double nx = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) nx = fma(a[i], a[i], nx);
+    nx = block_sum(nx, red);
+    if (threadIdx.x == 0) {
+      const double alpha = a[j];
+      if (nx == 0.0) { s_tau = 0.0; s_beta = alpha; s_scale = 0.0; }
+      else {
+        const double beta = -copysign(sqrt(alpha * alpha + nx), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scale = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+      tau[j] = s_tau;
+    }
+    __syncthreads();
+    const double sc = s_scale, tj = s_tau;
+    if (tj != 0.0)
+      for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[i] *= sc;
+    __syncthreads();
+    if (threadIdx.x == 0) a[j] = s_beta;
+    for (int c2 = j + 1 + warp; c2 < nn; c2 += nw) {
+      double* ac = A + (size_t)c2 * m;
+      if (tj != 0.0) {
+        double w = (lane == 0) ? ac[j] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w = fma(a[i], ac[i], w);
+        w = warp_sum(w) * tj;
+        if (lane == 0) ac[j] -= w;
+        for (int i = j + 1 + lane; i < m; i += 32) ac[i] -= w * a[i];
+      }
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
+      s = warp_sum(s);
+      if (lane == 0) nrm[c2] = s;
+    }
+    r0 = j + 1;
+    __syncthreads();
+  }
+  return r0;
+}
+
 namespace {
 // Truncated SVD through a rank-revealing pivoted QR (fill compression).
 // F P = Q R; stop at step r0 once ||R22||_F <= delta, delta = max(1e-9 thr,
@@ -376,8 +458,6 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
   __shared__ double red[32];
   __shared__ long long redi[32];
   __shared__ int sflag;
-  __shared__ double s_beta, s_tau, s_scale, s_tot;
-  __shared__ int s_p, s_stop;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const SvdDesc d = descs[bb];
@@ -417,74 +497,7 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
       continue;
     }
     const double delta = fmax(1e-6 * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
-    const double delta2 = delta * delta;
-    int r0 = 0;
-    for (int j = 0; j < kmax; ++j) {
-      // remaining Frobenius mass and pivot column
-      double t = 0.0, bv = -1.0;
-      long long bi = (1LL << 62);
-      for (int c2 = j + threadIdx.x; c2 < nn; c2 += blockDim.x) {
-        const double v = nrm[c2];
-        t += v;
-        if (v > bv || (v == bv && c2 < bi)) { bv = v; bi = c2; }
-      }
-      t = block_sum(t, red);
-      block_argmax(bv, bi, red, redi);
-      if (threadIdx.x == 0) { s_stop = t <= delta2; s_p = (int)bi; }
-      __syncthreads();
-      if (s_stop) break;
-      const int p = s_p;
-      if (p != j) {
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-          const double u = A[(size_t)j * m + i];
-          A[(size_t)j * m + i] = A[(size_t)p * m + i];
-          A[(size_t)p * m + i] = u;
-        }
-        if (threadIdx.x == 0) {
-          const double u = nrm[j]; nrm[j] = nrm[p]; nrm[p] = u;
-          const int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
-        }
-      }
-      __syncthreads();
-      // Householder on A[j:, j]
-      double* a = A + (size_t)j * m;
-      double nx = 0.0;
-      for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) nx = fma(a[i], a[i], nx);
-      nx = block_sum(nx, red);
-      if (threadIdx.x == 0) {
-        const double alpha = a[j];
-        if (nx == 0.0) { s_tau = 0.0; s_beta = alpha; s_scale = 0.0; }
-        else {
-          const double beta = -copysign(sqrt(alpha * alpha + nx), alpha);
-          s_tau = (beta - alpha) / beta;
-          s_scale = 1.0 / (alpha - beta);
-          s_beta = beta;
-        }
-        tau[j] = s_tau;
-      }
-      __syncthreads();
-      const double sc = s_scale, tj = s_tau;
-      if (tj != 0.0)
-        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[i] *= sc;
-      __syncthreads();
-      if (threadIdx.x == 0) a[j] = s_beta;
-      for (int c2 = j + 1 + warp; c2 < nn; c2 += nw) {
-        double* ac = A + (size_t)c2 * m;
-        if (tj != 0.0) {
-          double w = (lane == 0) ? ac[j] : 0.0;
-          for (int i = j + 1 + lane; i < m; i += 32) w = fma(a[i], ac[i], w);
-          w = warp_sum(w) * tj;
-          if (lane == 0) ac[j] -= w;
-          for (int i = j + 1 + lane; i < m; i += 32) ac[i] -= w * a[i];
-        }
-        double s = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
-        s = warp_sum(s);
-        if (lane == 0) nrm[c2] = s;
-      }
-      r0 = j + 1;
-      __syncthreads();
-    }
+    const int r0 = cta_qrcp(A, m, nn, kmax, nrm, perm, tau, delta * delta, red, redi);
     if (r0 == 0) { if (threadIdx.x == 0) *d.rank = 0; __syncthreads(); continue; }
     // Q0 (m x r0) and W2 = (R0 P^T)^T (n x r0)
     cta_orgqr(A, m, r0, m, tau, Q0, m);
@@ -618,87 +631,214 @@ __device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const do
 // Weighted basis union: ACA (full pivot) + QR + QR + Jacobi SVD
 // ============================================================================
 
-size_t union_work_doubles(int m, int k_old, int k_f) {
+__host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f) {
   const size_t C = (size_t)k_old + k_f;
   const size_t s = (size_t)(m < (int)C ? m : (int)C);
-  // M(mC) Acol(m s) Bt(C s) QA(m s) QB(C s) core(s s) V(s s) tau 2s sig s order s
-  return (size_t)m * C + 2 * (size_t)m * s + 2 * C * s + 2 * s * s + 5 * s + 16;
+  // M (m C; reused for QA m s) | Acol (m s) | Bt (C s) | QB (C s) | core (s s) | V (s s)
+  // | tauA tauB sig (3s) | order (s ints)
+  return (size_t)m * C + (size_t)m * s + 2 * C * s + 2 * s * s + 4 * s + 16;
+}
+
+
+void union_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_uprof, z, sizeof z);
+  }
 }
 
 namespace {
+constexpr int UNION_SMEM_DOUBLES = 28500;  // 228 KB
+
+// Interleaved Householder QR of two column-major matrices A (ra x s) and
+// B (rb x s): two barriers per column for both.  On exit: R in the upper
+// triangles, scaled reflectors below, taus in tauA / tauB.
+__device__ void cta_geqrf2(double* A, int ra, double* B, int rb, int s, double* tauA, double* tauB,
+                           double* pa, double* pb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double scA = 0.0, scB = 0.0, bA = 0.0, bB = 0.0;
+  for (int j = 0; j < s; ++j) {
+    // finish column j-1: scale its reflector and set the diagonal
+    if (j > 0) {
+      double* a = A + (size_t)(j - 1) * ra;
+      double* b = B + (size_t)(j - 1) * rb;
+      for (int i = j + threadIdx.x; i < ra; i += blockDim.x) a[i] *= scA;
+      for (int i = j + threadIdx.x; i < rb; i += blockDim.x) b[i] *= scB;
+      if (threadIdx.x == 0) { a[j - 1] = bA; b[j - 1] = bB; }
+    }
+    const double* a = A + (size_t)j * ra;
+    const double* b = B + (size_t)j * rb;
+    double na = 0.0, nb = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < ra; i += blockDim.x) na = fma(a[i], a[i], na);
+    for (int i = j + 1 + threadIdx.x; i < rb; i += blockDim.x) nb = fma(b[i], b[i], nb);
+    na = warp_sum(na);
+    nb = warp_sum(nb);
+    if (lane == 0) { pa[warp] = na; pb[warp] = nb; }
+    __syncthreads();
+    na = 0.0; nb = 0.0;
+    for (int w = 0; w < nw; ++w) { na += pa[w]; nb += pb[w]; }
+    const double alA = a[j], alB = b[j];
+    double tA = 0.0, tB = 0.0;
+    if (na == 0.0) { tA = 0.0; bA = alA; scA = 0.0; }
+    else { bA = -copysign(sqrt(alA * alA + na), alA); tA = (bA - alA) / bA; scA = 1.0 / (alA - bA); }
+    if (nb == 0.0) { tB = 0.0; bB = alB; scB = 0.0; }
+    else { bB = -copysign(sqrt(alB * alB + nb), alB); tB = (bB - alB) / bB; scB = 1.0 / (alB - bB); }
+    if (threadIdx.x == 0) { tauA[j] = tA; tauB[j] = tB; }
+    // trailing updates: columns of A then of B, one warp per column
+    const int ntr = s - j - 1;
+    for (int t = warp; t < 2 * ntr; t += nw) {
+      const bool isA = t < ntr;
+      const int cidx = j + 1 + (isA ? t : t - ntr);
+      const double tau = isA ? tA : tB;
+      if (tau == 0.0) continue;
+      const double sc = isA ? scA : scB;
+      const double* v = isA ? a : b;
+      double* col = (isA ? A + (size_t)cidx * ra : B + (size_t)cidx * rb);
+      const int rr = isA ? ra : rb;
+      double w = (lane == 0) ? col[j] : 0.0;
+      for (int i = j + 1 + lane; i < rr; i += 32) w = fma(v[i] * sc, col[i], w);
+      w = warp_sum(w) * tau;
+      if (lane == 0) col[j] -= w;
+      for (int i = j + 1 + lane; i < rr; i += 32) col[i] -= w * (v[i] * sc);
+    }
+    __syncthreads();
+  }
+  if (s > 0) {
+    double* a = A + (size_t)(s - 1) * ra;
+    double* b = B + (size_t)(s - 1) * rb;
+    for (int i = s + threadIdx.x; i < ra; i += blockDim.x) a[i] *= scA;
+    for (int i = s + threadIdx.x; i < rb; i += blockDim.x) b[i] *= scB;
+    if (threadIdx.x == 0) { a[s - 1] = bA; b[s - 1] = bB; }
+  }
+  __syncthreads();
+}
+
+// Interleaved Q formation for the two factorizations (one barrier / column).
+__device__ void cta_orgqr2(const double* A, int ra, const double* tauA, double* QA,
+                           const double* B, int rb, const double* tauB, double* QB, int s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long long e = threadIdx.x; e < (long long)ra * s; e += blockDim.x) {
+    const int c = (int)(e / ra), i = (int)(e % ra);
+    QA[e] = (i == c) ? 1.0 : 0.0;
+  }
+  for (long long e = threadIdx.x; e < (long long)rb * s; e += blockDim.x) {
+    const int c = (int)(e / rb), i = (int)(e % rb);
+    QB[e] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = s - 1; j >= 0; --j) {
+    const int ntr = s - j;
+    for (int t = warp; t < 2 * ntr; t += nw) {
+      const bool isA = t < ntr;
+      const int cidx = j + (isA ? t : t - ntr);
+      const double tau = isA ? tauA[j] : tauB[j];
+      if (tau == 0.0) continue;
+      const double* v = isA ? A + (size_t)j * ra : B + (size_t)j * rb;
+      double* q = isA ? QA + (size_t)cidx * ra : QB + (size_t)cidx * rb;
+      const int rr = isA ? ra : rb;
+      double w = (lane == 0) ? q[j] : 0.0;
+      for (int i = j + 1 + lane; i < rr; i += 32) w = fma(v[i], q[i], w);
+      w = warp_sum(w) * tau;
+      if (lane == 0) q[j] -= w;
+      for (int i = j + 1 + lane; i < rr; i += 32) q[i] -= w * v[i];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(512)
-union_kernel(const UnionDesc* __restrict__ descs, int n, double thr) {
-  __shared__ double red[32];
-  __shared__ long long redi[32];
+union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
+  extern __shared__ double smem[];
+  __shared__ double wv[32];
+  __shared__ long long wi[32];
+  __shared__ double pa[32], pb[32];
   __shared__ int sflag;
-  __shared__ double s_piv;
-  __shared__ int s_p, s_q, s_stop;
-  for (int b = blockIdx.x; b < n; b += gridDim.x) {
-    const UnionDesc d = descs[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
+    const UnionDesc d = descs[bb];
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
-    double* M = d.work;
+    const size_t need = union_work_doubles(m, d.k_old, d.k_f);
+    double* M = need <= (size_t)smem_doubles ? smem : d.work;
     double* Acol = M + (size_t)m * C;
     double* Bt = Acol + (size_t)m * smax;
-    double* QA = Bt + (size_t)C * smax;
-    double* QB = QA + (size_t)m * smax;
+    double* QB = Bt + (size_t)C * smax;
     double* core = QB + (size_t)C * smax;
     double* Vc = core + (size_t)smax * smax;
     double* tauA = Vc + (size_t)smax * smax;
     double* tauB = tauA + smax;
     double* sig = tauB + smax;
     int* order = (int*)(sig + smax);
+    double* QA = M;  // M is dead after the ACA loop
 
-    // concat [B*diag(w) | F*diag(wf)]  (col-major m x C)
-    for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
-      const int j = (int)(e / m), i = (int)(e % m);
-      M[e] = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
-                    : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+    // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax
+    const int tot = m * C;
+    const int bstep = blockDim.x / m, istep = blockDim.x % m;  // incremental (i, j)
+    const int i00 = threadIdx.x % m, j00 = threadIdx.x / m;
+    double bv = -1.0;
+    long long bi = (1LL << 62);
+    {
+      int i = i00, j = j00;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
+                                : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+        M[e] = v;
+        const double av = fabs(v);
+        const long long flat = (long long)(i * C + j);  // numpy row-major order
+        if (av > bv || (av == bv && flat < bi)) { bv = av; bi = flat; }
+        i += istep; j += bstep;
+        if (i >= m) { i -= m; ++j; }
+      }
     }
-    __syncthreads();
-    // ---- ACA with full pivoting, floor thr/8 (lowrank.py:145-151) ----
+    unsigned long long t0 = clock64();
+    // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step
     const double floor_ = thr / 8.0;
     int steps = 0;
     for (int it = 0; it < smax; ++it) {
-      double bv = -1.0;
-      long long bi = (1LL << 62);
-      for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
-        const double v = fabs(M[e]);
-        const int j = (int)(e / m), i = (int)(e % m);
-        const long long flat = (long long)i * C + j;  // numpy row-major order
-        if (v > bv || (v == bv && flat < bi)) { bv = v; bi = flat; }
-      }
-      block_argmax(bv, bi, red, redi);
-      if (threadIdx.x == 0) {
-        s_p = (int)(bi / C); s_q = (int)(bi % C);
-        s_piv = M[(size_t)s_q * m + s_p];
-        s_stop = (s_piv == 0.0 || (fabs(s_piv) <= floor_ && steps >= d.min_rank)) ? 1 : 0;
-      }
+      warp_argmax(bv, bi);
+      if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
       __syncthreads();
-      if (s_stop) break;
-      const int p = s_p, q = s_q;
-      const double piv = s_piv;
-      for (int i = threadIdx.x; i < m; i += blockDim.x) Acol[(size_t)steps * m + i] = M[(size_t)q * m + i];
-      for (int j = threadIdx.x; j < C; j += blockDim.x) Bt[(size_t)steps * C + j] = M[(size_t)j * m + p] / piv;
+      double gv = -1.0;
+      long long gi = (1LL << 62);
+      for (int w = 0; w < nw; ++w) {
+        const double ov = wv[w];
+        const long long oi = wi[w];
+        if (ov > gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+      }
+      const int p = (int)(gi / C), q = (int)(gi % C);
+      const double piv = M[(size_t)q * m + p];
+      if (piv == 0.0 || (fabs(piv) <= floor_ && steps >= d.min_rank)) break;  // uniform
+      double* cc = Acol + (size_t)steps * m;
+      double* rr = Bt + (size_t)steps * C;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) cc[i] = M[(size_t)q * m + i];
+      for (int j = threadIdx.x; j < C; j += blockDim.x) rr[j] = M[(size_t)j * m + p] / piv;
       __syncthreads();
-      const double* cc = Acol + (size_t)steps * m;
-      const double* rr = Bt + (size_t)steps * C;
-      for (long long e = threadIdx.x; e < (long long)m * C; e += blockDim.x) {
-        const int j = (int)(e / m), i = (int)(e % m);
-        M[e] -= cc[i] * rr[j];
+      bv = -1.0;
+      bi = (1LL << 62);
+      int i = i00, j = j00;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const double v = M[e] - cc[i] * rr[j];
+        M[e] = v;
+        const double av = fabs(v);
+        const long long flat = (long long)(i * C + j);
+        if (av > bv || (av == bv && flat < bi)) { bv = av; bi = flat; }
+        i += istep; j += bstep;
+        if (i >= m) { i -= m; ++j; }
       }
       ++steps;
-      __syncthreads();
     }
+    __syncthreads();
     if (steps == 0) {
       if (threadIdx.x == 0) *d.rank = 0;
       __syncthreads();
       continue;
     }
     const int s = steps;
-    // ---- QR(A), QR(B^T) ----
-    cta_geqrf(Acol, m, s, m, tauA, red);
-    cta_geqrf(Bt, C, s, C, tauB, red);
+    unsigned long long t1 = clock64();
+    // ---- QR(A), QR(B^T) interleaved ----
+    cta_geqrf2(Acol, m, Bt, C, s, tauA, tauB, pa, pb);
+    unsigned long long t2 = clock64();
     // core = RA * RB^T (s x s, col-major)
     for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
       const int j = e / s, i = e % s;
@@ -707,16 +847,16 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr) {
         acc = fma(Acol[(size_t)l * m + i], Bt[(size_t)l * C + j], acc);
       core[(size_t)j * s + i] = acc;
     }
-    cta_orgqr(Acol, m, s, m, tauA, QA, m);
-    cta_orgqr(Bt, C, s, C, tauB, QB, C);
-    __syncthreads();
+    cta_orgqr2(Acol, m, tauA, QA, Bt, C, tauB, QB, s);
+    unsigned long long t3 = clock64();
     cta_jacobi(core, s, s, s, Vc, &sflag);
     cta_sv_order(core, s, s, s, sig, order);
+    unsigned long long t4 = clock64();
     int kk = 0;
     for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
     const int mr = d.min_rank < s ? d.min_rank : s;
     const int k = kk > mr ? kk : mr;
-    // new basis = QA * Wcore[:, :k]  (Wcore col = core col / sigma)
+    // new basis = QA * Ucore[:, :k]  (Ucore col = core col / sigma)
     for (long long e = threadIdx.x; e < (long long)m * k; e += blockDim.x) {
       const int a = (int)(e / m), i = (int)(e % m);
       const int j = order[a];
@@ -725,7 +865,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr) {
       for (int l = 0; l < s; ++l) acc = fma(QA[(size_t)l * m + i], core[(size_t)j * s + l], acc);
       d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc * inv;
     }
-    // V_full = QB * Vc[:, order[:k]]  (C x k); maps = sigma_a V_full[col][a] / weight
+    // maps = sigma_a (QB Vc)[col][a] / weight[col]
     for (long long e = threadIdx.x; e < (long long)C * k; e += blockDim.x) {
       const int a = (int)(e / C), col = (int)(e % C);
       const int j = order[a];
@@ -738,13 +878,39 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr) {
     for (int a = threadIdx.x; a < k; a += blockDim.x) d.NW[a] = sig[order[a]];
     if (threadIdx.x == 0) *d.rank = k;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t5 = clock64();
+      atomicAdd(&g_uprof[0], t1 - t0);
+      atomicAdd(&g_uprof[1], t2 - t1);
+      atomicAdd(&g_uprof[2], t3 - t2);
+      atomicAdd(&g_uprof[3], t4 - t3);
+      atomicAdd(&g_uprof[4], t5 - t4);
+      atomicAdd(&g_uprof[5], (unsigned long long)s);
+      atomicAdd(&g_uprof[6], 1ull);
+      atomicAdd(&g_uprof[7], (unsigned long long)m);
+      atomicAdd(&g_uprof[8], (unsigned long long)C);
+      atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));
+    }
   }
 }
 }  // namespace
 
-void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s) {
+bool union_fits_smem(int m, int k_old, int k_f) {
+  return union_work_doubles(m, k_old, k_f) <= (size_t)UNION_SMEM_DOUBLES;
+}
+
+// smem != 0: every desc's workspace fits shared memory (caller partitions);
+// smem == 0: workspaces in global memory with the full L1 as cache.
+void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem) {
   if (n <= 0) return;
-  union_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d_descs, n, thr);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         UNION_SMEM_DOUBLES * 8);
+    attr = true;
+  }
+  const int sd = smem ? UNION_SMEM_DOUBLES : 0;
+  union_kernel<<<n < 4096 ? n : 4096, 512, (size_t)sd * 8, s>>>(d_descs, n, thr, sd);
 }
 
 // ============================================================================

@@ -70,7 +70,7 @@ struct UnionDesc {
   double* work;
 };
 
-size_t union_work_doubles(int m, int k_old, int k_f);
+__host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f);
 __host__ __device__ size_t svd_work_doubles(int m, int n);
 // doubles of dynamic smem launch_svd uses for a given max_smem_dim (0: none)
 size_t svd_smem_doubles(int max_smem_dim);
@@ -82,7 +82,8 @@ void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s);
 // rel_mode: thr is relative to sigma_max and rank >= 1 (h2.py:124-127).
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim,
                 cudaStream_t s, int rel_mode = 0);
-void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s);
+bool union_fits_smem(int m, int k_old, int k_f);
+void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem);
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to
@@ -149,3 +150,7 @@ void launch_finite_check(const double* A, int n, int lda, int* status, int tag, 
 void launch_extend(double* NB, int m, int k, const double* G, int extra, double* NW, double thr,
                    double* work, cudaStream_t s);
 }  // namespace ifmm
+
+namespace ifmm {
+void union_profile(unsigned long long* out, int reset);
+}

@@ -187,12 +187,14 @@ struct Eliminator {
       uflops += fl;
     }
     Phase ph(C, PH_UNION);
-    UnionDesc* dud = C.stage.push_vec(C, ud);
+    std::vector<UnionDesc> us, ug;  // shared-memory vs global-workspace unions
+    for (auto& u : ud) (union_fits_smem(u.m, u.k_old, u.k_f) ? us : ug).push_back(u);
     cudaEvent_t ka = nullptr;
     C.kt_begin(K_UNION, uflops, &ka);
-    launch_union(dud, (int)ud.size(), thr, C.st);
+    if (!us.empty()) launch_union(C.stage.push_vec(C, us), (int)us.size(), thr, C.st, 1);
+    if (!ug.empty()) launch_union(C.stage.push_vec(C, ug), (int)ug.size(), thr, C.st, 0);
     C.kt_end(K_UNION, uflops, ka);
-    C.launches++;
+    C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(dr, reqs.size());
     for (size_t i = 0; i < reqs.size(); ++i) {
