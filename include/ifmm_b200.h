@@ -61,7 +61,9 @@ int ifmm_h2_block(void* h2, int which, int i, int j, double* out, int* rows, int
 int ifmm_h2_matvec(void* h2, const double* x, double* y, int on_device);
 
 /* ---- extended graph:  graph.py:219-229 / sigma0 graph.py:232-241 ------ */
-void* ifmm_graph_build(void* h2);
+/* consume != 0 moves the operator blocks into the graph instead of copying
+ * them (halves peak memory; the operators are unusable afterwards). */
+void* ifmm_graph_build(void* h2, int consume);
 void ifmm_graph_destroy(void* graph);
 int ifmm_graph_info(void* graph, long long* dim, long long* n_nodes, long long* n_edges);
 /* randomized_svd(start_rank=1, max_rank=1) of the extended matrix with the

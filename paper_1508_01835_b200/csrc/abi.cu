@@ -49,6 +49,9 @@ void* ifmm_ctx_create(int device, unsigned long long arena_bytes) {
   Ctx* c = new Ctx;
   c->device = device;
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
   if (arena_bytes == 0) {
     size_t fr = 0, tot = 0;
     CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
@@ -70,6 +73,7 @@ void ifmm_ctx_destroy(void* p) {
   c->stage.release();
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_pinned_i) cudaFreeHost(c->h_pinned_i);
+  cudaStreamDestroy(c->st2);
   cudaStreamDestroy(c->st);
   delete c;
 }
@@ -197,6 +201,7 @@ int ifmm_h2_ranks(void* p, int* out) {
 
 int ifmm_h2_weights(void* p) {
   ABI_TRY
+  if (((H2*)p)->consumed) throw Error(E_VALUE, "operators were consumed by a graph");
   ((H2*)p)->weights();
   return 0;
   ABI_CATCH
@@ -245,6 +250,7 @@ __global__ void k_scatter(const double* in, const int* perm, int n, double* out)
 int ifmm_h2_matvec(void* p, const double* x, double* y, int on_device) {
   ABI_TRY
   H2* h = (H2*)p;
+  if (h->consumed) throw Error(E_VALUE, "operators were consumed by a graph");
   Ctx& C = *h->ctx;
   const int N = h->tree->n_points;
   Blk xin = C.alloc(1, N), xs = C.alloc(1, N), ys = C.alloc(1, N), yo = C.alloc(1, N);
@@ -263,15 +269,16 @@ int ifmm_h2_matvec(void* p, const double* x, double* y, int on_device) {
 }
 
 // ---- graph ------------------------------------------------------------------
-void* ifmm_graph_build(void* h2) {
+void* ifmm_graph_build(void* h2, int consume) {
   ABI_TRY
   H2* h = (H2*)h2;
+  if (h->consumed) throw Error(E_VALUE, "operators were consumed by an earlier graph");
   if (h->tree->depth >= 2 && !h->weighted)
     throw Error(E_VALUE, "operators have no basis weights; run initialize_weights first");
   Graph* g = new Graph;
   g->ctx = h->ctx;
   try {
-    g->build(h);
+    g->build(h, consume != 0);
   } catch (...) {
     delete g;
     throw;

@@ -47,6 +47,7 @@ struct H2 {
   int ncheb = 0;
   double eps = 0.0;
   bool weighted = false;
+  bool consumed = false;  // blocks moved into a graph
   std::vector<int> rank;                 // -1 where absent
   std::vector<Blk> leaf_u, leaf_v;       // leaf: m x k
   std::vector<Blk> tu, tvt;              // child: k_c x k_p / k_p x k_c
@@ -106,7 +107,7 @@ struct Graph {
     rows[t].erase(s); cols[s].erase(t);
     return b;
   }
-  void build(H2* h);
+  void build(H2* h, bool consume = false);
   long long dim() const {
     long long d = 0;
     for (int s : size) d += s;

@@ -189,10 +189,15 @@ struct Eliminator {
     Phase ph(C, PH_UNION);
     std::vector<UnionDesc> us, ug;  // shared-memory vs global-workspace unions
     for (auto& u : ud) (union_fits_smem(u.m, u.k_old, u.k_f) ? us : ug).push_back(u);
+    UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
+    UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
     cudaEvent_t ka = nullptr;
     C.kt_begin(K_UNION, uflops, &ka);
-    if (!us.empty()) launch_union(C.stage.push_vec(C, us), (int)us.size(), thr, C.st, 1);
-    if (!ug.empty()) launch_union(C.stage.push_vec(C, ug), (int)ug.size(), thr, C.st, 0);
+    if (dus && dug)
+      C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
+              [&](cudaStream_t s) { launch_union(dug, (int)ug.size(), thr, s, 0); });
+    else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
+    else launch_union(dug, (int)ug.size(), thr, C.st, 0);
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
@@ -885,10 +890,19 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       sd[i].rank = dr + i;
       sd[i].work = wsb.p + wo[i];
     }
-    SvdDesc* dsd = C.stage.push_vec(C, sd);
+    // small blocks use a shared-memory workspace, large ones global memory
+    // with the full L1 as cache: two launches running concurrently
+    std::vector<SvdDesc> sds, sdg;
+    for (auto& x : sd) (svd_work_doubles(x.m, x.n) <= smem_d ? sds : sdg).push_back(x);
+    SvdDesc* dss = sds.empty() ? nullptr : C.stage.push_vec(C, sds);
+    SvdDesc* dsg = sdg.empty() ? nullptr : C.stage.push_vec(C, sdg);
     cudaEvent_t ka = nullptr;
     C.kt_begin(K_SVD, sflops, &ka);
-    launch_svd(dsd, ns, thr, smem_dim, C.st, 0);
+    if (dss && dsg)
+      C.fork2([&](cudaStream_t s) { launch_svd(dss, (int)sds.size(), thr, smem_dim, s, 0); },
+              [&](cudaStream_t s) { launch_svd(dsg, (int)sdg.size(), thr, 0, s, 0); });
+    else if (dss) launch_svd(dss, (int)sds.size(), thr, smem_dim, C.st, 0);
+    else launch_svd(dsg, (int)sdg.size(), thr, 0, C.st, 0);
     C.kt_end(K_SVD, sflops, ka);
     C.launches++;
     CUDA_CHECK(cudaGetLastError());
@@ -1082,6 +1096,10 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
       C.check_status("cluster ");
       F->levels.push_back(st);
       if (l > 2) el.merge(l);
+      if (getenv("IFMM_MEMTRACE"))
+        fprintf(stderr, "[ifmm] level %d done: arena in use %.2f GB, peak %.2f GB, %.1f s\n", l,
+                C.arena.in_use() / 1073741824.0, C.arena.peak() / 1073741824.0,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
     el.top();
     C.sync();

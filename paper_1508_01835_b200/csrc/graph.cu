@@ -16,7 +16,7 @@ Graph::~Graph() {
   ctx->flush();
 }
 
-void Graph::build(H2* h) {
+void Graph::build(H2* h, bool consume) {
   ops = h;
   tree = h->tree;
   ctx = h->ctx;
@@ -32,14 +32,22 @@ void Graph::build(H2* h) {
       ny[c] = new_node(h->rank[c], NK_Y, c);
     }
   CopyBatch cb;
-  auto dup = [&](const Blk& s) {
+  // consume: move the operator blocks into the graph (no second copy; the
+  // operators are unusable afterwards)
+  auto dup = [&](Blk& s) {
+    if (consume) {
+      Blk b = s;
+      s = Blk();
+      return b;
+    }
     Blk b = C.alloc(s.r, s.c);
     cb.add(s.p, s.c, 1, b.p, b.c, 1, s.r, s.c, 0);
     return b;
   };
-  auto dupT = [&](const Blk& s) {
+  auto dupT = [&](Blk& s) {
     Blk b = C.alloc(s.c, s.r);
     cb.add(s.p, 1, s.c, b.p, b.c, 1, s.c, s.r, 0);
+    if (consume) C.free(s);
     return b;
   };
   // graph.py:63-84
@@ -74,6 +82,10 @@ void Graph::build(H2* h) {
       set(nz[p], ny[c], dup(h->tvt[c]));
     }
   cb.run(C);
+  if (consume) {
+    h->consumed = true;
+    C.flush();
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 

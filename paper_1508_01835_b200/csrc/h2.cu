@@ -88,6 +88,7 @@ void H2::build() {
       C.free(Pm[t]); C.free(Ub[t]); C.free(Sb[t]); C.free(Vb[t]); C.free(Wk[t]);
     }
     C.free(ranks_b);
+    C.flush();
   }
 
   // ---- Chebyshev grids of every cluster at levels >= 2 ----
@@ -174,6 +175,7 @@ void H2::build() {
       C.free(stack[t]); C.free(Ub[t]); C.free(Sb[t]); C.free(Vb[t]); C.free(Wk[t]);
     }
     C.free(ranks_b);
+    C.flush();
   }
 
   // ---- M2L couplings (h2.py:154-164): K(i,j) = G_i Kgrid(i,j) G_j^T, i<j ----
@@ -217,6 +219,7 @@ void H2::build() {
       cb.run(C);
       C.free(kg);
       C.free(t1);
+      C.flush();  // chunk workspaces are reusable once their launches are enqueued
     }
   }
 
@@ -262,42 +265,56 @@ void H2::weights() {
   for (int l = 2; l <= T.depth; ++l)
     for (int c : T.levels[l]) ids.push_back(c);
   std::vector<Blk> P(T.nc);
-  std::vector<WeightDesc> wd;
-  std::vector<Blk> Hs, Ws;
-  CopyBatch cb;
-  for (int j : ids) {
-    const int k = rank[j];
-    su[j] = C.alloc(1, k);
-    sv[j] = C.alloc(1, k);
-    P[j] = C.alloc(k, k);
-    if (T.inters[j].empty()) {  // unit weights, no rotation (h2.py:206-209)
-      cb.add(nullptr, 0, 0, su[j].p, 1, 1, 1, k, 4, 1.0);
-      cb.eye(P[j], 1.0);
-      continue;
+  // the concatenated coupling rows H_j (k x sum k_q) are built and reduced
+  // in chunks of at most ~2 GB so setup memory stays bounded
+  const size_t chunk_doubles = (size_t)256 << 20;
+  size_t pos = 0;
+  while (pos < ids.size()) {
+    std::vector<WeightDesc> wd;
+    std::vector<Blk> Hs, Ws;
+    CopyBatch cb;
+    size_t used = 0;
+    for (; pos < ids.size() && used < chunk_doubles; ++pos) {
+      const int j = ids[pos];
+      const int k = rank[j];
+      su[j] = C.alloc(1, k);
+      sv[j] = C.alloc(1, k);
+      P[j] = C.alloc(k, k);
+      if (T.inters[j].empty()) {  // unit weights, no rotation (h2.py:206-209)
+        cb.add(nullptr, 0, 0, su[j].p, 1, 1, 1, k, 4, 1.0);
+        cb.eye(P[j], 1.0);
+        continue;
+      }
+      int W = 0;
+      for (int q : T.inters[j]) W += rank[q];
+      Blk H = C.alloc(k, W);
+      int off = 0;
+      for (int q : T.inters[j]) {
+        Blk& K = coupling.at(key2(j, q));
+        cb.add(K.p, K.c, 1, H.p + off, W, 1, K.r, K.c, 0);
+        off += K.c;
+      }
+      Blk w = C.alloc(1, (int)weights_work_doubles(k, W));
+      WeightDesc d;
+      d.H = H.p; d.k = k; d.W = W; d.P = P[j].p; d.w = su[j].p; d.work = w.p;
+      wd.push_back(d);
+      Hs.push_back(H);
+      Ws.push_back(w);
+      used += (size_t)k * W + weights_work_doubles(k, W);
     }
-    int W = 0;
-    for (int q : T.inters[j]) W += rank[q];
-    Blk H = C.alloc(k, W);
-    int off = 0;
-    for (int q : T.inters[j]) {
-      Blk& K = coupling.at(key2(j, q));
-      cb.add(K.p, K.c, 1, H.p + off, W, 1, K.r, K.c, 0);
-      off += K.c;
-    }
-    Blk w = C.alloc(1, (int)weights_work_doubles(k, W));
-    WeightDesc d;
-    d.H = H.p; d.k = k; d.W = W; d.P = P[j].p; d.w = su[j].p; d.work = w.p;
-    wd.push_back(d);
-    Hs.push_back(H);
-    Ws.push_back(w);
+    cb.run(C);
+    if (!wd.empty()) launch_weights(C.stage.push_vec(C, wd), (int)wd.size(), C.st);
+    CUDA_CHECK(cudaGetLastError());
+    C.sync();
+    for (auto& b : Hs) C.free(b);
+    for (auto& b : Ws) C.free(b);
+    C.flush();
   }
-  cb.run(C);
-  if (!wd.empty()) launch_weights(C.stage.push_vec(C, wd), (int)wd.size(), C.st);
-  CUDA_CHECK(cudaGetLastError());
-  for (int j : ids) cb.add(su[j].p, 1, 1, sv[j].p, 1, 1, 1, rank[j], 0);
-  cb.run(C);
-  for (auto& b : Hs) C.free(b);
-  for (auto& b : Ws) C.free(b);
+  {
+    CopyBatch cb;
+    for (int j : ids) cb.add(su[j].p, 1, 1, sv[j].p, 1, 1, 1, rank[j], 0);
+    cb.run(C);
+  }
 
   std::vector<std::pair<Blk*, Blk>> repl;
   std::vector<Blk> tmp;
@@ -327,7 +344,16 @@ void H2::weights() {
     repl.emplace_back(&tu[c], nu);
     repl.emplace_back(&tvt[c], nv);
   }
-  // couplings: K(j,q) = (P_j^T K(j,q)) P_q
+  g1.run(C);
+  g2.run(C);
+  for (auto& r : repl) { C.free(*r.first); *r.first = r.second; }
+  for (auto& b : tmp) C.free(b);
+  repl.clear();
+  tmp.clear();
+  C.sync();
+  C.flush();
+  // couplings: K(j,q) = (P_j^T K(j,q)) P_q, in chunks (bounded temporaries)
+  size_t nb = 0;
   for (auto& kv : coupling) {
     const int j = (int)(kv.first >> 32), q = (int)(kv.first & 0xffffffffu);
     Blk& K = kv.second;
@@ -337,6 +363,16 @@ void H2::weights() {
     g2.add(t.p, kq, 0, P[q].p, kq, 0, nk.p, kq, kj, kq, kq, 1.0, 0.0);
     tmp.push_back(t);
     repl.emplace_back(&K, nk);
+    if (++nb % 200000 == 0) {
+      g1.run(C);
+      g2.run(C);
+      for (auto& r : repl) { C.free(*r.first); *r.first = r.second; }
+      for (auto& b : tmp) C.free(b);
+      repl.clear();
+      tmp.clear();
+      C.sync();
+      C.flush();
+    }
   }
   g1.run(C);
   g2.run(C);

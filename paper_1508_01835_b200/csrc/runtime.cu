@@ -25,6 +25,8 @@ void Arena::init(size_t bytes) {
 }
 
 void Arena::release() {
+  for (auto& kv : extern_) cudaFree(kv.first);
+  extern_.clear();
   if (base_) cudaFree(base_);
   base_ = nullptr;
   cap_ = 0;
@@ -46,10 +48,18 @@ bool Arena::drain_cache() {
   return true;
 }
 
+// size classes: 256-B steps up to 4 KiB, then 8 classes per octave
+static size_t class_round(size_t bytes) {
+  if (bytes <= 4096) return (bytes + 255) / 256 * 256;
+  int e = 63 - __builtin_clzll(bytes - 1);      // 2^e < bytes <= 2^(e+1)
+  const size_t step = (size_t)1 << (e - 3);      // 1/8 octave
+  return (bytes + step - 1) / step * step;
+}
+
 double* Arena::alloc(size_t ndoubles, int* cls) {
   size_t bytes = ndoubles * sizeof(double);
-  bytes = (bytes + 255) / 256 * 256;
   if (bytes == 0) bytes = 256;
+  bytes = class_round(bytes);
   *cls = (int)(bytes / 256);
   auto ci = cache_.find(bytes);
   if (ci != cache_.end() && !ci->second.empty()) {
@@ -60,9 +70,47 @@ double* Arena::alloc(size_t ndoubles, int* cls) {
     peak_ = std::max(peak_, in_use_);
     return reinterpret_cast<double*>(base_ + off);
   }
+  if (bytes >= ((size_t)8 << 20)) {
+    // large: first fit from the top of the slab, carved from the block's end
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      for (auto rit = by_addr_.rbegin(); rit != by_addr_.rend(); ++rit) {
+        if (rit->second < bytes) continue;
+        const size_t boff = rit->first, blen = rit->second;
+        by_size_.erase({blen, boff});
+        by_addr_.erase(boff);
+        if (blen > bytes) insert_free(boff, blen - bytes);
+        in_use_ += bytes;
+        peak_ = std::max(peak_, in_use_);
+        return reinterpret_cast<double*>(base_ + boff + blen - bytes);
+      }
+      if (!drain_cache()) break;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) == cudaSuccess) {
+      extern_[p] = bytes;
+      in_use_ += bytes;
+      peak_ = std::max(peak_, in_use_);
+      *cls = kExternCls;
+      return reinterpret_cast<double*>(p);
+    }
+    cudaGetLastError();
+    char msg[200];
+    snprintf(msg, sizeof msg, "device arena exhausted: need %zu B, %zu of %zu B in use", bytes,
+             in_use_, cap_);
+    throw Error(E_OOM, msg);
+  }
   auto it = by_size_.lower_bound({bytes, 0});
   if (it == by_size_.end() && drain_cache()) it = by_size_.lower_bound({bytes, 0});
   if (it == by_size_.end()) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) == cudaSuccess) {
+      extern_[p] = bytes;
+      in_use_ += bytes;
+      peak_ = std::max(peak_, in_use_);
+      *cls = kExternCls;
+      return reinterpret_cast<double*>(p);
+    }
+    cudaGetLastError();
     char msg[200];
     snprintf(msg, sizeof msg, "device arena exhausted: need %zu B, %zu of %zu B in use", bytes,
              in_use_, cap_);
@@ -80,6 +128,15 @@ double* Arena::alloc(size_t ndoubles, int* cls) {
 
 void Arena::free(void* p, int cls) {
   if (!p || cls <= 0) return;
+  if (cls == kExternCls) {
+    auto it = extern_.find(p);
+    if (it != extern_.end()) {
+      in_use_ -= it->second;
+      cudaFree(p);  // implicitly synchronises: no in-flight reader remains
+      extern_.erase(it);
+    }
+    return;
+  }
   const size_t off = (size_t)(reinterpret_cast<char*>(p) - base_);
   const size_t len = (size_t)cls * 256;
   in_use_ -= len;
@@ -162,37 +219,50 @@ void Ctx::check_status(const char* what_prefix) {
   }
 }
 
+static constexpr size_t kMaxBatch = (size_t)1 << 19;  // descriptors per launch
+
 void GemmBatch::run(Ctx& ctx) {
   if (d.empty()) return;
-  std::vector<int> ts(d.size() + 1);
-  int tot = 0;
-  for (size_t i = 0; i < d.size(); ++i) {
-    ts[i] = tot;
-    tot += ((d[i].M + 63) / 64) * ((d[i].N + 63) / 64);
+  for (size_t c0 = 0; c0 < d.size(); c0 += kMaxBatch) {
+    const size_t c1 = std::min(d.size(), c0 + kMaxBatch);
+    std::vector<GemmDesc> part(d.begin() + c0, d.begin() + c1);
+    std::vector<int> ts(part.size() + 1);
+    long long tot = 0;
+    double fl = 0;
+    for (size_t i = 0; i < part.size(); ++i) {
+      ts[i] = (int)tot;
+      tot += (long long)((part[i].M + 63) / 64) * ((part[i].N + 63) / 64);
+      fl += 2.0 * part[i].M * part[i].N * (double)part[i].K;
+    }
+    IFMM_ASSERT(tot < (1LL << 31), "GEMM batch tile count overflow");
+    ts[part.size()] = (int)tot;
+    GemmDesc* dd = ctx.stage.push_vec(ctx, part);
+    int* dt = ctx.stage.push_vec(ctx, ts);
+    cudaEvent_t ka = nullptr;
+    ctx.kt_begin(K_GEMM, fl, &ka);
+    launch_gemm(dd, dt, (int)part.size(), (int)tot, ctx.st);
+    ctx.kt_end(K_GEMM, fl, ka);
+    ctx.launches++;
+    CUDA_CHECK(cudaGetLastError());
   }
-  ts[d.size()] = tot;
-  GemmDesc* dd = ctx.stage.push_vec(ctx, d);
-  int* dt = ctx.stage.push_vec(ctx, ts);
-  cudaEvent_t ka = nullptr;
-  ctx.kt_begin(K_GEMM, flops, &ka);
-  launch_gemm(dd, dt, (int)d.size(), tot, ctx.st);
-  ctx.kt_end(K_GEMM, flops, ka);
-  ctx.launches++;
-  CUDA_CHECK(cudaGetLastError());
   d.clear();
 }
 
 void CopyBatch::run(Ctx& ctx) {
   if (d.empty()) return;
-  CopyDesc* dd = ctx.stage.push_vec(ctx, d);
-  double bytes = 0;
-  for (auto& x : d) bytes += 16.0 * x.rows * x.cols;
-  cudaEvent_t ka = nullptr;
-  ctx.kt_begin(K_COPY, bytes, &ka);
-  launch_copy(dd, (int)d.size(), ctx.st);
-  ctx.kt_end(K_COPY, bytes, ka);
-  ctx.launches++;
-  CUDA_CHECK(cudaGetLastError());
+  for (size_t c0 = 0; c0 < d.size(); c0 += kMaxBatch) {
+    const size_t c1 = std::min(d.size(), c0 + kMaxBatch);
+    std::vector<CopyDesc> part(d.begin() + c0, d.begin() + c1);
+    CopyDesc* dd = ctx.stage.push_vec(ctx, part);
+    double bytes = 0;
+    for (auto& x : part) bytes += 16.0 * x.rows * x.cols;
+    cudaEvent_t ka = nullptr;
+    ctx.kt_begin(K_COPY, bytes, &ka);
+    launch_copy(dd, (int)part.size(), ctx.st);
+    ctx.kt_end(K_COPY, bytes, ka);
+    ctx.launches++;
+    CUDA_CHECK(cudaGetLastError());
+  }
   d.clear();
 }
 

@@ -49,6 +49,7 @@ class Arena {
   double* alloc(size_t ndoubles, int* cls);
   int* alloc_int(size_t n, int* cls) { return reinterpret_cast<int*>(alloc((n + 1) / 2, cls)); }
   void free(void* p, int cls);
+  static constexpr int kExternCls = 0x7fffffff;
   size_t in_use() const { return in_use_; }
   size_t peak() const { return peak_; }
   size_t capacity() const { return cap_; }
@@ -62,6 +63,8 @@ class Arena {
   // cache is drained back (with coalescing) only when the backend is full.
   std::unordered_map<size_t, std::vector<size_t>> cache_;
   size_t cached_ = 0;
+  // large requests the fragmented slab cannot serve go to cudaMalloc
+  std::unordered_map<void*, size_t> extern_;
   char* base_ = nullptr;
   size_t cap_ = 0, in_use_ = 0, peak_ = 0;
   std::map<size_t, size_t> by_addr_;              // offset -> length
@@ -99,6 +102,18 @@ class Staging {
 struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;        // forked side stream (concurrent variants)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // run `a` on st and `b` on st2 concurrently; st waits for both afterwards
+  template <class FA, class FB>
+  void fork2(FA a, FB b) {
+    CUDA_CHECK(cudaEventRecord(fork_ev, st));
+    CUDA_CHECK(cudaStreamWaitEvent(st2, fork_ev, 0));
+    a(st);
+    b(st2);
+    CUDA_CHECK(cudaEventRecord(join_ev, st2));
+    CUDA_CHECK(cudaStreamWaitEvent(st, join_ev, 0));
+  }
   Arena arena;
   Staging stage;
   int* d_status = nullptr;   // singular-pivot flag (tag+1)

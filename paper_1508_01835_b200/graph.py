@@ -47,12 +47,15 @@ class ExtendedGraph:
         return self._info()[2]
 
 
-def assemble_extended_graph(ops: H2Operators, topology=None, b=None) -> ExtendedGraph:
+def assemble_extended_graph(ops: H2Operators, topology=None, b=None,
+                            consume: bool = False) -> ExtendedGraph:
     """graph.py:219-229.  The right-hand side is not carried by the device
-    graph: the solve replays the event log from b (factor.py:99-157)."""
+    graph: the solve replays the event log from b (factor.py:99-157).
+    ``consume=True`` moves the operator blocks into the graph (no copy; the
+    operators cannot be used afterwards) -- for problems near device memory."""
     if ops.tree.depth >= 2 and not ops._weighted:
         raise ValueError("operators have no basis weights; run initialize_weights first")
-    h = N.lib().ifmm_graph_build(ops._h)
+    h = N.lib().ifmm_graph_build(ops._h, 1 if consume else 0)
     return ExtendedGraph(ops, N.check_handle(h))
 
 
