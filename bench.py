@@ -199,7 +199,8 @@ def run_ours(args, rank, world):
     fp64_peak = fp64_peak_tflops() if rank == 0 else None
     if "IFMM_ARENA_GB" not in os.environ:  # the engine arena takes most of the device
         free, _ = torch.cuda.mem_get_info()
-        os.environ["IFMM_ARENA_GB"] = f"{0.92 * free / 2**30:.1f}"
+        # leave ~22 GB outside the arena for the dedicated >= 256 MB blocks
+        os.environ["IFMM_ARENA_GB"] = f"{max(0.5 * free, free - 22 * 2**30) / 2**30:.1f}"
     cfg = args.config
     inp = inputs(cfg, args.n)
     N = inp["N"]

@@ -1031,42 +1031,45 @@ lusolve_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks_per_
     x[i * ld] = ((s0 + s1) + (s2 + s3)) / U[i];
   }
 }
-// One CTA per (system, 32-column chunk): the chunk lives in shared memory
-// (n x 33 padded), lane = column, 8 warps split the rows of each rank-1
-// column sweep; one barrier per pivot.  Final backward values go straight
-// to global memory so no thread ever overwrites a value another may read.
+// One CTA per (system, CW-column chunk): the chunk lives in shared memory
+// (n x (CW+1) padded), column = tid % CW, 256/CW row groups split the rows
+// of each rank-1 column sweep; one barrier per pivot.  Final backward values
+// go straight to global memory so no thread overwrites a value another may
+// still read.
+template <int CW>
 __global__ void __launch_bounds__(256)
 lusolve_smem_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks_per_desc) {
   extern __shared__ double xs[];
-  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  constexpr int LD = CW + 1, RG = 256 / CW;
+  const int c = threadIdx.x % CW, r0 = threadIdx.x / CW;
   const int di = blockIdx.x / chunks_per_desc, ch = blockIdx.x % chunks_per_desc;
   if (di >= ndesc) return;
   const LuSolveDesc d = descs[di];
-  const int c0 = ch * 32;
+  const int c0 = ch * CW;
   if (c0 >= d.nrhs) return;
-  const int nc = min(32, d.nrhs - c0);
+  const int nc = min(CW, d.nrhs - c0);
   const int N = d.n;
   const size_t ld = d.ldx;
-  for (int e = threadIdx.x; e < N * 32; e += blockDim.x) {
-    const int i = e >> 5, cc = e & 31;
-    xs[i * 33 + cc] = cc < nc ? d.X[(size_t)i * ld + c0 + cc] : 0.0;
+  for (int e = threadIdx.x; e < N * CW; e += blockDim.x) {
+    const int i = e / CW, cc = e % CW;
+    xs[i * LD + cc] = cc < nc ? d.X[(size_t)i * ld + c0 + cc] : 0.0;
   }
   __syncthreads();
-  if (threadIdx.x < 32)
+  if (threadIdx.x < CW)
     for (int j = 0; j < N; ++j) {
       const int p = d.piv[j];
-      if (p != j) { const double t = xs[j * 33 + c]; xs[j * 33 + c] = xs[p * 33 + c]; xs[p * 33 + c] = t; }
+      if (p != j) { const double t = xs[j * LD + c]; xs[j * LD + c] = xs[p * LD + c]; xs[p * LD + c] = t; }
     }
   __syncthreads();
   for (int j = 0; j < N - 1; ++j) {
-    const double xj = xs[j * 33 + c];
-    for (int i = j + 1 + r0; i < N; i += 8) xs[i * 33 + c] -= d.LU[(size_t)i * d.lda + j] * xj;
+    const double xj = xs[j * LD + c];
+    for (int i = j + 1 + r0; i < N; i += RG) xs[i * LD + c] -= d.LU[(size_t)i * d.lda + j] * xj;
     __syncthreads();
   }
   for (int j = N - 1; j >= 0; --j) {
-    const double xj = xs[j * 33 + c] / d.LU[(size_t)j * d.lda + j];
-    if (r0 == (j & 7) && c < nc) d.X[(size_t)j * ld + c0 + c] = xj;
-    for (int i = r0; i < j; i += 8) xs[i * 33 + c] -= d.LU[(size_t)i * d.lda + j] * xj;
+    const double xj = xs[j * LD + c] / d.LU[(size_t)j * d.lda + j];
+    if (r0 == (j % RG) && c < nc) d.X[(size_t)j * ld + c0 + c] = xj;
+    for (int i = r0; i < j; i += RG) xs[i * LD + c] -= d.LU[(size_t)i * d.lda + j] * xj;
     __syncthreads();
   }
 }
@@ -1086,15 +1089,31 @@ void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
 void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs, cudaStream_t s,
                     int max_n) {
   if (ndesc <= 0 || max_nrhs <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lusolve_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    cudaFuncSetAttribute(lusolve_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    cudaFuncSetAttribute(lusolve_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
   if (max_n > 0 && max_n <= 800) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(lusolve_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           220 * 1024);
-      attr = true;
-    }
     const int chunks = (max_nrhs + 31) / 32;
-    lusolve_smem_kernel<<<ndesc * chunks, 256, (size_t)max_n * 33 * sizeof(double), s>>>(
+    lusolve_smem_kernel<32><<<ndesc * chunks, 256, (size_t)max_n * 33 * sizeof(double), s>>>(
+        d_descs, ndesc, chunks);
+    return;
+  }
+  if (max_n > 0 && max_n <= 1600) {
+    const int chunks = (max_nrhs + 15) / 16;
+    lusolve_smem_kernel<16><<<ndesc * chunks, 256, (size_t)max_n * 17 * sizeof(double), s>>>(
+        d_descs, ndesc, chunks);
+    return;
+  }
+  if (max_n > 0 && max_n <= 3000) {
+    const int chunks = (max_nrhs + 7) / 8;
+    lusolve_smem_kernel<8><<<ndesc * chunks, 256, (size_t)max_n * 9 * sizeof(double), s>>>(
         d_descs, ndesc, chunks);
     return;
   }

@@ -126,6 +126,7 @@ struct LevelStats {
 struct ElimEv {
   int nx, nz, ny, m, k;
   Blk LU;
+  Blk Pinv;                              // P^{-1} (n x n), used by the solve
   int* piv = nullptr;
   int piv_cls = -1;
   std::vector<int> src, src_off, src_w;  // sources (node, col offset, width)

@@ -452,9 +452,11 @@ void Eliminator::rebase_many(std::vector<RebaseReq>& reqs) {
     g.set(nzn, nyn, a);
     g.set(nyn, nzn, b2);
     if (!(bu.identity && kn == ko)) {
-      Blk r = C.alloc(kn, ko);  // r (kn x ko) kept for the solve replay
-      ce.add(bu.OM.p, ko, 1, r.p, ko, 1, kn, ko, 0);
-      F.rebases.push_back({nyn, r});
+      // factor.py:429-430 records ("rebase", ny, r).  In the replay a rebase
+      // always acts on a zero vector: a live cluster's y node has no edge to
+      // any x node, so its rhs is untouched until its own elimination.  The
+      // event is counted, r itself is not needed by the solve.
+      F.rebases.push_back({nyn, Blk()});
       F.events.push_back({1, (int)F.rebases.size() - 1});
     }
   }
@@ -748,8 +750,11 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       ev.Tstk = C.alloc(std::max(w.Rtgt, 1), m);
       w.NC = Csrc + k;
       w.NR = w.Rtgt + k;
-      w.X = C.alloc(w.n, w.NC);
-      const int NC = w.NC;
+      // X = P^{-1} [[E_src, 0, I_m], [0, -I_k, 0]]: the trailing m columns and
+      // the -I_k block give P^{-1} itself (kept for the solve replay)
+      const int LDX = w.NC + m;
+      w.X = C.alloc(w.n, LDX);
+      const int NC = LDX;
       for (size_t i = 0; i < w.srcB.size(); ++i) {
         cb.add(w.srcB[i].p, w.srcB[i].c, 1, ev.Scat.p + ev.src_off[i], std::max(Csrc, 1), 1, m,
                w.srcB[i].c, 0);
@@ -761,6 +766,8 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       cb.add(nullptr, 0, 0, w.X.p + (size_t)m * NC, NC, 1, k, Csrc, 3);
       cb.add(nullptr, 0, 0, w.X.p + Csrc, NC, 1, m, k, 3);
       cb.add(nullptr, 0, 0, w.X.p + (size_t)m * NC + Csrc, NC, 1, k, k, 2, -1.0);
+      cb.add(nullptr, 0, 0, w.X.p + Csrc + k, NC, 1, m, m, 2, 1.0);                 // I_m
+      cb.add(nullptr, 0, 0, w.X.p + (size_t)m * NC + Csrc + k, NC, 1, k, m, 3);     // 0
       g.dead[w.c] = 1;
       LuSolveDesc d;
       d.LU = w.P.p; d.piv = w.piv; d.n = w.n; d.lda = w.n; d.X = w.X.p; d.nrhs = NC; d.ldx = NC;
@@ -796,15 +803,28 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     CopyBatch cb;
     for (size_t i = 0; i < ws.size(); ++i) {
       W& w = ws[i];
-      const ElimEv& ev = F.elims[e0 + i];
+      ElimEv& ev = F.elims[e0 + i];
+      const int LDX = w.NC + w.m;
       w.Fm = C.alloc(w.NR, w.NC);
-      gb.add(ev.Tstk.p, w.m, 0, w.X.p, w.NC, 0, w.Fm.p, w.NC, w.Rtgt, w.NC, w.m, -1.0, 0.0);
-      cb.add(w.X.p + (size_t)w.m * w.NC, w.NC, 1, w.Fm.p + (size_t)w.Rtgt * w.NC, w.NC, 1, w.k,
+      gb.add(ev.Tstk.p, w.m, 0, w.X.p, LDX, 0, w.Fm.p, w.NC, w.Rtgt, w.NC, w.m, -1.0, 0.0);
+      cb.add(w.X.p + (size_t)w.m * LDX, LDX, 1, w.Fm.p + (size_t)w.Rtgt * w.NC, w.NC, 1, w.k,
              w.NC, 0);
+      // P^{-1} = [X[:, NC:NC+m] | -X[:, Csrc:Csrc+k]]  (n x n)
+      ev.Pinv = C.alloc(w.n, w.n);
+      cb.add(w.X.p + w.NC, LDX, 1, ev.Pinv.p, w.n, 1, w.n, w.m, 0);
+      cb.add(w.X.p + w.Csrc, LDX, 1, ev.Pinv.p + w.m, w.n, 1, w.n, w.k, 0, -1.0);
     }
     run_gemm(gb);
     cb.run(C);
-    for (W& w : ws) C.free(w.X);
+    for (size_t i = 0; i < ws.size(); ++i) {
+      W& w = ws[i];
+      ElimEv& ev = F.elims[e0 + i];
+      C.free(w.X);
+      C.free(ev.LU);  // the solve replays with P^{-1}
+      C.free_raw(ev.piv, ev.piv_cls);
+      ev.piv = nullptr;
+      ev.piv_cls = -1;
+    }
   }
   delete ph;
   ph = new Phase(C, PH_ADD);

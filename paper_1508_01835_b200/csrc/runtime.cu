@@ -70,6 +70,19 @@ double* Arena::alloc(size_t ndoubles, int* cls) {
     peak_ = std::max(peak_, in_use_);
     return reinterpret_cast<double*>(base_ + off);
   }
+  if (bytes >= ((size_t)256 << 20)) {
+    // very large (top-level LU, solve workspace): dedicated cudaMalloc, so a
+    // fragmented slab can never block them (bench leaves headroom for this)
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) == cudaSuccess) {
+      extern_[p] = bytes;
+      in_use_ += bytes;
+      peak_ = std::max(peak_, in_use_);
+      *cls = kExternCls;
+      return reinterpret_cast<double*>(p);
+    }
+    cudaGetLastError();
+  }
   if (bytes >= ((size_t)8 << 20)) {
     // large: first fit from the top of the slab, carved from the block's end
     for (int attempt = 0; attempt < 2; ++attempt) {

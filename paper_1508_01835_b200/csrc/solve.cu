@@ -52,16 +52,15 @@ struct Factor::Program {
   long long sol0 = 0;  // sol region of leaf x (N)
   int max_n = 0;
   int fwd_waves = 0, bwd_waves = 0;
-  std::vector<int> perm;
+  int smem = 0;  // doubles of dynamic shared memory per op
 };
 
 Factor::~Factor() {
   if (!ctx) return;
   for (auto& e : elims) {
-    ctx->free(e.LU); ctx->free(e.Scat); ctx->free(e.Tstk);
+    ctx->free(e.LU); ctx->free(e.Pinv); ctx->free(e.Scat); ctx->free(e.Tstk);
     ctx->free_raw(e.piv, e.piv_cls);
   }
-  for (auto& r : rebases) ctx->free(r.r);
   ctx->free(top_lu);
   if (top_piv) ctx->free_raw(top_piv, top_piv_cls);
   if (prog) {
@@ -78,8 +77,77 @@ Factor::~Factor() {
 // ---------------------------------------------------------------------------
 namespace {
 
-// In-place LU solve of v (smem, length n) by one warp (warp 0 does the
-// serial pivots, lanes split every row dot product).
+// One CTA per elimination op.  Forward (factor.py:111-119):
+//   g = P^{-1}[:, :m] rhs_x ;  rhs[a] -= T_a g[:m] ;  rhs[y] += g[m:]
+// Backward (factor.py:139-146):
+//   v = [rhs_x - S gather(sol_b) ; sol_y] ;  [sol_x ; sol_z] = P^{-1} v
+// Every product is a warp-per-row GEMV (lanes split the dot product, fixed
+// shuffle tree) -> deterministic, no serial triangular solves.
+__global__ void __launch_bounds__(256)
+solve_wave_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists, int first,
+                  int count, double* __restrict__ W) {
+  extern __shared__ double v[];  // n (+ Csrc gather for backward)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int oi = blockIdx.x; oi < count; oi += gridDim.x) {
+    const SolveOp op = ops[first + oi];
+    const int n = op.n, m = op.m;
+    if (op.type == OP_FWD_ELIM) {
+      double* rx = v + n;  // rhs_x staged in smem
+      for (int i = threadIdx.x; i < m; i += blockDim.x) rx[i] = W[op.a + i];
+      __syncthreads();
+      for (int i = warp; i < n; i += nw) {
+        const double* row = op.LU + (size_t)i * n;  // P^{-1} row i, first m columns
+        double s = 0.0;
+        for (int j = lane; j < m; j += 32) s = fma(row[j], rx[j], s);
+        s = warp_sum(s);
+        if (lane == 0) v[i] = s;
+      }
+      __syncthreads();
+      for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+        const ListEnt t = lists[l];
+        for (int i = warp; i < t.len; i += nw) {
+          const double* row = op.M + (size_t)(t.off + i) * op.ldm;
+          double s = 0.0;
+          for (int j = lane; j < m; j += 32) s = fma(row[j], v[j], s);
+          s = warp_sum(s);
+          if (lane == 0) W[t.slot + i] = W[t.slot + i] - s;
+        }
+      }
+      for (int i = threadIdx.x; i < op.k; i += blockDim.x) W[op.b + i] = W[op.b + i] + v[m + i];
+      __syncthreads();
+      continue;
+    }
+    // OP_BWD_ELIM
+    double* gsol = v + n;
+    for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+      const ListEnt s = lists[l];
+      for (int j = threadIdx.x; j < s.len; j += blockDim.x) gsol[s.off + j] = W[s.slot + j];
+    }
+    __syncthreads();
+    for (int i = warp; i < m; i += nw) {
+      const double* row = op.M + (size_t)i * op.ldm;
+      double s = 0.0;
+      for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
+      s = warp_sum(s);
+      if (lane == 0) v[i] = W[op.a + i] - s;
+    }
+    for (int i = threadIdx.x; i < op.k; i += blockDim.x) v[m + i] = W[op.b + i];
+    __syncthreads();
+    for (int i = warp; i < n; i += nw) {
+      const double* row = op.LU + (size_t)i * n;
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s = fma(row[j], v[j], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        if (i < m) W[op.c + i] = s;
+        else W[op.d + i - m] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// In-place LU solve of v (smem) by one warp (top-level system).
 __device__ void warp_lu_solve(const double* __restrict__ LU, const int* __restrict__ piv, int n,
                               double* v) {
   const int lane = threadIdx.x & 31;
@@ -108,73 +176,6 @@ __device__ void warp_lu_solve(const double* __restrict__ LU, const int* __restri
   }
 }
 
-__global__ void __launch_bounds__(256)
-solve_wave_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists, int first,
-                  int count, double* __restrict__ W) {
-  extern __shared__ double v[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int oi = blockIdx.x; oi < count; oi += gridDim.x) {
-    const SolveOp op = ops[first + oi];
-    if (op.type == OP_REBASE) {
-      const double* in = W + op.a;
-      for (int i = warp; i < op.rows; i += nw) {
-        const double* r = op.M + (size_t)i * op.cols;
-        double s = 0.0;
-        for (int j = lane; j < op.cols; j += 32) s = fma(r[j], in[j], s);
-        s = warp_sum(s);
-        if (lane == 0) W[op.b + i] = s;
-      }
-      __syncthreads();
-      continue;
-    }
-    if (op.type == OP_FWD_ELIM) {
-      // g = P^{-1} [rhs_x; 0]
-      for (int i = threadIdx.x; i < op.n; i += blockDim.x) v[i] = i < op.m ? W[op.a + i] : 0.0;
-      __syncthreads();
-      warp_lu_solve(op.LU, op.piv, op.n, v);
-      __syncthreads();
-      // rhs[a] -= T_a g[:m]  over all target rows
-      for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
-        const ListEnt t = lists[l];
-        for (int i = warp; i < t.len; i += nw) {
-          const double* row = op.M + (size_t)(t.off + i) * op.ldm;
-          double s = 0.0;
-          for (int j = lane; j < op.m; j += 32) s = fma(row[j], v[j], s);
-          s = warp_sum(s);
-          if (lane == 0) W[t.slot + i] = W[t.slot + i] - s;
-        }
-      }
-      // rhs[ny] += g[m:]
-      for (int i = threadIdx.x; i < op.k; i += blockDim.x) W[op.b + i] = W[op.b + i] + v[op.m + i];
-      __syncthreads();
-      continue;
-    }
-    // OP_BWD_ELIM: gather sources' solutions into scratch
-    for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
-      const ListEnt s = lists[l];
-      for (int j = threadIdx.x; j < s.len; j += blockDim.x) W[op.e + s.off + j] = W[s.slot + j];
-    }
-    __syncthreads();
-    const double* gsol = W + op.e;
-    for (int i = warp; i < op.m; i += nw) {
-      const double* row = op.M + (size_t)i * op.ldm;
-      double s = 0.0;
-      for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
-      s = warp_sum(s);
-      if (lane == 0) v[i] = W[op.a + i] - s;
-    }
-    for (int i = threadIdx.x; i < op.k; i += blockDim.x) v[op.m + i] = W[op.b + i];
-    __syncthreads();
-    warp_lu_solve(op.LU, op.piv, op.n, v);
-    __syncthreads();
-    for (int i = threadIdx.x; i < op.n; i += blockDim.x) {
-      if (i < op.m) W[op.c + i] = v[i];
-      else W[op.d + i - op.m] = v[i];
-    }
-    __syncthreads();
-  }
-}
-
 __global__ void __launch_bounds__(1024)
 top_solve_kernel(const double* LU, const int* piv, int n, const double* rhs, double* out) {
   extern __shared__ double v[];
@@ -183,6 +184,51 @@ top_solve_kernel(const double* LU, const int* piv, int n, const double* rhs, dou
   warp_lu_solve(LU, piv, n, v);
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v[i];
+}
+
+// Blocked top-level solve for n beyond one CTA's shared memory:
+// per 256-row block a one-warp triangular solve, then a multi-CTA GEMV update
+// of the remaining rows (factor.py:129-135 semantics, LAPACK getrs order).
+__global__ void top_perm_kernel(const int* piv, int n, double* v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int j = 0; j < n; ++j) {
+      const int p = piv[j];
+      if (p != j) { const double t = v[j]; v[j] = v[p]; v[p] = t; }
+    }
+}
+__global__ void top_diag_kernel(const double* LU, int n, int b0, int bs, double* v, int upper) {
+  const int lane = threadIdx.x;
+  if (!upper) {
+    for (int i = b0 + 1; i < b0 + bs; ++i) {
+      const double* L = LU + (size_t)i * n;
+      double s = 0.0;
+      for (int j = b0 + lane; j < i; j += 32) s = fma(L[j], v[j], s);
+      s = warp_sum(s);
+      if (lane == 0) v[i] -= s;
+      __syncwarp();
+    }
+  } else {
+    for (int i = b0 + bs - 1; i >= b0; --i) {
+      const double* U = LU + (size_t)i * n;
+      double s = 0.0;
+      for (int j = i + 1 + lane; j < b0 + bs; j += 32) s = fma(U[j], v[j], s);
+      s = warp_sum(s);
+      if (lane == 0) v[i] = (v[i] - s) / U[i];
+      __syncwarp();
+    }
+  }
+}
+// rows [r0, r1): v[i] -= sum_{j in [c0, c0+bs)} A[i][j] v[j]
+__global__ void top_update_kernel(const double* LU, int n, int r0, int r1, int c0, int bs,
+                                  double* v) {
+  const int lane = threadIdx.x & 31;
+  const int row = r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= r1) return;
+  const double* A = LU + (size_t)row * n + c0;
+  double s = 0.0;
+  for (int j = lane; j < bs; j += 32) s = fma(A[j], v[c0 + j], s);
+  s = warp_sum(s);
+  if (lane == 0) v[row] -= s;
 }
 
 __global__ void gather_perm_kernel(const double* b, const int* perm, int n, double* out) {
@@ -200,69 +246,43 @@ __global__ void scatter_perm_kernel(const double* in, const int* perm, int n, do
 // host side: compile the event log
 // ---------------------------------------------------------------------------
 void Factor::build_program(const std::vector<int>& final_size) {
-  (void)final_size;
   Ctx& C = *ctx;
   prog = new Program;
   Program& P = *prog;
   const int nnodes = (int)std::max(init_sizes.size(), final_size.size());
-  std::vector<int> nsize(nnodes, 0);
-  for (size_t i = 0; i < init_sizes.size(); ++i) nsize[i] = init_sizes[i];
-  for (auto& mv : merges) {
-    int s = 0;
-    for (int q : mv.psize) s += q;
-    nsize[mv.px] = s;
-  }
-  // ---- versions of y nodes ----
-  std::vector<int> nver(nnodes, 1);
-  for (auto& ev : events)
-    if (ev.type == 1) nver[rebases[ev.idx].ny]++;
-  // final-version alias targets
-  std::vector<long long> final_slot(nnodes, -1);
-  long long top = n_points;  // [0, N) leaf x slots
+  // Slots.  Forward rhs: leaf x in [0, N) (sorted order); every merged
+  // parent x gets a region holding its children's y slots (factor.py:123);
+  // the level-2 y slots live in the top rhs region.  Rebases act on zero
+  // rhs (see factor.cu) and need no slots of their own.
+  std::vector<long long> rslot(nnodes, -1), sslot(nnodes, -1);
+  long long top = n_points;
   auto alloc = [&](long long n) { long long o = top; top += n; return o; };
-  // merged parents: region per px; parts alias final versions
-  std::vector<long long> xslot(nnodes, -1);
-  for (int t = 0; t < (int)leaf_nodes.size(); ++t) xslot[leaf_nodes[t]] = leaf_start[t];
+  for (int t = 0; t < (int)leaf_nodes.size(); ++t) rslot[leaf_nodes[t]] = leaf_start[t];
   for (auto& mv : merges) {
-    const long long o = alloc(nsize[mv.px]);
-    xslot[mv.px] = o;
+    long long sz = 0;
+    for (int q : mv.psize) sz += q;
+    const long long o = alloc(sz);
+    rslot[mv.px] = o;
     long long off = 0;
     for (size_t q = 0; q < mv.parts.size(); ++q) {
-      final_slot[mv.parts[q]] = o + off;
+      rslot[mv.parts[q]] = o + off;
       off += mv.psize[q];
     }
   }
   P.top_n = 0;
   for (int s : top_sizes) P.top_n += s;
-  // a top node is an x node only for depth < 2 (no elimination at all): the
-  // top system is then the leaf region itself
-  const bool top_is_x = !top_nodes.empty() && xslot[top_nodes[0]] >= 0;
+  const bool top_is_x = !top_nodes.empty() && rslot[top_nodes[0]] >= 0;
   P.top_rhs = top_is_x ? 0 : alloc(P.top_n);
   if (!top_is_x) {
     long long off = 0;
     for (size_t q = 0; q < top_nodes.size(); ++q) {
-      final_slot[top_nodes[q]] = P.top_rhs + off;
+      rslot[top_nodes[q]] = P.top_rhs + off;
       off += top_sizes[q];
     }
   }
-  // version slots
-  std::vector<std::vector<long long>> vslot(nnodes);
-  std::vector<std::vector<int>> vsize(nnodes);
-  {
-    // sizes per version: v0 = init size; after each rebase = r rows
-    for (int i = 0; i < nnodes; ++i) vsize[i].push_back(nsize[i]);
-    for (auto& ev : events)
-      if (ev.type == 1) vsize[rebases[ev.idx].ny].push_back(rebases[ev.idx].r.r);
-    for (int i = 0; i < nnodes; ++i) {
-      if (xslot[i] >= 0) { vslot[i].push_back(xslot[i]); continue; }
-      for (int v = 0; v < nver[i]; ++v) {
-        const bool last = v == nver[i] - 1;
-        vslot[i].push_back(last && final_slot[i] >= 0 ? final_slot[i] : alloc(vsize[i][v]));
-      }
-    }
-  }
-  // ---- solution slots ----
-  std::vector<long long> sslot(nnodes, -1);
+  // backward solutions: leaf x in the sol region (sorted order), merged
+  // parents' regions contain their children's y, the top solution holds the
+  // level-2 y; z solutions get their own slots.
   P.sol0 = alloc(n_points);
   for (int t = 0; t < (int)leaf_nodes.size(); ++t) sslot[leaf_nodes[t]] = P.sol0 + leaf_start[t];
   P.top_sol = top_is_x ? P.sol0 : alloc(P.top_n);
@@ -273,10 +293,11 @@ void Factor::build_program(const std::vector<int>& final_size) {
       off += top_sizes[q];
     }
   }
-  // merged parents' sol regions (top-down so children alias inside)
   for (int mi = (int)merges.size() - 1; mi >= 0; --mi) {
     auto& mv = merges[mi];
-    if (sslot[mv.px] < 0) sslot[mv.px] = alloc(nsize[mv.px]);
+    long long sz = 0;
+    for (int q : mv.psize) sz += q;
+    if (sslot[mv.px] < 0) sslot[mv.px] = alloc(sz);
     long long off = 0;
     for (size_t q = 0; q < mv.parts.size(); ++q) {
       sslot[mv.parts[q]] = sslot[mv.px] + off;
@@ -285,27 +306,24 @@ void Factor::build_program(const std::vector<int>& final_size) {
   }
   for (auto& E : elims) {
     if (sslot[E.nz] < 0) sslot[E.nz] = alloc(E.k);
-    if (sslot[E.nx] < 0) sslot[E.nx] = alloc(E.m);
+    IFMM_ASSERT(rslot[E.nx] >= 0 && rslot[E.ny] >= 0 && sslot[E.nx] >= 0 && sslot[E.ny] >= 0,
+                "solve program: unmapped slot");
   }
-
-  // ---- ops + dependency waves ----
-  std::vector<SolveOp> fops, bops;
-  std::vector<ListEnt> lists;
-  std::vector<int> fwave, bwave;
-  // resources: slot start offsets identify atomic slots; composite px slots
-  // are expanded to their parts via the merge table.
-  std::map<int, std::vector<long long>> comp;  // px -> child final slots
+  // composite resources: a merged parent x = its children's y slots
+  std::map<int, std::vector<long long>> comp_r, comp_s;
   for (auto& mv : merges) {
-    std::vector<long long> v;
-    for (int q : mv.parts) v.push_back(final_slot[q]);
-    comp[mv.px] = v;
+    for (int q : mv.parts) {
+      comp_r[mv.px].push_back(rslot[q]);
+      comp_s[mv.px].push_back(sslot[q]);
+    }
   }
-  std::unordered_map<long long, int> lw, lr;  // last write wave / max read wave
-  auto res_of = [&](int node, long long slot, std::vector<long long>& out) {
+  auto res = [](const std::map<int, std::vector<long long>>& comp, int node, long long slot,
+                std::vector<long long>& out) {
     auto it = comp.find(node);
-    if (it != comp.end()) { for (long long s : it->second) out.push_back(s); }
+    if (it != comp.end()) for (long long s : it->second) out.push_back(s);
     else out.push_back(slot);
   };
+  std::unordered_map<long long, int> lw, lr;
   auto wave_for = [&](const std::vector<long long>& rd, const std::vector<long long>& wr) {
     int w = 0;
     for (long long r : rd) { auto it = lw.find(r); if (it != lw.end()) w = std::max(w, it->second); }
@@ -318,59 +336,36 @@ void Factor::build_program(const std::vector<int>& final_size) {
     for (long long r : wr) lw[r] = w;
     return w;
   };
-  std::vector<int> cur(nnodes, 0);
-  P.max_n = 0;
+  std::vector<SolveOp> fops, bops;
+  std::vector<ListEnt> lists;
+  std::vector<int> fwave, bwave;
+  P.max_n = 1;
+  int max_smem = 1;
   for (auto& ev : events) {
-    if (ev.type == 0) {
-      const ElimEv& E = elims[ev.idx];
-      SolveOp o{};
-      o.type = OP_FWD_ELIM;
-      o.n = E.m + E.k; o.m = E.m; o.k = E.k;
-      o.LU = E.LU.p; o.piv = E.piv; o.M = E.Tstk.p; o.ldm = E.m;
-      o.a = vslot[E.nx][cur[E.nx]];
-      o.b = vslot[E.ny][cur[E.ny]];
-      o.list0 = (int)lists.size(); o.nlist = (int)E.tgt.size();
-      std::vector<long long> rd, wr;
-      res_of(E.nx, o.a, rd);
-      wr.push_back(o.b);
-      for (size_t t = 0; t < E.tgt.size(); ++t) {
-        const int a = E.tgt[t];
-        const long long s = vslot[a][cur[a]];
-        lists.push_back({s, E.tgt_off[t], E.tgt_h[t]});
-        res_of(a, s, wr);
-      }
-      P.max_n = std::max(P.max_n, o.n);
-      fops.push_back(o);
-      fwave.push_back(wave_for(rd, wr));
-    } else if (ev.type == 1) {
-      const RebaseEv& R = rebases[ev.idx];
-      SolveOp o{};
-      o.type = OP_REBASE;
-      o.M = R.r.p; o.rows = R.r.r; o.cols = R.r.c;
-      o.a = vslot[R.ny][cur[R.ny]];
-      cur[R.ny]++;
-      o.b = vslot[R.ny][cur[R.ny]];
-      fops.push_back(o);
-      fwave.push_back(wave_for({o.a}, {o.b}));
+    if (ev.type != 0) continue;
+    const ElimEv& E = elims[ev.idx];
+    SolveOp o{};
+    o.type = OP_FWD_ELIM;
+    o.n = E.m + E.k; o.m = E.m; o.k = E.k;
+    o.LU = E.Pinv.p; o.M = E.Tstk.p; o.ldm = E.m;
+    o.a = rslot[E.nx];
+    o.b = rslot[E.ny];
+    o.list0 = (int)lists.size(); o.nlist = (int)E.tgt.size();
+    std::vector<long long> rd, wr;
+    res(comp_r, E.nx, o.a, rd);
+    wr.push_back(o.b);
+    for (size_t t = 0; t < E.tgt.size(); ++t) {
+      const int a = E.tgt[t];
+      IFMM_ASSERT(rslot[a] >= 0, "solve program: unmapped target");
+      lists.push_back({rslot[a], E.tgt_off[t], E.tgt_h[t]});
+      res(comp_r, a, rslot[a], wr);
     }
+    P.max_n = std::max(P.max_n, o.n);
+    max_smem = std::max(max_smem, o.n + o.m);
+    fops.push_back(o);
+    fwave.push_back(wave_for(rd, wr));
   }
-  // sanity: final versions reached the aliased slots
-  for (auto& mv : merges)
-    for (int q : mv.parts) IFMM_ASSERT(vslot[q][cur[q]] == final_slot[q], "merge alias broken");
   lw.clear(); lr.clear();
-  std::map<int, std::vector<long long>> comp_sol;
-  for (auto& mv : merges) {
-    std::vector<long long> v;
-    for (int q : mv.parts) v.push_back(sslot[q]);
-    comp_sol[mv.px] = v;
-  }
-  auto res_sol = [&](int node, std::vector<long long>& out) {
-    auto it = comp_sol.find(node);
-    if (it != comp_sol.end()) { for (long long s : it->second) out.push_back(s); }
-    else out.push_back(sslot[node]);
-  };
-  long long scratch = 0;
-  std::vector<long long> bscr;
   for (int ei = (int)events.size() - 1; ei >= 0; --ei) {
     const Event& ev = events[ei];
     if (ev.type != 0) continue;
@@ -378,8 +373,8 @@ void Factor::build_program(const std::vector<int>& final_size) {
     SolveOp o{};
     o.type = OP_BWD_ELIM;
     o.n = E.m + E.k; o.m = E.m; o.k = E.k;
-    o.LU = E.LU.p; o.piv = E.piv; o.M = E.Scat.p; o.ldm = E.Scat.c;
-    o.a = vslot[E.nx][0];
+    o.LU = E.Pinv.p; o.M = E.Scat.p; o.ldm = E.Scat.c;
+    o.a = rslot[E.nx];
     o.b = sslot[E.ny];
     o.c = sslot[E.nx];
     o.d = sslot[E.nz];
@@ -392,21 +387,15 @@ void Factor::build_program(const std::vector<int>& final_size) {
     for (size_t t = 0; t < E.src.size(); ++t) {
       const int b = E.src[t];
       lists.push_back({sslot[b], E.src_off[t], E.src_w[t]});
-      res_sol(b, rd);
+      res(comp_s, b, sslot[b], rd);
     }
-    res_sol(E.nx, wr);  // a px's solution slots are its children's y slots
+    res(comp_s, E.nx, o.c, wr);
     wr.push_back(o.d);
-    o.e = -1;
-    bscr.push_back(csrc);
+    max_smem = std::max(max_smem, o.n + csrc);
     bops.push_back(o);
     bwave.push_back(wave_for(rd, wr));
-    scratch = std::max<long long>(scratch, csrc);
   }
-  // gather scratch: one region per op (ops of one wave run concurrently)
-  for (size_t i = 0; i < bops.size(); ++i) bops[i].e = alloc(std::max<long long>(bscr[i], 1));
   const long long wtot = top;
-
-  // ---- sort ops by wave ----
   auto order_by = [](const std::vector<int>& wv, std::vector<int>& starts) {
     std::vector<int> idx(wv.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
@@ -427,6 +416,7 @@ void Factor::build_program(const std::vector<int>& final_size) {
   P.n_bwd = (int)bops.size();
   P.fwd_waves = (int)P.fwd_wave_start.size() - 1;
   P.bwd_waves = (int)P.bwd_wave_start.size() - 1;
+  P.smem = max_smem;
   const size_t ob = all.size() * sizeof(SolveOp), lb = lists.size() * sizeof(ListEnt);
   P.ops_d = C.alloc(1, (int)(ob / 8 + 1));
   P.list_d = C.alloc(1, (int)(lb / 8 + 1));
@@ -444,30 +434,47 @@ void Factor::solve(const double* d_b, double* d_x) {
     cudaFuncSetAttribute(top_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  IFMM_ASSERT(prog->top_n <= 25000 && prog->max_n <= 25000, "solve vector exceeds shared memory");
+  IFMM_ASSERT(prog->smem <= 25000, "solve vector exceeds shared memory");
   Program& P = *prog;
   const int N = n_points;
   double* W = P.work.p;
-  double solve_bytes = 0;  // algorithmic bytes: every stored factor block read twice
-  for (auto& e : elims)
-    solve_bytes += 8.0 * (2.0 * (double)(e.m + e.k) * (e.m + e.k) + (double)e.m * e.Scat.c +
-                          (double)e.Tstk.r * e.m);
-  for (auto& r : rebases) solve_bytes += 8.0 * r.r.r * r.r.c;
+  // algorithmic bytes: P^{-1}[:, :m] + T (forward), S + P^{-1} (backward)
+  double solve_bytes = 0;
+  for (auto& e : elims) {
+    const double n = e.m + e.k;
+    solve_bytes += 8.0 * (n * e.m + n * n + (double)e.Tstk.r * e.m + (double)e.m * e.Scat.c);
+  }
   const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
   CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, C.st));
   gather_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(d_b, d_perm, N, W);
   const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
   const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
-  const size_t smem = (size_t)std::max(P.max_n, 1) * sizeof(double);
+  const size_t smem = (size_t)std::max(P.smem, 1) * sizeof(double);
   cudaEvent_t ka = nullptr;
   C.kt_begin(K_SOLVE, 0, &ka);
   for (int w = 0; w < P.fwd_waves; ++w) {
     const int a = P.fwd_wave_start[w], b = P.fwd_wave_start[w + 1];
     solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
   }
-  if (P.top_n > 0) {
+  if (P.top_n > 0 && P.top_n <= 20000) {
     top_solve_kernel<<<1, 1024, (size_t)P.top_n * sizeof(double), C.st>>>(
         top_lu.p, top_piv, P.top_n, W + P.top_rhs, W + P.top_sol);
+  } else if (P.top_n > 0) {
+    const int n = P.top_n, bs = 256;
+    double* v = W + P.top_sol;
+    CUDA_CHECK(cudaMemcpyAsync(v, W + P.top_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, C.st));
+    top_perm_kernel<<<1, 32, 0, C.st>>>(top_piv, n, v);
+    for (int b0 = 0; b0 < n; b0 += bs) {  // L (unit) forward
+      const int b = std::min(bs, n - b0);
+      top_diag_kernel<<<1, 32, 0, C.st>>>(top_lu.p, n, b0, b, v, 0);
+      if (b0 + b < n)
+        top_update_kernel<<<(n - b0 - b + 7) / 8, 256, 0, C.st>>>(top_lu.p, n, b0 + b, n, b0, b, v);
+    }
+    for (int b0 = ((n - 1) / bs) * bs; b0 >= 0; b0 -= bs) {  // U backward
+      const int b = std::min(bs, n - b0);
+      top_diag_kernel<<<1, 32, 0, C.st>>>(top_lu.p, n, b0, b, v, 1);
+      if (b0 > 0) top_update_kernel<<<(b0 + 7) / 8, 256, 0, C.st>>>(top_lu.p, n, 0, b0, b0, b, v);
+    }
   }
   for (int w = 0; w < P.bwd_waves; ++w) {
     const int a = P.n_fwd + P.bwd_wave_start[w], b = P.n_fwd + P.bwd_wave_start[w + 1];

@@ -68,7 +68,8 @@ def test_svd(N, m, n):
     np.testing.assert_allclose(Uo.T @ Uo, np.eye(r), atol=1e-12)
 
 
-@pytest.mark.parametrize("n,nrhs", [(1, 1), (17, 3), (90, 40), (160, 70), (161, 5), (400, 33)])
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (17, 3), (90, 40), (160, 70), (161, 5), (400, 33),
+                                    (1000, 40), (2000, 9)])
 def test_lu_solve(N, n, nrhs):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((n, n)) + n * 0.05 * np.eye(n)
