@@ -15,6 +15,7 @@
 #include "dense.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace ifmm {
 
@@ -453,7 +454,8 @@ namespace {
 // singular value moves by <= delta, so `sigma > thr` only differs from an
 // exact SVD for sigma within delta of thr.
 __global__ void __launch_bounds__(512)
-fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
+fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_doubles,
+                double delta_rel) {
   extern __shared__ double smem[];
   __shared__ double red[32];
   __shared__ long long redi[32];
@@ -496,7 +498,7 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
       __syncthreads();
       continue;
     }
-    const double delta = fmax(1e-6 * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
+    const double delta = fmax(delta_rel * thr, 2.2e-16 * sqrt(fro) * sqrt((double)kmax));
     const int r0 = cta_qrcp(A, m, nn, kmax, nrm, perm, tau, delta * delta, red, redi);
     if (r0 == 0) { if (threadIdx.x == 0) *d.rank = 0; __syncthreads(); continue; }
     // Q0 (m x r0) and W2 = (R0 P^T)^T (n x r0)
@@ -539,8 +541,14 @@ void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim, cud
       attr2 = true;
     }
     const size_t bytes = svd_smem_doubles(max_smem_dim) * sizeof(double);
+    static double delta_rel = -1.0;
+    if (delta_rel < 0) {  // IFMM_FILL_DELTA: truncation tolerance of the QRCP (x thr)
+      const char* e = getenv("IFMM_FILL_DELTA");
+      delta_rel = e ? atof(e) : 1e-6;
+    }
     fill_svd_kernel<<<n < 4096 ? n : 4096, 512, bytes, s>>>(d_descs, n, thr,
-                                                           (int)(bytes / sizeof(double)));
+                                                           (int)(bytes / sizeof(double)),
+                                                           delta_rel);
     return;
   }
   if (n <= 0) return;
