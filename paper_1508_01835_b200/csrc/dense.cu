@@ -1464,3 +1464,94 @@ void launch_extend(double* NB, int m, int k, const double* G, int extra, double*
 }
 
 }  // namespace ifmm
+
+// ============================================================================
+// Randomized SVD pieces (lowrank.py:79-125) for large fills
+// ============================================================================
+namespace ifmm {
+namespace {
+
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void randn_kernel(const RandDesc* __restrict__ descs, int n) {
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const RandDesc d = descs[b];
+    for (int e = threadIdx.x; e < d.count; e += blockDim.x) {
+      const unsigned long long r1 = splitmix(d.key ^ (2ull * e + 1ull) * 0x632be59bd9b4e019ULL);
+      const unsigned long long r2 = splitmix(r1 ^ 0x85ebca6b2ull);
+      const double u1 = ((r1 >> 11) + 1) * (1.0 / 9007199254740993.0);  // (0, 1]
+      const double u2 = (r2 >> 11) * (1.0 / 9007199254740992.0);
+      d.out[e] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) orth_kernel(const OrthDesc* __restrict__ descs, int n) {
+  __shared__ double red[32];
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const OrthDesc d = descs[b];
+    double* A = d.work;                 // copy of Y (reflectors)
+    double* tau = A + (size_t)d.m * d.w;
+    for (long long e = threadIdx.x; e < (long long)d.m * d.w; e += blockDim.x) A[e] = d.Y[e];
+    __syncthreads();
+    cta_geqrf(A, d.m, d.w, d.m, tau, red);
+    cta_orgqr(A, d.m, d.w, d.m, tau, d.Y, d.m);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512)
+rsvd_fin_kernel(const RsvdFinDesc* __restrict__ descs, int n, double thr) {
+  __shared__ int sflag;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const RsvdFinDesc d = descs[b];
+    const int w = d.w;
+    double* Wb = d.work;                 // w x w
+    double* sig = Wb + (size_t)w * w;
+    int* order = (int*)(sig + w);
+    // B^T = V S Wb^T  (one-sided Jacobi on the w columns of B^T)
+    cta_jacobi(d.Bt, d.n, w, d.n, Wb, &sflag);
+    cta_sv_order(d.Bt, d.n, w, d.n, sig, order);
+    int keep = 0;
+    for (int j = 0; j < w; ++j) keep += sig[order[j]] > thr;
+    const int cap = d.full;
+    if (keep > cap) keep = cap;
+    // lowrank.py:104: stop if width >= full or k_try >= cap or s[k_try] <= thr
+    const bool stop = w >= d.full || d.k_try >= cap || (w > d.k_try && sig[order[d.k_try]] <= thr);
+    // U = Q Wb[:, order[:keep]]  (m x keep), V = B^T col / sigma
+    for (long long e = threadIdx.x; e < (long long)d.m * keep; e += blockDim.x) {
+      const int a = (int)(e / d.m), i = (int)(e % d.m);
+      const double* wv = Wb + (size_t)order[a] * w;
+      double acc = 0.0;
+      for (int l = 0; l < w; ++l) acc = fma(d.Q[(size_t)l * d.m + i], wv[l], acc);
+      d.U[(size_t)a * d.m + i] = acc;
+    }
+    for (long long e = threadIdx.x; e < (long long)d.n * keep; e += blockDim.x) {
+      const int a = (int)(e / d.n), i = (int)(e % d.n);
+      const int j = order[a];
+      d.V[(size_t)a * d.n + i] = d.Bt[(size_t)j * d.n + i] / sig[j];
+    }
+    for (int a = threadIdx.x; a < keep; a += blockDim.x) d.S[a] = sig[order[a]];
+    if (threadIdx.x == 0) { *d.rank = keep; *d.stop = stop ? 1 : 0; }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void launch_randn(const RandDesc* d, int n, cudaStream_t s) {
+  if (n > 0) randn_kernel<<<n < 4096 ? n : 4096, 256, 0, s>>>(d, n);
+}
+void launch_orth(const OrthDesc* d, int n, cudaStream_t s) {
+  if (n > 0) orth_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d, n);
+}
+void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s) {
+  if (n > 0) rsvd_fin_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d, n, thr);
+}
+
+}  // namespace ifmm

@@ -154,3 +154,38 @@ void launch_extend(double* NB, int m, int k, const double* G, int extra, double*
 namespace ifmm {
 void union_profile(unsigned long long* out, int reset);
 }
+
+namespace ifmm {
+// ---- randomized SVD pieces for large fills (lowrank.py:79-125) ----
+// Gaussian sketch: out (n x w row-major) ~ N(0,1), counter-based (seed, tag)
+struct RandDesc {
+  double* out;
+  int count;            // n * w
+  unsigned long long key;
+};
+void launch_randn(const RandDesc* d, int n, cudaStream_t s);
+// Orthonormal basis of a col-major m x w block, in place (Householder QR +
+// explicit Q).  work >= m*w + w doubles per desc.
+struct OrthDesc {
+  double* Y;   // col-major m x w (ld m) -> overwritten with Q
+  int m, w;
+  double* work;
+};
+void launch_orth(const OrthDesc* d, int n, cudaStream_t s);
+// SVD of B (w x n) given B^T col-major (n x w, ld n); U = Q Wb (m x keep,
+// col-major ld m), S, V (n x keep col-major ld n).  rank = #{s > thr}
+// (capped), flag[0] = 1 when the reference's doubling test says "stop"
+// (width >= full or k_try >= cap or s[k_try] <= thr).
+struct RsvdFinDesc {
+  double* Bt;        // n x w col-major (clobbered)
+  const double* Q;   // m x w col-major
+  int m, n, w, k_try, full;
+  double* U;
+  double* S;
+  double* V;
+  int* rank;
+  int* stop;
+  double* work;      // >= w*w + 2w + 8
+};
+void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s);
+}  // namespace ifmm

@@ -254,6 +254,17 @@ struct Eliminator {
   void process_pairs(std::vector<PairJob>& pairs, LevelStats& st);
   void run_wave(std::vector<PairJob*>& jobs, LevelStats& st);
   void eliminate_wave(const std::vector<int>& cs, LevelStats& st);
+  bool exact_fill = false;
+  unsigned long long rsvd_calls = 0;
+  template <class T>
+  std::vector<unsigned long long> items_key(const T& items) {
+    std::vector<unsigned long long> k;
+    for (auto& it : items)
+      k.push_back(((unsigned long long)(unsigned)it.first.first << 32) | (unsigned)it.first.second);
+    return k;
+  }
+  void rsvd_fills(std::vector<SvdDesc>& sd, const std::vector<int>& big,
+                  const std::vector<unsigned long long>& keys, int* dr);
   void merge(int level);
   void top();
 };
@@ -910,10 +921,17 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       sd[i].rank = dr + i;
       sd[i].work = wsb.p + wo[i];
     }
-    // small blocks use a shared-memory workspace, large ones global memory
-    // with the full L1 as cache: two launches running concurrently
+    // factor.py:329-332: fills with min(shape) > 64 are compressed by the
+    // randomized SVD (as the reference does); the rest exactly, through the
+    // rank-revealing pivoted QR (shared- or global-memory workspace variants
+    // run as two concurrent launches).
     std::vector<SvdDesc> sds, sdg;
-    for (auto& x : sd) (svd_work_doubles(x.m, x.n) <= smem_d ? sds : sdg).push_back(x);
+    std::vector<int> big;
+    for (int i = 0; i < ns; ++i) {
+      const SvdDesc& x = sd[i];
+      if (std::min(x.m, x.n) > 64 && !exact_fill) big.push_back(i);
+      else (svd_work_doubles(x.m, x.n) <= smem_d ? sds : sdg).push_back(x);
+    }
     SvdDesc* dss = sds.empty() ? nullptr : C.stage.push_vec(C, sds);
     SvdDesc* dsg = sdg.empty() ? nullptr : C.stage.push_vec(C, sdg);
     cudaEvent_t ka = nullptr;
@@ -922,10 +940,9 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       C.fork2([&](cudaStream_t s) { launch_svd(dss, (int)sds.size(), thr, smem_dim, s, 0); },
               [&](cudaStream_t s) { launch_svd(dsg, (int)sdg.size(), thr, 0, s, 0); });
     else if (dss) launch_svd(dss, (int)sds.size(), thr, smem_dim, C.st, 0);
-    else launch_svd(dsg, (int)sdg.size(), thr, 0, C.st, 0);
+    else if (dsg) launch_svd(dsg, (int)sdg.size(), thr, 0, C.st, 0);
     C.kt_end(K_SVD, sflops, ka);
-    C.launches++;
-    CUDA_CHECK(cudaGetLastError());
+    if (!big.empty()) rsvd_fills(sd, big, items_key(items), dr);
     const int* hr = C.readback_ints(dr, ns);
     for (int i = 0; i < ns; ++i) {
       fac[i].U = sd[i].U; fac[i].S = sd[i].S; fac[i].V = sd[i].V;
@@ -956,6 +973,85 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
   C.free(wsb);
   for (W& w : ws) C.free(w.Fm);
   C.flush();
+}
+
+// Randomized SVD of the large fills (lowrank.py:79-125, start_rank 16,
+// oversample 10, 2 power iterations, rank doubling), batched across the
+// fills: sketch, GEMMs (grouped DMMA), orthonormalisation and the final
+// small SVD are one launch each per round; the host re-runs the fills whose
+// doubling test has not stopped.  Writes rank into dr[i].
+void Eliminator::rsvd_fills(std::vector<SvdDesc>& sd, const std::vector<int>& big,
+                            const std::vector<unsigned long long>& keys, int* dr) {
+  struct A { int i, m, n, full, k_try; };
+  std::vector<A> act;
+  for (int i : big) {
+    const int full = std::min(sd[i].m, sd[i].n);
+    act.push_back({i, sd[i].m, sd[i].n, full, std::min(16, full)});
+  }
+  Blk stopb = C.alloc(1, (int)big.size() / 2 + 2);
+  int* d_stop = reinterpret_cast<int*>(stopb.p);
+  std::vector<int> final_rank(sd.size(), -1);
+  while (!act.empty()) {
+    ++rsvd_calls;
+    const int na = (int)act.size();
+    std::vector<Blk> Om(na), Yt(na), Zt(na), Ow(na), Fw(na);
+    std::vector<RandDesc> rd;
+    std::vector<OrthDesc> od;
+    std::vector<RsvdFinDesc> fd;
+    GemmBatch g0, g1, g2, g3;
+    for (int t = 0; t < na; ++t) {
+      A& a = act[t];
+      const SvdDesc& s = sd[a.i];
+      const int w = std::min(a.k_try + 10, a.full);
+      const double* M = s.src;  // row-major m x n, ld s_r
+      const int ld = s.s_r;
+      Om[t] = C.alloc(a.n, w);
+      Yt[t] = C.alloc(w, a.m);   // Y col-major m x w
+      Zt[t] = C.alloc(w, a.n);   // Z col-major n x w
+      Ow[t] = C.alloc(1, a.m * w + w + 8);
+      Fw[t] = C.alloc(1, w * w + 2 * w + 8);
+      rd.push_back({Om[t].p, a.n * w, (keys[a.i] * 0x9e3779b97f4a7c15ULL) ^ ((unsigned long long)a.k_try << 48) ^ rsvd_calls});
+      // Y^T = Om^T M^T ; Z^T = Q^T M ; Y^T = Z^T M^T
+      g0.add(Om[t].p, w, 1, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
+      g1.add(Yt[t].p, a.m, 0, M, ld, 0, Zt[t].p, a.n, w, a.n, a.m, 1.0, 0.0);
+      g2.add(Zt[t].p, a.n, 0, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
+      od.push_back({Yt[t].p, a.m, w, Ow[t].p});
+      RsvdFinDesc f;
+      f.Bt = Zt[t].p; f.Q = Yt[t].p; f.m = a.m; f.n = a.n; f.w = w; f.k_try = a.k_try;
+      f.full = a.full; f.U = s.U; f.S = s.S; f.V = s.V; f.rank = s.rank; f.stop = d_stop + t;
+      f.work = Fw[t].p;
+      fd.push_back(f);
+    }
+    launch_randn(C.stage.push_vec(C, rd), na, C.st);
+    OrthDesc* dod = C.stage.push_vec(C, od);
+    run_gemm(g0);
+    for (int q = 0; q < 2; ++q) {  // power iterations (lowrank.py:99-100)
+      launch_orth(dod, na, C.st);
+      GemmBatch a1 = g1, a2 = g2;
+      run_gemm(a1);
+      run_gemm(a2);
+    }
+    launch_orth(dod, na, C.st);
+    run_gemm(g1);  // B^T = M^T Q  (into Zt)
+    launch_rsvd_fin(C.stage.push_vec(C, fd), na, thr, C.st);
+    C.launches += 8;
+    CUDA_CHECK(cudaGetLastError());
+    const int* hs = C.readback_ints(d_stop, na);
+    std::vector<int> stop(hs, hs + na);
+    std::vector<A> next;
+    for (int t = 0; t < na; ++t) {
+      if (!stop[t]) {
+        A a = act[t];
+        a.k_try = std::min(2 * a.k_try, a.full);
+        next.push_back(a);
+      }
+      C.free(Om[t]); C.free(Yt[t]); C.free(Zt[t]); C.free(Ow[t]); C.free(Fw[t]);
+    }
+    C.flush();
+    act.swap(next);
+  }
+  C.free(stopb);
+  (void)dr;
 }
 
 // Waves of clusters of one level: Morton order, a cluster joins the first
@@ -1107,6 +1203,7 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
   }
   Eliminator el(C, g, *F, eps * sigma0, 0x1f2e3d4c5b6a7988ULL);
   el.exact_order = (flags & 1) != 0;
+  el.exact_fill = (flags & 2) != 0 || getenv("IFMM_EXACT_FILL") != nullptr;
   for (double& v : g_prof) v = 0.0;
   try {
     for (int l = T.depth; l >= 2; --l) {
@@ -1116,10 +1213,20 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
       C.check_status("cluster ");
       F->levels.push_back(st);
       if (l > 2) el.merge(l);
-      if (getenv("IFMM_MEMTRACE"))
+      if (getenv("IFMM_MEMTRACE")) {
         fprintf(stderr, "[ifmm] level %d done: arena in use %.2f GB, peak %.2f GB, %.1f s\n", l,
                 C.arena.in_use() / 1073741824.0, C.arena.peak() / 1073741824.0,
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        if (C.ktime_on) {
+          C.kt_collect();
+          static const char* nm[] = {"gemm", "copy", "svd", "union", "lu", "lusolve", "spmv",
+                                     "solve", "other"};
+          fprintf(stderr, "[ifmm]   cumulative kernel s:");
+          for (int i = 0; i < K_NCAT; ++i)
+            if (C.kcount[i]) fprintf(stderr, " %s %.2f (%lld)", nm[i], C.ktime[i], C.kcount[i]);
+          fprintf(stderr, "\n");
+        }
+      }
     }
     el.top();
     C.sync();
