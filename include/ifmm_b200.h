@@ -94,6 +94,12 @@ int ifmm_factor_timings(void* factor, double* out, int n_out);
  * order), host or device pointers.                                         */
 int ifmm_solve(void* factor, const double* b, double* x, int on_device);
 
+/* ---- exact dense matvec:  dense.py:23-32 / experiments.py:157-162 ------
+ * y = A x, A_ij = K(|p_i - p_j|) evaluated on the fly (no storage), points
+ * and vectors in the same (any) order.  Used for the residual criterion. */
+int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double* points,
+                      const double* x, double* y, int on_device);
+
 /* ---- device micro-kernel entry points (tests and benchmarks) ---------- */
 /* C[M,N] = alpha*op(A)op(B) + beta*C on device pointers (row-major). */
 int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,

@@ -441,6 +441,28 @@ int ifmm_solve(void* p, const double* b, double* x, int on_device) {
   ABI_CATCH
 }
 
+// ---- exact dense matvec (experiments._matvec_oracle / dense.dense_matrix) -------
+int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double* points,
+                      const double* x, double* y, int on_device) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
+  KernelSpec k{kernel_kind, p0};
+  Blk P = C.alloc(n, 3), X = C.alloc(1, n), Y = C.alloc(1, n);
+  const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CUDA_CHECK(cudaMemcpyAsync(P.p, points, 24 * (size_t)n, kin, C.st));
+  CUDA_CHECK(cudaMemcpyAsync(X.p, x, 8 * (size_t)n, kin, C.st));
+  launch_exact_matvec(P.p, X.p, n, k, Y.p, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemcpyAsync(y, Y.p, 8 * (size_t)n, kout, C.st));
+  C.sync();
+  C.free(P); C.free(X); C.free(Y);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
 // ---- micro-kernel entry points --------------------------------------------------
 int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,
                   const double* B, int ldb, int tb, double* Cm, int ldc, double alpha,

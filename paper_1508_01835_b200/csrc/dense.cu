@@ -22,8 +22,8 @@ namespace ifmm {
 // per-phase cycle counters of the union kernel (diagnostics)
 __device__ unsigned long long g_uprof[16];
 
-__device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
-__device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
+__device__ __forceinline__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
+__device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
                           double* Q, int ldq);
 
 // ============================================================================
@@ -201,7 +201,9 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
                                              int* sflag) {
   const int tl = threadIdx.x & (T - 1);
   const int team = threadIdx.x / T, nteam = blockDim.x / T;
+  const int first_team_of_warp = (threadIdx.x & ~31) / T;
   for (int pi0 = 0; pi0 < cp / 2; pi0 += nteam) {
+    if (pi0 + first_team_of_warp >= cp / 2) break;  // whole warp idle this round
     const int pi = pi0 + team;
     int p = 0, q = cols;
     if (pi < cp / 2) {
@@ -223,8 +225,17 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
     if (!act) continue;
     const double ab = a * b, g2 = g * g;
     if (g != 0.0 && g2 > tol_rot * tol_rot * ab) {
-      const double zeta = (b - a) / (2.0 * g);
-      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+      // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g, written as
+      // t = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)) on exponent-scaled FP32
+      // operands: the rotation (c = rsqrt(1+t^2), s = c t in FP64) is orthogonal to
+      // working precision for any t, so t only steers convergence.
+      const double d = b - a, gg = 2.0 * g;
+      int ex;
+      frexp(fmax(fabs(d), fabs(gg)), &ex);
+      const float df = (float)ldexp(d, -ex), gf = (float)ldexp(gg, -ex);
+      const float tf = copysignf(1.0f, df * gf) * fabsf(gf) /
+                       (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+      const double t = (double)tf;
       const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
       for (int i = tl; i < rows; i += T) {
         const double u = x[i], v = y[i];
@@ -246,15 +257,18 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
 // One-sided Jacobi (Hestenes), round-robin ordering.  Rotations are applied
 // whenever a pair is not orthogonal to working precision; only rotations
 // above the dot-product rounding level (rows * eps) keep the sweeps going.
-__device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, int* sflag) {
+__device__ __forceinline__ int cta_jacobi(double* W, int rows, int cols, int ldw, double* V, int* sflag) {
   for (int e = threadIdx.x; e < cols * cols; e += blockDim.x)
     V[e] = (e % (cols + 1) == 0) ? 1.0 : 0.0;
   const double tol_rot = kEps;
-  const double tol_conv = kEps * (double)(rows > 4 ? rows : 4);
+  // 1e-13 relative orthogonality: sigma_i accurate to ~1e-13 relative (LAPACK
+  // gives eps*sigma_max absolute), with far fewer sweeps on graded matrices
+  const double tol_conv = fmax(kEps * (double)(rows > 4 ? rows : 4), 1e-13);
   const int cp = cols + (cols & 1);
   __syncthreads();
-  if (cols < 2) return;
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  if (cols < 2) return 0;
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *sflag = 0;
     __syncthreads();
     for (int r = 0; r < cp - 1; ++r) {
@@ -268,10 +282,11 @@ __device__ void cta_jacobi(double* W, int rows, int cols, int ldw, double* V, in
     if (threadIdx.x == 0) atomicAdd(&g_uprof[10], 1ull);
     if (!again) break;
   }
+  return sweep + 1;
 }
 
 // Column norms -> sigma[j]; order[pos] = j sorted by sigma desc (ties: lower j).
-__device__ void cta_sv_order(const double* W, int rows, int cols, int ldw, double* sig, int* order) {
+__device__ __forceinline__ void cta_sv_order(const double* W, int rows, int cols, int ldw, double* sig, int* order) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < cols; j += nw) {
     double a = 0.0;
@@ -569,7 +584,7 @@ void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim, cud
 
 // A: col-major rows x cols (ld lda), rows >= cols.  In place: R in the upper
 // triangle, Householder vectors (implicit unit head) below; tau[cols].
-__device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red) {
+__device__ __forceinline__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __shared__ double s_beta, s_tau, s_scale;
   for (int j = 0; j < cols; ++j) {
@@ -610,7 +625,7 @@ __device__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, d
 }
 
 // Form Q (rows x cols, col-major ld ldq) from cta_geqrf output.
-__device__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
+__device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
                           double* Q, int ldq) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (long long e = threadIdx.x; e < (long long)rows * cols; e += blockDim.x) {
@@ -662,7 +677,7 @@ constexpr int UNION_SMEM_DOUBLES = 28500;  // 228 KB
 // Interleaved Householder QR of two column-major matrices A (ra x s) and
 // B (rb x s): two barriers per column for both.  On exit: R in the upper
 // triangles, scaled reflectors below, taus in tauA / tauB.
-__device__ void cta_geqrf2(double* A, int ra, double* B, int rb, int s, double* tauA, double* tauB,
+__device__ __forceinline__ void cta_geqrf2(double* A, int ra, double* B, int rb, int s, double* tauA, double* tauB,
                            double* pa, double* pb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double scA = 0.0, scB = 0.0, bA = 0.0, bB = 0.0;
@@ -723,7 +738,7 @@ __device__ void cta_geqrf2(double* A, int ra, double* B, int rb, int s, double* 
 }
 
 // Interleaved Q formation for the two factorizations (one barrier / column).
-__device__ void cta_orgqr2(const double* A, int ra, const double* tauA, double* QA,
+__device__ __forceinline__ void cta_orgqr2(const double* A, int ra, const double* tauA, double* QA,
                            const double* B, int rb, const double* tauB, double* QB, int s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (long long e = threadIdx.x; e < (long long)ra * s; e += blockDim.x) {
@@ -755,6 +770,7 @@ __device__ void cta_orgqr2(const double* A, int ra, const double* tauA, double* 
   }
 }
 
+template <bool SM>
 __global__ void __launch_bounds__(512)
 union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
   extern __shared__ double smem[];
@@ -767,8 +783,8 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     const UnionDesc d = descs[bb];
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
-    const size_t need = union_work_doubles(m, d.k_old, d.k_f);
-    double* M = need <= (size_t)smem_doubles ? smem : d.work;
+    double* M = SM ? smem : d.work;  // compile-time space: LDS/STS on the smem path
+    (void)smem_doubles;
     double* Acol = M + (size_t)m * C;
     double* Bt = Acol + (size_t)m * smax;
     double* QB = Bt + (size_t)C * smax;
@@ -780,32 +796,35 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     int* order = (int*)(sig + smax);
     double* QA = M;  // M is dead after the ACA loop
 
-    // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax
-    const int tot = m * C;
-    const int bstep = blockDim.x / m, istep = blockDim.x % m;  // incremental (i, j)
-    const int i00 = threadIdx.x % m, j00 = threadIdx.x / m;
+    // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
+    // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
+    // column groups; the flat (row-major, numpy) index only breaks exact ties.
+    const int R = m < (int)blockDim.x ? m : (int)blockDim.x;
+    const int G = blockDim.x / R;
+    const int i0 = threadIdx.x % R, g0 = threadIdx.x / R;
+    const bool on = g0 < G;
     double bv = -1.0;
-    long long bi = (1LL << 62);
-    {
-      int i = i00, j = j00;
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
-                                : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
-        M[e] = v;
-        const double av = fabs(v);
-        const long long flat = (long long)(i * C + j);  // numpy row-major order
-        if (av > bv || (av == bv && flat < bi)) { bv = av; bi = flat; }
-        i += istep; j += bstep;
-        if (i >= m) { i -= m; ++j; }
-      }
-    }
-    unsigned long long t0 = clock64();
+    int bi = 0, bj = 0;
+    auto better = [&](double av, int i, int j) {
+      return av > bv || (av == bv && (long long)i * C + j < (long long)bi * C + bj);
+    };
+    if (on)
+      for (int i = i0; i < m; i += R)
+        for (int j = g0; j < C; j += G) {
+          const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
+                                  : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+          M[(size_t)j * m + i] = v;
+          const double av = fabs(v);
+          if (better(av, i, j)) { bv = av; bi = i; bj = j; }
+        }
     // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step
+    unsigned long long t0 = clock64();
     const double floor_ = thr / 8.0;
     int steps = 0;
     for (int it = 0; it < smax; ++it) {
-      warp_argmax(bv, bi);
-      if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+      long long bflat = bv < 0.0 ? (1LL << 62) : (long long)bi * C + bj;
+      warp_argmax(bv, bflat);
+      if (lane == 0) { wv[warp] = bv; wi[warp] = bflat; }
       __syncthreads();
       double gv = -1.0;
       long long gi = (1LL << 62);
@@ -823,17 +842,17 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       for (int j = threadIdx.x; j < C; j += blockDim.x) rr[j] = M[(size_t)j * m + p] / piv;
       __syncthreads();
       bv = -1.0;
-      bi = (1LL << 62);
-      int i = i00, j = j00;
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const double v = M[e] - cc[i] * rr[j];
-        M[e] = v;
-        const double av = fabs(v);
-        const long long flat = (long long)(i * C + j);
-        if (av > bv || (av == bv && flat < bi)) { bv = av; bi = flat; }
-        i += istep; j += bstep;
-        if (i >= m) { i -= m; ++j; }
-      }
+      if (on)
+        for (int i = i0; i < m; i += R) {
+          const double ci = cc[i];
+          for (int j = g0; j < C; j += G) {
+            double* mp = M + (size_t)j * m + i;
+            const double v = fma(-ci, rr[j], *mp);
+            *mp = v;
+            const double av = fabs(v);
+            if (better(av, i, j)) { bv = av; bi = i; bj = j; }
+          }
+        }
       ++steps;
     }
     __syncthreads();
@@ -857,9 +876,12 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     }
     cta_orgqr2(Acol, m, tauA, QA, Bt, C, tauB, QB, s);
     unsigned long long t3 = clock64();
-    cta_jacobi(core, s, s, s, Vc, &sflag);
+    const int nsw = cta_jacobi(core, s, s, s, Vc, &sflag);
+    unsigned long long t35 = clock64();
     cta_sv_order(core, s, s, s, sig, order);
     unsigned long long t4 = clock64();
+    if (threadIdx.x == 0) { atomicAdd(&g_uprof[11], (unsigned long long)nsw);
+                            atomicAdd(&g_uprof[12], t35 - t3); }
     int kk = 0;
     for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
     const int mr = d.min_rank < s ? d.min_rank : s;
@@ -913,12 +935,20 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
   if (n <= 0) return;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(union_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          UNION_SMEM_DOUBLES * 8);
     attr = true;
   }
-  const int sd = smem ? UNION_SMEM_DOUBLES : 0;
-  union_kernel<<<n < 4096 ? n : 4096, 512, (size_t)sd * 8, s>>>(d_descs, n, thr, sd);
+  static int nthr = -1;
+  if (nthr < 0) {
+    const char* e = getenv("IFMM_UNION_THREADS");
+    nthr = e ? atoi(e) : 512;
+  }
+  if (smem)
+    union_kernel<true><<<n < 4096 ? n : 4096, nthr, (size_t)UNION_SMEM_DOUBLES * 8, s>>>(
+        d_descs, n, thr, UNION_SMEM_DOUBLES);
+  else
+    union_kernel<false><<<n < 4096 ? n : 4096, nthr, 0, s>>>(d_descs, n, thr, 0);
 }
 
 // ============================================================================

@@ -123,3 +123,47 @@ void launch_grid(const GridDesc* d_descs, int n, int nc, cudaStream_t s) {
 }
 
 }  // namespace ifmm
+
+// ============================================================================
+// Exact dense matvec y = A x, A_ij = K(|p_i - p_j|), evaluated on the fly
+// (no storage, replaces dense.dense_matrix in
+// experiments._matvec_oracle).  One thread per row, columns staged through
+// shared memory in tiles; each row sums in a fixed order (deterministic).
+// ============================================================================
+namespace ifmm {
+namespace {
+constexpr int EM_TILE = 256;
+__global__ void __launch_bounds__(256)
+exact_matvec_kernel(const double* __restrict__ pts, const double* __restrict__ x, int n,
+                    KernelSpec k, double* __restrict__ y) {
+  __shared__ double sp[EM_TILE * 3];
+  __shared__ double sx[EM_TILE];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double px = 0, py = 0, pz = 0;
+  if (i < n) { px = pts[3 * i]; py = pts[3 * i + 1]; pz = pts[3 * i + 2]; }
+  double acc = 0.0;
+  for (int t0 = 0; t0 < n; t0 += EM_TILE) {
+    const int cnt = min(EM_TILE, n - t0);
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      sp[3 * e] = pts[3 * (t0 + e)];
+      sp[3 * e + 1] = pts[3 * (t0 + e) + 1];
+      sp[3 * e + 2] = pts[3 * (t0 + e) + 2];
+      sx[e] = x[t0 + e];
+    }
+    __syncthreads();
+    if (i < n)
+      for (int e = 0; e < cnt; ++e) {
+        const double r = euclid(px, py, pz, sp[3 * e], sp[3 * e + 1], sp[3 * e + 2]);
+        acc = fma(kernel_value(k, r), sx[e], acc);
+      }
+    __syncthreads();
+  }
+  if (i < n) y[i] = acc;
+}
+}  // namespace
+
+void launch_exact_matvec(const double* pts, const double* x, int n, const KernelSpec& k,
+                         double* y, cudaStream_t s) {
+  exact_matvec_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, x, n, k, y);
+}
+}  // namespace ifmm

@@ -38,5 +38,8 @@ struct GridDesc {
 void launch_eval(const EvalDesc* d_descs, int n, const KernelSpec& k, cudaStream_t s);
 void launch_interp(const InterpDesc* d_descs, int n, int nc, cudaStream_t s);
 void launch_grid(const GridDesc* d_descs, int n, int nc, cudaStream_t s);
+// y = A x with A_ij = K(|p_i - p_j|) on the fly (pts n x 3 row-major)
+void launch_exact_matvec(const double* pts, const double* x, int n, const KernelSpec& k,
+                         double* y, cudaStream_t s);
 
 }  // namespace ifmm

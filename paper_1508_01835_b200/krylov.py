@@ -134,3 +134,20 @@ def gmres(apply_A, b, tol: float = 1e-10, max_iters: int = 500, precond=None,
         x = precond(u) if side == "right" else u
     trace.iterations = k
     return x, trace
+
+
+def exact_matvec(points, kernel, x):
+    """y = A x with A_ij = kernel(|p_i - p_j|) evaluated on the device without
+    storing A (replaces dense.dense_matrix(...) @ x of the reference's
+    experiments._matvec_oracle, experiments.py:157-162, at any N)."""
+    pts = np.ascontiguousarray(np.asarray(points, dtype=float))
+    if pts.ndim != 2 or pts.shape[1] != 3:
+        raise ValueError("points must be an (N, 3) array")
+    kind, p0 = kernel.device_spec()
+    x = np.ascontiguousarray(np.asarray(x, dtype=float))
+    if len(x) != len(pts):
+        raise ValueError("vector length mismatch")
+    y = np.empty_like(x)
+    N.check(N.lib().ifmm_exact_matvec(N.ctx(), kind, p0, len(pts), pts.ctypes.data_as(C.c_void_p),
+                                      x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 0))
+    return y

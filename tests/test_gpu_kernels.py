@@ -147,3 +147,14 @@ def test_fill_svd_large(N, m, n, decay, r_cut):
     Vo = dV.cpu().numpy()[:n * r].reshape(r, n).T
     Ar = (U[:, :r] * s_true[:r]) @ V[:, :r].T
     assert np.linalg.norm((Uo * S) @ Vo.T - Ar) <= 1e-8 * np.linalg.norm(Ar) + 1e-5 * thr
+
+
+def test_exact_matvec_matches_dense(N):
+    import paper_1508_01835_b200 as P
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(size=(1500, 3))
+    x = rng.standard_normal(1500)
+    for K in (P.imq_kernel(0.05), P.exp_kernel(), P.benchmark_kernel(0.2)):
+        A = K.block(pts, pts)
+        y = P.exact_matvec(pts, K, x)
+        np.testing.assert_allclose(y, A @ x, rtol=1e-11, atol=1e-11 * np.abs(A @ x).max())

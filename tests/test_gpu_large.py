@@ -2,12 +2,14 @@
 run with reference semantics (tests/golden/large/, written by
 tests/golden/make_large_stats.py -- 53 min on one CPU core).
 
-Gates: H2 ranks (sum) and leaf-level fill statistics exact; x within 10 eps.
-Upper-level statistics are reported, not gated: the reference compresses
-fills with min(shape) > 64 by randomized SVD (factor.py:329-332), whose
-decisions for the many level-3/2 fills with sigma_1 near the threshold
-differ from an exact SVD (ours) -- both are valid compressions and x agrees
-within 10 eps."""
+Gates: tree, H2 ranks (sum), leaf-level fill statistics and peak edges
+exact; relative residual against the EXACT matvec within 2x the
+reference's (north star); x within the reference's own variability.
+
+Why not "x within 10 eps" at this size: the reference's x itself moves by
+9.4e-3 between factorize rng seeds 0 and 1 (rSVD sketches of fills with
+min(shape) > 64, factor.py:329-332), see tests/golden/large/c3_seed1_*.
+Upper-level fill statistics are reported, not gated, for the same reason."""
 
 import json
 import os
@@ -41,8 +43,16 @@ def test_c3_parity_against_reference_semantics():
             sum(lv[0].ranks)] == leaf[:5]
     assert fct.stats.peak_edges == st["peak_edges"]
     x = fct.solve(inp["b"])
+    b = inp["b"]
+    K = P.imq_kernel(inp["kernel"][1]["h"])
+    res = float(np.linalg.norm(P.exact_matvec(inp["points"], K, x) - b) / np.linalg.norm(b))
+    res_ref = float(np.linalg.norm(P.exact_matvec(inp["points"], K, x_ref) - b) / np.linalg.norm(b))
+    x_s1 = np.load(os.path.join(GOLDEN, "large", "c3_seed1_x.npy"))
+    var_ref = float(np.linalg.norm(x_s1 - x_ref) / np.linalg.norm(x_ref))
     rel = float(np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref))
-    print(f"c3 |x - x_ref|/|x_ref| = {rel:.3e}; levels ours "
+    print(f"c3 |x - x_ref|/|x_ref| = {rel:.3e} (reference seed0 vs seed1: {var_ref:.3e}); "
+          f"exact residual ours {res:.4e} ref {res_ref:.4e}; levels ours "
           f"{[(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in lv]} "
           f"ref {[tuple(v[:3]) + (v[4],) for v in st['levels']]}")
-    assert rel <= 10 * inp["eps"], rel
+    assert res <= 2.0 * res_ref, (res, res_ref)
+    assert rel <= 5.0 * var_ref, (rel, var_ref)
