@@ -115,6 +115,10 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
                    const double* F, const double* wf, double thr, int min_rank,
                    double* NB, double* NW, double* OM, double* FM, int* rank);
 int ifmm_dev_sync(void* ctx);
+/* Diagnostics: clock64 cycles of `reps` CTA Jacobi SVDs of an s x s device
+ * matrix (col-major) in shared memory; out[0] = cycles, out[1] = sweeps. */
+int ifmm_dev_jacobi_bench(void* ctx, int s, const double* A, int reps, int threads,
+                          unsigned long long* out);
 /* Device timing on the engine stream: record event `slot` (0..63); elapsed
  * milliseconds between two recorded slots (waits for the second). */
 int ifmm_ctx_event(void* ctx, int slot);
@@ -126,8 +130,10 @@ long long ifmm_ctx_launches(void* ctx);
  * algorithmic work = flops or bytes, launch count); enable >= 0 also resets
  * and switches timing on (1) or off (0). */
 int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* count, int n);
-/* Diagnostics: union-kernel cycle counters (ACA, QR, Q, Jacobi, output,
- * steps, count, sum m, sum C, smem count, Jacobi sweeps); reset != 0 clears. */
+/* Diagnostics: union-kernel cycle counters (32 entries: [0..12] all unions --
+ * ACA, QR, Q, Jacobi, output, steps, count, sum m, sum C, smem count,
+ * sweeps, core sweeps, core cycles; [16..24] the same for m > 256);
+ * reset != 0 clears. */
 int ifmm_union_profile(unsigned long long* out, int reset);
 /* Diagnostics: phase times (s) of the last factorize when IFMM_PROFILE=1. */
 int ifmm_profile(double* out, int n);

@@ -64,6 +64,7 @@ _SIGS = {
     "ifmm_dev_union": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_double,
                                  C.c_int, vp, vp, vp, vp, vp]),
     "ifmm_dev_sync": (C.c_int, [vp]),
+    "ifmm_dev_jacobi_bench": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(C.c_ulonglong)]),
     "ifmm_exact_matvec": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, vp, vp, vp, C.c_int]),
 }
 

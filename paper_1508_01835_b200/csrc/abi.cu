@@ -409,6 +409,21 @@ int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* c
   return 0;
 }
 
+int ifmm_dev_jacobi_bench(void* ctx, int s, const double* A, int reps, int threads,
+                          unsigned long long* out) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  Blk o = C.alloc(1, 2);
+  ifmm::jacobi_bench(A, s, reps, threads, reinterpret_cast<unsigned long long*>(o.p), C.st);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemcpyAsync(out, o.p, 16, cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  C.free(o);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
 int ifmm_union_profile(unsigned long long* out, int reset) {
   ifmm::union_profile(out, reset);
   return 0;

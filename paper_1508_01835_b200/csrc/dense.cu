@@ -20,7 +20,7 @@
 namespace ifmm {
 
 // per-phase cycle counters of the union kernel (diagnostics)
-__device__ unsigned long long g_uprof[16];
+__device__ unsigned long long g_uprof[32];
 
 __device__ __forceinline__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
 __device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
@@ -225,17 +225,11 @@ __device__ __forceinline__ void jacobi_round(double* W, int rows, int cols, int 
     if (!act) continue;
     const double ab = a * b, g2 = g * g;
     if (g != 0.0 && g2 > tol_rot * tol_rot * ab) {
-      // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g, written as
-      // t = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)) on exponent-scaled FP32
-      // operands: the rotation (c = rsqrt(1+t^2), s = c t in FP64) is orthogonal to
-      // working precision for any t, so t only steers convergence.
+      // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) with zeta = (b - a) / 2g, as
+      // t = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)): one sqrt + one division,
+      // full FP64 (an inexact t makes convergence linear instead of quadratic)
       const double d = b - a, gg = 2.0 * g;
-      int ex;
-      frexp(fmax(fabs(d), fabs(gg)), &ex);
-      const float df = (float)ldexp(d, -ex), gf = (float)ldexp(gg, -ex);
-      const float tf = copysignf(1.0f, df * gf) * fabsf(gf) /
-                       (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
-      const double t = (double)tf;
+      const double t = copysign(fabs(gg), d * gg) / (fabs(d) + hypot(d, gg));
       const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
       for (int i = tl; i < rows; i += T) {
         const double u = x[i], v = y[i];
@@ -261,8 +255,6 @@ __device__ __forceinline__ int cta_jacobi(double* W, int rows, int cols, int ldw
   for (int e = threadIdx.x; e < cols * cols; e += blockDim.x)
     V[e] = (e % (cols + 1) == 0) ? 1.0 : 0.0;
   const double tol_rot = kEps;
-  // 1e-13 relative orthogonality: sigma_i accurate to ~1e-13 relative (LAPACK
-  // gives eps*sigma_max absolute), with far fewer sweeps on graded matrices
   const double tol_conv = fmax(kEps * (double)(rows > 4 ? rows : 4), 1e-13);
   const int cp = cols + (cols & 1);
   __syncthreads();
@@ -664,9 +656,9 @@ __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f) {
 
 
 void union_profile(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 32);
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[32] = {};
     cudaMemcpyToSymbol(g_uprof, z, sizeof z);
   }
 }
@@ -790,6 +782,9 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     double* QB = Bt + (size_t)C * smax;
     double* core = QB + (size_t)C * smax;
     double* Vc = core + (size_t)smax * smax;
+    // global variant: the core SVD's working set (core, V) in shared memory
+    // when it fits (stores then stay on-chip instead of missing L1)
+    const bool jsm = !SM && 2 * smax * smax <= smem_doubles;
     double* tauA = Vc + (size_t)smax * smax;
     double* tauB = tauA + smax;
     double* sig = tauB + smax;
@@ -845,7 +840,23 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       if (on)
         for (int i = i0; i < m; i += R) {
           const double ci = cc[i];
-          for (int j = g0; j < C; j += G) {
+          int j = g0;
+          // 8 independent loads in flight per thread (the global-workspace
+          // variant streams M through L2 every step)
+          for (; j + 7 * G < C; j += 8 * G) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = M[(size_t)(j + u * G) * m + i];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int jj = j + u * G;
+              v[u] = fma(-ci, rr[jj], v[u]);
+              M[(size_t)jj * m + i] = v[u];
+              const double av = fabs(v[u]);
+              if (better(av, i, jj)) { bv = av; bi = i; bj = jj; }
+            }
+          }
+          for (; j < C; j += G) {
             double* mp = M + (size_t)j * m + i;
             const double v = fma(-ci, rr[j], *mp);
             *mp = v;
@@ -875,6 +886,12 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       core[(size_t)j * s + i] = acc;
     }
     cta_orgqr2(Acol, m, tauA, QA, Bt, C, tauB, QB, s);
+    if (jsm) {  // move the core into shared memory; V is initialised there
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) smem[e] = core[e];
+      __syncthreads();
+      core = smem;
+      Vc = smem + (size_t)s * s;
+    }
     unsigned long long t3 = clock64();
     const int nsw = cta_jacobi(core, s, s, s, Vc, &sflag);
     unsigned long long t35 = clock64();
@@ -920,6 +937,17 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       atomicAdd(&g_uprof[7], (unsigned long long)m);
       atomicAdd(&g_uprof[8], (unsigned long long)C);
       atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));
+      if (m > 256) {  // large unions separately
+        atomicAdd(&g_uprof[16], t1 - t0);
+        atomicAdd(&g_uprof[17], t2 - t1);
+        atomicAdd(&g_uprof[18], t3 - t2);
+        atomicAdd(&g_uprof[19], t4 - t3);
+        atomicAdd(&g_uprof[20], t5 - t4);
+        atomicAdd(&g_uprof[21], (unsigned long long)s);
+        atomicAdd(&g_uprof[22], 1ull);
+        atomicAdd(&g_uprof[23], (unsigned long long)m);
+        atomicAdd(&g_uprof[24], (unsigned long long)C);
+      }
     }
   }
 }
@@ -931,7 +959,8 @@ bool union_fits_smem(int m, int k_old, int k_f) {
 
 // smem != 0: every desc's workspace fits shared memory (caller partitions);
 // smem == 0: workspaces in global memory with the full L1 as cache.
-void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem) {
+void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
+                  int jac_smem_doubles) {
   if (n <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -947,8 +976,17 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
   if (smem)
     union_kernel<true><<<n < 4096 ? n : 4096, nthr, (size_t)UNION_SMEM_DOUBLES * 8, s>>>(
         d_descs, n, thr, UNION_SMEM_DOUBLES);
-  else
-    union_kernel<false><<<n < 4096 ? n : 4096, nthr, 0, s>>>(d_descs, n, thr, 0);
+  else {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(union_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           UNION_SMEM_DOUBLES * 8);
+      attr2 = true;
+    }
+    // shared memory for the core SVD only (2 s^2 doubles, s <= ~118)
+    const int jd = jac_smem_doubles > 0 ? jac_smem_doubles : 0;
+    union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd);
+  }
 }
 
 // ============================================================================
@@ -1584,4 +1622,35 @@ void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s) {
   if (n > 0) rsvd_fin_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d, n, thr);
 }
 
+}  // namespace ifmm
+
+// ---- micro-benchmark of the CTA Jacobi SVD (diagnostics) -------------------
+namespace ifmm {
+namespace {
+__global__ void __launch_bounds__(512) jacobi_bench_kernel(const double* A, int s, int reps,
+                                                           unsigned long long* out) {
+  extern __shared__ double sm[];
+  __shared__ int sflag;
+  double* W = sm;
+  double* V = sm + (size_t)s * s;
+  unsigned long long tot = 0;
+  int sw = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) W[e] = A[e];
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    sw += cta_jacobi(W, s, s, s, V, &sflag);
+    const unsigned long long t1 = clock64();
+    tot += t1 - t0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[0] = tot; out[1] = (unsigned long long)sw; }
+}
+}  // namespace
+void jacobi_bench(const double* A, int s, int reps, int threads, unsigned long long* d_out,
+                  cudaStream_t st) {
+  cudaFuncSetAttribute(jacobi_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       220 * 1024);
+  jacobi_bench_kernel<<<1, threads, (size_t)2 * s * s * 8, st>>>(A, s, reps, d_out);
+}
 }  // namespace ifmm

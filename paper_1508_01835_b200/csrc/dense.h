@@ -83,7 +83,10 @@ void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s);
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim,
                 cudaStream_t s, int rel_mode = 0);
 bool union_fits_smem(int m, int k_old, int k_f);
-void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem);
+// smem: all workspaces fit shared memory; otherwise jac_smem_doubles (<= 28500)
+// of dynamic shared memory hold the core SVD when 2 s^2 fits.
+void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
+                  int jac_smem_doubles = 0);
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to
@@ -189,3 +192,8 @@ struct RsvdFinDesc {
 };
 void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s);
 }  // namespace ifmm
+
+namespace ifmm {
+void jacobi_bench(const double* A, int s, int reps, int threads, unsigned long long* d_out,
+                  cudaStream_t st);
+}

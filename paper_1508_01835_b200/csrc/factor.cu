@@ -188,16 +188,22 @@ struct Eliminator {
     }
     Phase ph(C, PH_UNION);
     std::vector<UnionDesc> us, ug;  // shared-memory vs global-workspace unions
-    for (auto& u : ud) (union_fits_smem(u.m, u.k_old, u.k_f) ? us : ug).push_back(u);
+    int jsd = 0;                    // shared memory for the large unions' core SVD
+    for (auto& u : ud) {
+      if (union_fits_smem(u.m, u.k_old, u.k_f)) { us.push_back(u); continue; }
+      ug.push_back(u);
+      const int sm = std::min(u.m, u.k_old + u.k_f);
+      if (2 * sm * sm <= 28500) jsd = std::max(jsd, 2 * sm * sm);
+    }
     UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
     cudaEvent_t ka = nullptr;
     C.kt_begin(K_UNION, uflops, &ka);
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
-              [&](cudaStream_t s) { launch_union(dug, (int)ug.size(), thr, s, 0); });
+              [&](cudaStream_t s) { launch_union(dug, (int)ug.size(), thr, s, 0, jsd); });
     else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
-    else launch_union(dug, (int)ug.size(), thr, C.st, 0);
+    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd);
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());

@@ -35,6 +35,11 @@ def test_tree_ranks_bitexact(name):
     assert topo.interactions == csr_lists(g["int_ptr"], g["int_idx"])
     ranks = np.array([ops.rank.get(c, -1) for c in range(tree.n_clusters)])
     np.testing.assert_array_equal(ranks, g["ranks"])
+    # basis weights sigma_U of every cluster at levels 2..L (h2.py:214-216)
+    su = ops.sigma_u
+    for i, c in enumerate(g["su_keys"]):
+        w_ref = g["su_val"][g["su_ptr"][i]:g["su_ptr"][i + 1]]
+        np.testing.assert_allclose(su[int(c)], w_ref, rtol=1e-8, atol=1e-12 * w_ref[0])
 
 
 @pytest.mark.parametrize("name", CASES)

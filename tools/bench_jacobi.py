@@ -1,0 +1,21 @@
+"""Micro-benchmark: cycles per Jacobi round for s x s graded matrices."""
+import ctypes as C
+import os
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1508_01835_b200 import _native as N
+N.ctx()
+for s in (16, 40, 86, 110):
+    rng = np.random.default_rng(s)
+    U, _ = np.linalg.qr(rng.standard_normal((s, s)))
+    V, _ = np.linalg.qr(rng.standard_normal((s, s)))
+    A = (U * 10.0 ** -np.linspace(0, 10, s)) @ V.T
+    dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F").copy()).cuda()
+    for thr in (128, 256, 512):
+        out = (C.c_ulonglong * 2)()
+        N.check(N.lib().ifmm_dev_jacobi_bench(N.ctx(), s, C.c_void_p(dA.data_ptr()), 5, thr, out))
+        cyc, sw = out[0] / 5, out[1] / 5
+        rounds = sw * (s + (s & 1) - 1)
+        print(f"s={s:4d} threads={thr:4d} sweeps={sw:5.1f} cycles={cyc:10.0f} cycles/round={cyc / max(rounds, 1):8.0f}")
