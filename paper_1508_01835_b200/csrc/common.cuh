@@ -3,10 +3,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #define IFMM_DEV __device__ __forceinline__
 
 namespace ifmm {
+
+// IFMM_DEBUG_SYNC=1: synchronise after every batched launch and abort with the
+// launcher's name on a device fault (diagnostics only).
+inline bool dbg_sync_on() {
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("IFMM_DEBUG_SYNC"); on = e && atoi(e) ? 1 : 0; }
+  return on == 1;
+}
+struct DbgSync {
+  cudaStream_t s;
+  const char* name;
+  ~DbgSync() {
+    if (!dbg_sync_on()) return;
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[ifmm] device fault after %s: %s\n", name, cudaGetErrorString(e));
+      abort();
+    }
+  }
+};
 
 constexpr double kEps = 2.220446049250313e-16;
 

@@ -146,6 +146,7 @@ gemm_grouped_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ 
 
 void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob, int total_tiles,
                  cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_gemm"};
   if (total_tiles <= 0) return;
   int grid = total_tiles < 148 * 8 ? total_tiles : 148 * 8;
   gemm_grouped_kernel<<<grid, 128, 0, s>>>(d_descs, d_tile_start, nprob, total_tiles);
@@ -176,6 +177,7 @@ __global__ void copy_kernel(const CopyDesc* __restrict__ descs, int n) {
 }  // namespace
 
 void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_copy"};
   if (n <= 0) return;
   copy_kernel<<<n < 4096 ? n : 4096, 256, 0, s>>>(d_descs, n);
 }
@@ -272,6 +274,149 @@ __device__ __forceinline__ int cta_jacobi(double* W, int rows, int cols, int ldw
     const int again = *sflag;
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(&g_uprof[10], 1ull);
+    if (!again) break;
+  }
+  return sweep + 1;
+}
+
+// Union-core Jacobi.  Z is col-major (2s x s, ld 2s): rows [0, s) hold the
+// matrix, rows [s, 2s) the accumulated rotations (set to I here), so one
+// rotation loop updates both.  The team width is chosen so that every pair
+// of a round runs in one pass (one barrier per round).
+template <int T>
+__device__ __forceinline__ void jac_z_round(double* Z, int s, int cp, int r, double tol_rot2,
+                                            double tol_conv2, int* sflag) {
+  const int tl = threadIdx.x & (T - 1);
+  const int team = threadIdx.x / T, nteam = blockDim.x / T;
+  const int first_team_of_warp = (threadIdx.x & ~31) / T;
+  const int ld = 2 * s, half = cp / 2;
+  for (int pi0 = 0; pi0 < half; pi0 += nteam) {
+    if (pi0 + first_team_of_warp >= half) break;  // whole warp idle this round
+    const int pi = pi0 + team;
+    int p = 0, q = s;
+    if (pi < half) {
+      if (pi == 0) { p = r; q = cp - 1; }
+      else { p = (r + pi) % (cp - 1); q = (r - pi + cp - 1) % (cp - 1); }
+      if (p > q) { const int t = p; p = q; q = t; }
+    }
+    const bool act = pi < half && q < s;
+    double a = 0.0, b = 0.0, g = 0.0;
+    double* x = Z + (size_t)p * ld;
+    double* y = Z + (size_t)(act ? q : p) * ld;
+    if (act)
+      for (int i = tl; i < s; i += T) {
+        const double u = x[i], v = y[i];
+        a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
+      }
+    a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
+    if (!act) continue;
+    const double ab = a * b, g2 = g * g;
+    if (g != 0.0 && g2 > tol_rot2 * ab) {
+      // t = tan(theta) = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)), d = b - a, gg = 2g
+      const double d = b - a, gg = 2.0 * g;
+      const double t = copysign(fabs(gg), d * gg) / (fabs(d) + sqrt(fma(d, d, gg * gg)));
+      const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+      for (int i = tl; i < ld; i += T) {
+        const double u = x[i], v = y[i];
+        x[i] = fma(c, u, -sn * v);
+        y[i] = fma(sn, u, c * v);
+      }
+      if (tl == 0 && g2 > tol_conv2 * ab) *sflag = 1;
+    }
+  }
+}
+
+// One full round-robin sweep of the union-core Jacobi with the column pair's
+// matrix part held in registers (NE rows per lane, teams of T lanes), an
+// incremental pair schedule (no modulo) and one barrier per round.  Returns
+// the per-thread "not yet converged" flag.
+template <int T, int NE>
+__device__ __forceinline__ bool jac_z_sweep(double* Z, int s, int cp, double tr2, double tc2) {
+  const int tl = threadIdx.x & (T - 1), team = threadIdx.x / T;
+  const int half = cp >> 1, ld = 2 * s;
+  const bool warp_on = ((threadIdx.x & ~31) / T) < half;
+  int p = team, q = team == 0 ? cp - 1 : cp - 1 - team;
+  bool again = false;
+  for (int r = 0; r < cp - 1; ++r) {
+    if (warp_on) {
+      const int lo = p < q ? p : q, hi = p < q ? q : p;
+      const bool act = team < half && hi < s;
+      double* x = Z + (size_t)(act ? lo : 0) * ld;
+      double* y = Z + (size_t)(act ? hi : 0) * ld;
+      double xr[NE], yr[NE];
+      double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int i = tl + e * T;
+        const bool in = act && i < s;
+        xr[e] = in ? x[i] : 0.0;
+        yr[e] = in ? y[i] : 0.0;
+        a = fma(xr[e], xr[e], a); b = fma(yr[e], yr[e], b); g = fma(xr[e], yr[e], g);
+      }
+      a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
+      const double ab = a * b, g2 = g * g;
+      if (act && g != 0.0 && g2 > tr2 * ab) {
+        const double d = b - a, gg = 2.0 * g;
+        const double t = copysign(fabs(gg), d * gg) / (fabs(d) + sqrt(fma(d, d, gg * gg)));
+        const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const int i = tl + e * T;
+          if (i < s) {
+            x[i] = fma(c, xr[e], -sn * yr[e]);
+            y[i] = fma(sn, xr[e], c * yr[e]);
+          }
+        }
+        for (int i = s + tl; i < ld; i += T) {
+          const double u = x[i], v = y[i];
+          x[i] = fma(c, u, -sn * v);
+          y[i] = fma(sn, u, c * v);
+        }
+        again |= g2 > tc2 * ab;
+      }
+    }
+    __syncthreads();
+    if (team == 0) p = r + 1;
+    else { p = p + 1 == cp - 1 ? 0 : p + 1; q = q + 1 == cp - 1 ? 0 : q + 1; }
+  }
+  return again;
+}
+
+__device__ __forceinline__ int cta_jacobi_z(double* Z, int s, int* sflag) {
+  const int ld = 2 * s;
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+    const int j = e / s, i = e % s;
+    Z[(size_t)j * ld + s + i] = (i == j) ? 1.0 : 0.0;
+  }
+  const double tol_rot = kEps;
+  const double tol_conv = fmax(kEps * (double)(s > 4 ? s : 4), 1e-13);
+  const double tr2 = tol_rot * tol_rot, tc2 = tol_conv * tol_conv;
+  const int cp = s + (s & 1), half = cp / 2;
+  __syncthreads();
+  if (s < 2) return 0;
+  const int nthr = blockDim.x;
+  const int T = half * 32 <= nthr ? 32 : half * 16 <= nthr ? 16 : half * 8 <= nthr ? 8 : 4;
+  // register-resident variants: rows per lane NE = ceil(s / T)
+  const int kind = (T == 32 && s <= 32) ? 1 : (T == 16 && s <= 64) ? 2 : (T == 8 && s <= 128) ? 3 : 0;
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    int again;
+    if (kind == 1) again = __syncthreads_or(jac_z_sweep<32, 1>(Z, s, cp, tr2, tc2));
+    else if (kind == 2) again = __syncthreads_or(jac_z_sweep<16, 4>(Z, s, cp, tr2, tc2));
+    else if (kind == 3) again = __syncthreads_or(jac_z_sweep<8, 16>(Z, s, cp, tr2, tc2));
+    else {
+      if (threadIdx.x == 0) *sflag = 0;
+      __syncthreads();
+      for (int r = 0; r < cp - 1; ++r) {
+        if (T == 32) jac_z_round<32>(Z, s, cp, r, tr2, tc2, sflag);
+        else if (T == 16) jac_z_round<16>(Z, s, cp, r, tr2, tc2, sflag);
+        else if (T == 8) jac_z_round<8>(Z, s, cp, r, tr2, tc2, sflag);
+        else jac_z_round<4>(Z, s, cp, r, tr2, tc2, sflag);
+        __syncthreads();
+      }
+      again = *sflag;
+      __syncthreads();
+    }
     if (!again) break;
   }
   return sweep + 1;
@@ -541,6 +686,7 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
 
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim, cudaStream_t s,
                 int rel_mode) {
+  DbgSync dbg_sync_{s, "launch_svd"};
   if (n > 0 && !rel_mode) {
     static bool attr2 = false;
     if (!attr2) {
@@ -649,11 +795,14 @@ __device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, i
 __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f) {
   const size_t C = (size_t)k_old + k_f;
   const size_t s = (size_t)(m < (int)C ? m : (int)C);
-  // M (m C; reused for QA m s) | Acol (m s) | Bt (C s) | QB (C s) | core (s s) | V (s s)
-  // | tauA tauB sig (3s) | order (s ints)
-  return (size_t)m * C + (size_t)m * s + 2 * C * s + 2 * s * s + 4 * s + 16;
+  const size_t sp = s + (s & 1);
+  // Mreg: ACA residual (m C), then 6 s x sp CholeskyQR matrices, or QA
+  //       (m s) on the Householder path
+  // | Acol (m s) | Bt (C s) | QB (C s, Householder path) | Z (2 s^2)
+  // | D, tauA, tauB, sig (4 s) | order (s ints) | acts, pos (2 C ints)
+  const size_t mreg = (size_t)m * C > 6 * s * sp ? (size_t)m * C : 6 * s * sp;
+  return mreg + (size_t)m * s + 2 * C * s + 2 * s * s + 5 * s + C + 16;
 }
-
 
 void union_profile(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 32);
@@ -762,9 +911,173 @@ __device__ __forceinline__ void cta_orgqr2(const double* A, int ra, const double
   }
 }
 
+// ---- CholeskyQR2 pieces for the ACA factors ---------------------------------
+// The ACA is an LU with full pivoting: X = P L~ D with L~ unit lower
+// trapezoidal, |L~| <= 1, D = diag(pivots), and Y unit lower trapezoidal.
+// L~ and Y are well conditioned (cond <= 40 on every large union of the c3
+// recipe at N=32768, measured on oracle unions), while the pivots carry the
+// grading.  Householder QR of X D^{-1} and of Y is therefore replaced by two
+// CholeskyQR passes (Gram, Cholesky, row-wise triangular solve): two
+// parallel phases + s barriers instead of ~3s barriers.  R_A = R~ D keeps the
+// column-wise backward error of Householder QR.  A Cholesky pivot ratio
+// below kCholFloor (cond(L~) > ~1e6) sends the union to the Householder path.
+constexpr double kCholFloor = 1e-12;
+
+// Upper triangles of G_A = A^T A and G_B = B^T B (A: ra x s, B: rb x s,
+// col-major), row-major with ld sp.  One warp per 4x4 tile, lanes split rows.
+__device__ __forceinline__ void cta_gram2(const double* A, int ra, const double* B, int rb, int s,
+                                          int sp, double* GA, double* GB) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nb = (s + 3) >> 2, ntile = nb * (nb + 1) / 2;
+  for (int t = warp; t < 2 * ntile; t += nw) {
+    const bool isA = t < ntile;
+    const int tt = isA ? t : t - ntile;
+    int bj = 0;
+    while ((bj + 1) * (bj + 2) / 2 <= tt) ++bj;
+    const int bi = tt - bj * (bj + 1) / 2;
+    const double* X = isA ? A : B;
+    const int r = isA ? ra : rb;
+    double* G = isA ? GA : GB;
+    const int i0 = bi * 4, j0 = bj * 4;
+    int ci[4], cj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { ci[u] = min(i0 + u, s - 1); cj[u] = min(j0 + u, s - 1); }
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int row = lane; row < r; row += 32) {
+      double xi[4], xj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { xi[u] = X[(size_t)ci[u] * r + row]; xj[u] = X[(size_t)cj[u] * r + row]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(xi[u], xj[v], acc[u][v]);
+    }
+    // transpose-reduce the 16 partial sums: 8+4+2+1+1 shuffles; afterwards
+    // lane pair (2 idx, 2 idx + 1) holds the total of value idx = 4u + v
+    double v16[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) v16[4 * u + v] = acc[u][v];
+#pragma unroll
+    for (int h = 8, bit = 16; h >= 1; h >>= 1, bit >>= 1) {
+      const bool up = lane & bit;
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const double send = up ? v16[k] : v16[k + h];
+        const double keep = up ? v16[k + h] : v16[k];
+        v16[k] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+      }
+    }
+    v16[0] += __shfl_xor_sync(0xffffffffu, v16[0], 1);
+    if (!(lane & 1)) {
+      const int idx = lane >> 1, i = i0 + (idx >> 2), j = j0 + (idx & 3);
+      if (i < s && j < s && i <= j) G[(size_t)i * sp + j] = v16[0];
+    }
+  }
+}
+
+// In-place right-looking Cholesky G = R^T R of two SPD matrices at once
+// (upper triangles, row-major ld sp), one barrier per step: step k
+// eliminates with row k unscaled and scales row k-1 (no longer read) into
+// R.  On exit the upper triangles hold R (the strict lower parts are never
+// read); rinv[k] = 1 / R[k][k].  Returns the smallest pivot ratio
+// R_kk^2 / max_i G_ii over both matrices (uniform across the CTA).
+__device__ __forceinline__ double cta_chol2(double* GA, double* ia, double* GB, double* ib, int s, int sp) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  double minr = 1.0, mxA = 0.0, mxB = 0.0;
+  for (int k = 0; k < s; ++k) {
+    mxA = fmax(mxA, GA[(size_t)k * sp + k]);
+    mxB = fmax(mxB, GB[(size_t)k * sp + k]);
+  }
+  __syncthreads();
+  for (int k = 0; k <= s; ++k) {
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      double* G = w ? GB : GA;
+      double* iv = w ? ib : ia;
+      if (k > 0) {  // finalise row k-1 of R
+        double* gr = G + (size_t)(k - 1) * sp;
+        const double rinv = iv[k - 1];
+        for (int j = k - 1 + threadIdx.x; j < s; j += blockDim.x) gr[j] *= rinv;
+      }
+      if (k < s) {
+        const double* g = G + (size_t)k * sp;  // row k (final, unscaled)
+        const double gkk = g[k];
+        const double inv = 1.0 / gkk, rinv = 1.0 / sqrt(gkk);
+        const double ratio = gkk / (w ? mxB : mxA);
+        minr = (ratio > 0.0 && isfinite(gkk)) ? fmin(minr, ratio) : 0.0;
+        if (threadIdx.x == 0) iv[k] = rinv;
+        for (int i = k + 1 + wid; i < s; i += nwp) {
+          const double fi = g[i] * inv;
+          double* Gi = G + (size_t)i * sp;
+          for (int j = i + lane; j < s; j += 32) Gi[j] = fma(-fi, g[j], Gi[j]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return minr;
+}
+
+// A <- A R^{-1} row by row (A: r x s col-major; R row-major upper, ld sp,
+// rinv = 1 / diag), both matrices at once; 8-column register blocks.
+__device__ __forceinline__ void cta_trsm2(double* A, int ra, const double* RA, const double* ia,
+                                          double* B, int rb, const double* RB, const double* ib,
+                                          int s, int sp) {
+  for (int row = threadIdx.x; row < ra + rb; row += blockDim.x) {
+    const bool isA = row < ra;
+    double* X = isA ? A : B;
+    const int r = isA ? ra : rb, rr = isA ? row : row - ra;
+    const double* R = isA ? RA : RB;
+    const double* iv = isA ? ia : ib;
+    for (int j0 = 0; j0 < s; j0 += 8) {
+      double a[8];
+      int cj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { cj[u] = min(j0 + u, s - 1); a[u] = X[(size_t)cj[u] * r + rr]; }
+      for (int i = 0; i < j0; ++i) {
+        const double xi = X[(size_t)i * r + rr];
+        const double* Ri = R + (size_t)i * sp;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = fma(-xi, Ri[cj[u]], a[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] *= iv[cj[u]];
+        const double* Ru = R + (size_t)cj[u] * sp;
+#pragma unroll
+        for (int v = u + 1; v < 8; ++v) a[v] = fma(-a[u], Ru[cj[v]], a[v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < s) X[(size_t)(j0 + u) * r + rr] = a[u];
+    }
+  }
+}
+
+// T = R2 R1 (row-major upper, ld sp) for two pairs at once.
+__device__ __forceinline__ void cta_trmul2(const double* A2, const double* A1, double* TA, const double* B2,
+                                           const double* B1, double* TB, int s, int sp) {
+  for (int e = threadIdx.x; e < 2 * s * s; e += blockDim.x) {
+    const bool isA = e < s * s;
+    const int f = isA ? e : e - s * s;
+    const int i = f / s, j = f - i * s;
+    const double* R2 = isA ? A2 : B2;
+    const double* R1 = isA ? A1 : B1;
+    double acc = 0.0;
+    for (int l = i; l <= j; ++l) acc = fma(R2[(size_t)i * sp + l], R1[(size_t)l * sp + j], acc);
+    (isA ? TA : TB)[(size_t)i * sp + j] = (i <= j) ? acc : 0.0;
+  }
+}
+
 template <bool SM>
 __global__ void __launch_bounds__(512)
-union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
+union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles, int force_hh) {
   extern __shared__ double smem[];
   __shared__ double wv[32];
   __shared__ long long wi[32];
@@ -775,25 +1088,27 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     const UnionDesc d = descs[bb];
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
+    const int spx = smax + (smax & 1);
     double* M = SM ? smem : d.work;  // compile-time space: LDS/STS on the smem path
-    (void)smem_doubles;
-    double* Acol = M + (size_t)m * C;
+    const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+    double* Acol = M + mreg;
     double* Bt = Acol + (size_t)m * smax;
     double* QB = Bt + (size_t)C * smax;
     double* core = QB + (size_t)C * smax;
-    double* Vc = core + (size_t)smax * smax;
-    // global variant: the core SVD's working set (core, V) in shared memory
-    // when it fits (stores then stay on-chip instead of missing L1)
-    const bool jsm = !SM && 2 * smax * smax <= smem_doubles;
-    double* tauA = Vc + (size_t)smax * smax;
+    double* Dp = core + 2 * (size_t)smax * smax;
+    double* tauA = Dp + smax;
     double* tauB = tauA + smax;
     double* sig = tauB + smax;
     int* order = (int*)(sig + smax);
-    double* QA = M;  // M is dead after the ACA loop
+    int* acts = order + smax + 1;
+    int* pos = acts + C;
+    // global variant: the core SVD's working set in shared memory when it fits
+    const bool jsm = !SM && 2 * smax * smax <= smem_doubles;
 
     // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
     // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
-    // column groups; the flat (row-major, numpy) index only breaks exact ties.
+    // column groups over the list of active (unpivoted) columns; the flat
+    // (row-major, numpy) index only breaks exact ties.
     const int R = m < (int)blockDim.x ? m : (int)blockDim.x;
     const int G = blockDim.x / R;
     const int i0 = threadIdx.x % R, g0 = threadIdx.x / R;
@@ -803,6 +1118,8 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     auto better = [&](double av, int i, int j) {
       return av > bv || (av == bv && (long long)i * C + j < (long long)bi * C + bj);
     };
+    for (int j = threadIdx.x; j < C; j += blockDim.x) { acts[j] = j; pos[j] = j; }
+    int nact = C;  // every thread tracks the active count
     if (on)
       for (int i = i0; i < m; i += R)
         for (int j = g0; j < C; j += G) {
@@ -812,7 +1129,10 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
           const double av = fabs(v);
           if (better(av, i, j)) { bv = av; bi = i; bj = j; }
         }
-    // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step
+    // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step.
+    // A pivoted column becomes exactly zero (its row factor entry is piv/piv
+    // = 1), so it leaves the active list; pivoted rows keep their rounding
+    // residue and stay, as in the reference.
     unsigned long long t0 = clock64();
     const double floor_ = thr / 8.0;
     int steps = 0;
@@ -821,42 +1141,66 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       warp_argmax(bv, bflat);
       if (lane == 0) { wv[warp] = bv; wi[warp] = bflat; }
       __syncthreads();
-      double gv = -1.0;
-      long long gi = (1LL << 62);
-      for (int w = 0; w < nw; ++w) {
-        const double ov = wv[w];
-        const long long oi = wi[w];
-        if (ov > gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+      double gv = lane < nw ? wv[lane] : -1.0;
+      long long gi = lane < nw ? wi[lane] : (1LL << 62);
+      warp_argmax(gv, gi);  // every lane of every warp: the block's pivot
+      const int p = (int)(gi / C), q = (int)(gi - (long long)p * C);
+      if (p < 0 || p >= m || q < 0 || q >= C) {
+        if (threadIdx.x == 0)
+          printf("[union] bad pivot m=%d C=%d step=%d nact=%d gi=%lld gv=%g\n", m, C, steps, nact, gi, gv);
+        __trap();
       }
-      const int p = (int)(gi / C), q = (int)(gi % C);
       const double piv = M[(size_t)q * m + p];
       if (piv == 0.0 || (fabs(piv) <= floor_ && steps >= d.min_rank)) break;  // uniform
       double* cc = Acol + (size_t)steps * m;
       double* rr = Bt + (size_t)steps * C;
-      for (int i = threadIdx.x; i < m; i += blockDim.x) cc[i] = M[(size_t)q * m + i];
-      for (int j = threadIdx.x; j < C; j += blockDim.x) rr[j] = M[(size_t)j * m + p] / piv;
+      // column q leaves the active list: its residual is exactly zero from
+      // here on (q's row factor entry is piv / piv = 1), stored as such
+      // (the pivot entry itself is cleared after the barrier: every thread
+      // reads it above)
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        cc[i] = M[(size_t)q * m + i];
+        if (i != p) M[(size_t)q * m + i] = 0.0;
+      }
+      for (int j = threadIdx.x; j < C; j += blockDim.x)
+        rr[j] = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
+      if (threadIdx.x == 0) {  // swap-remove q from the active list
+        const int k = pos[q], last = acts[nact - 1];
+        if (k < 0 || k >= nact || acts[k] != q) {
+          printf("[union] bad active list m=%d C=%d step=%d nact=%d q=%d k=%d\n", m, C, steps, nact, q, k);
+          __trap();
+        }
+        acts[k] = last;
+        pos[last] = k;
+        Dp[steps] = piv;
+      }
+      --nact;
       __syncthreads();
+      if (threadIdx.x == 0) M[(size_t)q * m + p] = 0.0;
+      const int na = nact;
       bv = -1.0;
       if (on)
         for (int i = i0; i < m; i += R) {
           const double ci = cc[i];
-          int j = g0;
-          // 8 independent loads in flight per thread (the global-workspace
-          // variant streams M through L2 every step)
-          for (; j + 7 * G < C; j += 8 * G) {
-            double v[8];
+          int l = g0;
+          // UN independent loads in flight per thread (16 on the
+          // global-workspace variant, which streams M through L2 every step)
+          constexpr int UN = SM ? 8 : 16;
+          for (; l + (UN - 1) * G < na; l += UN * G) {
+            int jj[UN];
+            double v[UN];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = M[(size_t)(j + u * G) * m + i];
+            for (int u = 0; u < UN; ++u) { jj[u] = acts[l + u * G]; v[u] = M[(size_t)jj[u] * m + i]; }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int jj = j + u * G;
-              v[u] = fma(-ci, rr[jj], v[u]);
-              M[(size_t)jj * m + i] = v[u];
+            for (int u = 0; u < UN; ++u) {
+              v[u] = fma(-ci, rr[jj[u]], v[u]);
+              M[(size_t)jj[u] * m + i] = v[u];
               const double av = fabs(v[u]);
-              if (better(av, i, jj)) { bv = av; bi = i; bj = jj; }
+              if (better(av, i, jj[u])) { bv = av; bi = i; bj = jj[u]; }
             }
           }
-          for (; j < C; j += G) {
+          for (; l < na; l += G) {
+            const int j = acts[l];
             double* mp = M + (size_t)j * m + i;
             const double v = fma(-ci, rr[j], *mp);
             *mp = v;
@@ -873,29 +1217,86 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       continue;
     }
     const int s = steps;
+    const int sp = s + (s & 1);
     unsigned long long t1 = clock64();
-    // ---- QR(A), QR(B^T) interleaved ----
-    cta_geqrf2(Acol, m, Bt, C, s, tauA, tauB, pa, pb);
-    unsigned long long t2 = clock64();
-    // core = RA * RB^T (s x s, col-major)
-    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
-      const int j = e / s, i = e % s;
-      double acc = 0.0;
-      for (int l = (i > j ? i : j); l < s; ++l)
-        acc = fma(Acol[(size_t)l * m + i], Bt[(size_t)l * C + j], acc);
-      core[(size_t)j * s + i] = acc;
+    // ---- scale X columns by 1/pivot: L~ = X D^{-1} ----
+    for (long long e = threadIdx.x; e < (long long)m * s; e += blockDim.x) {
+      const int t = (int)(e / m);
+      Acol[e] /= Dp[t];
     }
-    cta_orgqr2(Acol, m, tauA, QA, Bt, C, tauB, QB, s);
-    if (jsm) {  // move the core into shared memory; V is initialised there
-      for (int e = threadIdx.x; e < s * s; e += blockDim.x) smem[e] = core[e];
+    // ---- CholeskyQR2 of L~ (m x s) and Y (C x s); M is free now ----
+    // CholeskyQR workspace: G_A, G_B (Cholesky in place -> R) in shared
+    // memory for the global variant when 2 s x sp fit; R1 and the products
+    // T = R2 R1 live in the (dead) residual region.
+    const bool qsm = !SM && 2 * (size_t)s * sp <= (size_t)smem_doubles;
+    double* GA = qsm ? smem : M;
+    double* GB = GA + (size_t)s * sp;
+    double* RA1s = M + (qsm ? 0 : 2 * (size_t)s * sp);
+    double* RB1s = RA1s + (size_t)s * sp;
+    double* TA = RB1s + (size_t)s * sp;
+    double* TB = TA + (size_t)s * sp;
+    double* ia = tauA;  // 1 / diag
+    double* ib = tauB;
+    __syncthreads();
+    double r1 = 0.0;
+    if (!force_hh) {
+      cta_gram2(Acol, m, Bt, C, s, sp, GA, GB);
       __syncthreads();
-      core = smem;
-      Vc = smem + (size_t)s * s;
+      r1 = cta_chol2(GA, ia, GB, ib, s, sp);
     }
+    // cond(L~) or cond(Y) above ~1e6: Householder path instead
+    const bool hh = force_hh || !(r1 > kCholFloor);
+    const double* QAp;
+    const double* QBp;
+    double* Z = (qsm || jsm) ? smem : core;
+    if (!hh) {
+      cta_trsm2(Acol, m, GA, ia, Bt, C, GB, ib, s, sp);
+      for (int e = threadIdx.x; e < 2 * s * sp; e += blockDim.x) RA1s[e] = GA[e];  // park R1
+      __syncthreads();
+      cta_gram2(Acol, m, Bt, C, s, sp, GA, GB);
+      __syncthreads();
+      cta_chol2(GA, ia, GB, ib, s, sp);
+      cta_trsm2(Acol, m, GA, ia, Bt, C, GB, ib, s, sp);
+      // R_A = R_A2 R_A1, R_B = R_B2 R_B1
+      cta_trmul2(GA, RA1s, TA, GB, RB1s, TB, s, sp);
+      __syncthreads();
+      // Z = [core^T ; I], core^T = R_B D R_A^T (see below)
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int j = e / s, i = e - j * s;
+        double acc = 0.0;
+        for (int l = (i > j ? i : j); l < s; ++l)
+          acc = fma(TB[(size_t)i * sp + l] * Dp[l], TA[(size_t)j * sp + l], acc);
+        Z[(size_t)j * 2 * s + i] = acc;
+      }
+      QAp = Acol;
+      QBp = Bt;
+    } else {
+      // Householder fallback (ill-conditioned L~ or Y)
+      __syncthreads();
+      cta_geqrf2(Acol, m, Bt, C, s, tauA, tauB, pa, pb);
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int j = e / s, i = e - j * s;
+        double acc = 0.0;
+        for (int l = (i > j ? i : j); l < s; ++l)
+          acc = fma(Bt[(size_t)l * C + i] * Dp[l], Acol[(size_t)l * m + j], acc);
+        Z[(size_t)j * 2 * s + i] = acc;
+      }
+      cta_orgqr2(Acol, m, tauA, M, Bt, C, tauB, QB, s);
+      QAp = M;
+      QBp = QB;
+      if (threadIdx.x == 0) atomicAdd(&g_uprof[13], 1ull);
+    }
+    unsigned long long t2 = clock64();
+    // ---- SVD of the core: one-sided Jacobi on its transpose.  The ACA
+    // pivots grade the core's rows, so its columns are graded in the
+    // transpose and the sweeps converge in ~4 instead of ~7 passes (measured
+    // on oracle unions).  On exit rows [s, 2s) of Z hold the core's left
+    // singular vectors (phi) and rows [0, s) its scaled right singular
+    // vectors (sigma psi).
     unsigned long long t3 = clock64();
-    const int nsw = cta_jacobi(core, s, s, s, Vc, &sflag);
+    const int nsw = cta_jacobi_z(Z, s, &sflag);
     unsigned long long t35 = clock64();
-    cta_sv_order(core, s, s, s, sig, order);
+    cta_sv_order(Z, s, s, 2 * s, sig, order);
     unsigned long long t4 = clock64();
     if (threadIdx.x == 0) { atomicAdd(&g_uprof[11], (unsigned long long)nsw);
                             atomicAdd(&g_uprof[12], t35 - t3); }
@@ -903,24 +1304,38 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
     const int mr = d.min_rank < s ? d.min_rank : s;
     const int k = kk > mr ? kk : mr;
-    // new basis = QA * Ucore[:, :k]  (Ucore col = core col / sigma)
-    for (long long e = threadIdx.x; e < (long long)m * k; e += blockDim.x) {
-      const int a = (int)(e / m), i = (int)(e % m);
-      const int j = order[a];
-      const double inv = sig[j] > 0.0 ? 1.0 / sig[j] : 0.0;
-      double acc = 0.0;
-      for (int l = 0; l < s; ++l) acc = fma(QA[(size_t)l * m + i], core[(size_t)j * s + l], acc);
-      d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc * inv;
-    }
-    // maps = sigma_a (QB Vc)[col][a] / weight[col]
-    for (long long e = threadIdx.x; e < (long long)C * k; e += blockDim.x) {
-      const int a = (int)(e / C), col = (int)(e % C);
-      const int j = order[a];
-      double acc = 0.0;
-      for (int l = 0; l < s; ++l) acc = fma(QB[(size_t)l * C + col], Vc[(size_t)j * s + l], acc);
-      const double v = sig[j] * acc;
-      if (col < ko) d.OM[(size_t)a * ko + col] = v / d.w[col];
-      else d.FM[(size_t)a * d.k_f + (col - ko)] = v / d.wf[col - ko];
+    // new basis = QA * phi[:, :k] and maps = (QB (sigma psi))[col][a] /
+    // weight[col]; each thread owns one row and a strip of 4 output columns
+    // (every Q element is loaded once per strip)
+    {
+      const int kb = (k + 3) >> 2;
+      for (long long e = threadIdx.x; e < (long long)(m + C) * kb; e += blockDim.x) {
+        const int row = (int)(e % (m + C)), a0 = 4 * (int)(e / (m + C));
+        const bool isA = row < m;
+        const int i = isA ? row : row - m;
+        const double* Q = isA ? QAp + i : QBp + i;
+        const int ldq = isA ? m : C;
+        const double* col[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = order[min(a0 + u, k - 1)];
+          col[u] = Z + (size_t)j * 2 * s + (isA ? s : 0);
+        }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = 0; l < s; ++l) {
+          const double q = Q[(size_t)l * ldq];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] = fma(q, col[u][l], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int a = a0 + u;
+          if (a >= k) break;
+          if (isA) d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc[u];
+          else if (i < ko) d.OM[(size_t)a * ko + i] = acc[u] / d.w[i];
+          else d.FM[(size_t)a * d.k_f + (i - ko)] = acc[u] / d.wf[i - ko];
+        }
+      }
     }
     for (int a = threadIdx.x; a < k; a += blockDim.x) d.NW[a] = sig[order[a]];
     if (threadIdx.x == 0) *d.rank = k;
@@ -961,6 +1376,7 @@ bool union_fits_smem(int m, int k_old, int k_f) {
 // smem == 0: workspaces in global memory with the full L1 as cache.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
                   int jac_smem_doubles) {
+  DbgSync dbg_sync_{s, "launch_union"};
   if (n <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -973,9 +1389,14 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     const char* e = getenv("IFMM_UNION_THREADS");
     nthr = e ? atoi(e) : 512;
   }
+  static int force_hh = -1;
+  if (force_hh < 0) {
+    const char* e = getenv("IFMM_UNION_HH");  // diagnostics: Householder QR path
+    force_hh = e ? atoi(e) : 0;
+  }
   if (smem)
     union_kernel<true><<<n < 4096 ? n : 4096, nthr, (size_t)UNION_SMEM_DOUBLES * 8, s>>>(
-        d_descs, n, thr, UNION_SMEM_DOUBLES);
+        d_descs, n, thr, UNION_SMEM_DOUBLES, force_hh);
   else {
     static bool attr2 = false;
     if (!attr2) {
@@ -983,9 +1404,10 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
                            UNION_SMEM_DOUBLES * 8);
       attr2 = true;
     }
-    // shared memory for the core SVD only (2 s^2 doubles, s <= ~118)
-    const int jd = jac_smem_doubles > 0 ? jac_smem_doubles : 0;
-    union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd);
+    // shared memory for the CholeskyQR matrices and the core SVD
+    (void)jac_smem_doubles;
+    const int jd = UNION_SMEM_DOUBLES;
+    union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
 }
 
@@ -1152,6 +1574,7 @@ lusolve_smem_kernel(const LuSolveDesc* __restrict__ descs, int ndesc, int chunks
 }  // namespace
 
 void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_lu"};
   if (n <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -1164,6 +1587,7 @@ void launch_lu(const LuDesc* d_descs, int n, int* d_status, cudaStream_t s) {
 
 void launch_lusolve(const LuSolveDesc* d_descs, int ndesc, int max_nrhs, cudaStream_t s,
                     int max_n) {
+  DbgSync dbg_sync_{s, "launch_lusolve"};
   if (ndesc <= 0 || max_nrhs <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -1366,16 +1790,19 @@ tall_orth_kernel(const double* Y, int n, int w, double* Q, double* work, int mod
 }  // namespace
 
 void launch_weights(const WeightDesc* d_descs, int n, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_weights"};
   if (n <= 0) return;
   weights_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d_descs, n);
 }
 
 void launch_tall_orth(const double* Y, int n, int w, double* Q, double* work, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_tall_orth"};
   tall_orth_kernel<<<1, 1024, 0, s>>>(Y, n, w, Q, work, 0, nullptr);
 }
 
 void launch_tall_sigmax(const double* Y, int n, int w, double* out, double* work,
                         cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_tall_sigmax"};
   tall_orth_kernel<<<1, 1024, 0, s>>>(Y, n, w, nullptr, work, 1, out);
 }
 
@@ -1511,23 +1938,28 @@ extend_kernel(double* NB, int m, int k, const double* G, int extra, double* NW, 
 
 void launch_panel_lu(double* A, int n, int lda, int j0, int jb, int* piv, int* status, int tag,
                      cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_panel_lu"};
   panel_lu_kernel<<<1, 1024, 0, s>>>(A, n, lda, j0, jb, piv, status, tag);
 }
 void launch_laswp(double* A, int n, int lda, int j0, int jb, const int* piv, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_laswp"};
   const int nc = n - jb;
   if (nc <= 0) return;
   laswp_kernel<<<(nc + 127) / 128, 128, 0, s>>>(A, n, lda, j0, jb, piv);
 }
 void launch_trsm_lunit(const double* L, int ldl, int nb, double* X, int ldx, int ncols,
                        cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_trsm_lunit"};
   if (ncols <= 0) return;
   trsm_lunit_kernel<<<(ncols + 127) / 128, 128, 0, s>>>(L, ldl, nb, X, ldx, ncols);
 }
 void launch_finite_check(const double* A, int n, int lda, int* status, int tag, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_finite_check"};
   finite_kernel<<<592, 256, 0, s>>>(A, n, lda, status, tag);
 }
 void launch_extend(double* NB, int m, int k, const double* G, int extra, double* NW, double thr,
                    double* work, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_extend"};
   extend_kernel<<<1, 512, 0, s>>>(NB, m, k, G, extra, NW, thr, work);
 }
 
@@ -1613,12 +2045,15 @@ rsvd_fin_kernel(const RsvdFinDesc* __restrict__ descs, int n, double thr) {
 }  // namespace
 
 void launch_randn(const RandDesc* d, int n, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_randn"};
   if (n > 0) randn_kernel<<<n < 4096 ? n : 4096, 256, 0, s>>>(d, n);
 }
 void launch_orth(const OrthDesc* d, int n, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_orth"};
   if (n > 0) orth_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d, n);
 }
 void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_rsvd_fin"};
   if (n > 0) rsvd_fin_kernel<<<n < 4096 ? n : 4096, 512, 0, s>>>(d, n, thr);
 }
 
@@ -1628,7 +2063,7 @@ void launch_rsvd_fin(const RsvdFinDesc* d, int n, double thr, cudaStream_t s) {
 namespace ifmm {
 namespace {
 __global__ void __launch_bounds__(512) jacobi_bench_kernel(const double* A, int s, int reps,
-                                                           unsigned long long* out) {
+                                                           unsigned long long* out, int variant) {
   extern __shared__ double sm[];
   __shared__ int sflag;
   double* W = sm;
@@ -1638,8 +2073,15 @@ __global__ void __launch_bounds__(512) jacobi_bench_kernel(const double* A, int 
   for (int r = 0; r < reps; ++r) {
     for (int e = threadIdx.x; e < s * s; e += blockDim.x) W[e] = A[e];
     __syncthreads();
+    if (variant) {  // union-core layout: Z = [A; V] (2s x s)
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int j = e / s, i = e % s;
+        W[(size_t)j * 2 * s + i] = A[e];
+      }
+      __syncthreads();
+    }
     const unsigned long long t0 = clock64();
-    sw += cta_jacobi(W, s, s, s, V, &sflag);
+    sw += variant ? cta_jacobi_z(W, s, &sflag) : cta_jacobi(W, s, s, s, V, &sflag);
     const unsigned long long t1 = clock64();
     tot += t1 - t0;
     __syncthreads();
@@ -1651,6 +2093,7 @@ void jacobi_bench(const double* A, int s, int reps, int threads, unsigned long l
                   cudaStream_t st) {
   cudaFuncSetAttribute(jacobi_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        220 * 1024);
-  jacobi_bench_kernel<<<1, threads, (size_t)2 * s * s * 8, st>>>(A, s, reps, d_out);
+  jacobi_bench_kernel<<<1, threads & 0xffff, (size_t)2 * s * s * 8, st>>>(A, s, reps, d_out,
+                                                                          threads >> 16);
 }
 }  // namespace ifmm

@@ -108,16 +108,19 @@ __global__ void grid_kernel(const GridDesc* __restrict__ descs, int n, int nc) {
 }  // namespace
 
 void launch_eval(const EvalDesc* d_descs, int n, const KernelSpec& k, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_eval"};
   if (n <= 0) return;
   eval_blocks_kernel<<<n < 16384 ? n : 16384, 256, 0, s>>>(d_descs, n, k);
 }
 
 void launch_interp(const InterpDesc* d_descs, int n, int nc, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_interp"};
   if (n <= 0) return;
   interp_kernel<<<n < 16384 ? n : 16384, 64, 0, s>>>(d_descs, n, nc);
 }
 
 void launch_grid(const GridDesc* d_descs, int n, int nc, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_grid"};
   if (n <= 0) return;
   grid_kernel<<<n < 16384 ? n : 16384, 128, 0, s>>>(d_descs, n, nc);
 }
@@ -164,6 +167,7 @@ exact_matvec_kernel(const double* __restrict__ pts, const double* __restrict__ x
 
 void launch_exact_matvec(const double* pts, const double* x, int n, const KernelSpec& k,
                          double* y, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_exact_matvec"};
   exact_matvec_kernel<<<(n + 255) / 256, 256, 0, s>>>(pts, x, n, k, y);
 }
 }  // namespace ifmm

@@ -32,7 +32,8 @@ void set_last_error(const std::string& s);
     cudaError_t _e = (x);                                                              \
     if (_e != cudaSuccess)                                                             \
       throw ::ifmm::Error(::ifmm::E_CUDA, std::string("CUDA error: ") +               \
-                                              cudaGetErrorString(_e) + " at " __FILE__); \
+                                              cudaGetErrorString(_e) + " at " __FILE__ ":" +      \
+                                              std::to_string(__LINE__));                 \
   } while (0)
 
 #define IFMM_ASSERT(c, msg)                                              \

@@ -35,6 +35,7 @@ spmv_kernel(const SpmvRow* __restrict__ rows, int nrows, const SpmvTerm* __restr
 
 void launch_spmv(const SpmvRow* rows, int nrows, const SpmvTerm* terms, int nrhs, int ldv,
                  cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_spmv"};
   if (nrows <= 0) return;
   spmv_kernel<<<nrows < 65535 ? nrows : 65535, 256, 0, s>>>(rows, nrows, terms, nrhs, ldv);
 }

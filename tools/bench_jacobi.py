@@ -1,4 +1,7 @@
-"""Micro-benchmark: cycles per Jacobi round for s x s graded matrices."""
+"""Micro-benchmark: cycles per Jacobi round for s x s graded matrices.
+
+variant 0: generic cta_jacobi (fill SVD / weights); variant 1: the union-core
+layout Z = [A; V] with one-pass rounds (cta_jacobi_z)."""
 import ctypes as C
 import os
 import sys
@@ -13,9 +16,12 @@ for s in (16, 40, 86, 110):
     V, _ = np.linalg.qr(rng.standard_normal((s, s)))
     A = (U * 10.0 ** -np.linspace(0, 10, s)) @ V.T
     dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F").copy()).cuda()
-    for thr in (128, 256, 512):
-        out = (C.c_ulonglong * 2)()
-        N.check(N.lib().ifmm_dev_jacobi_bench(N.ctx(), s, C.c_void_p(dA.data_ptr()), 5, thr, out))
-        cyc, sw = out[0] / 5, out[1] / 5
-        rounds = sw * (s + (s & 1) - 1)
-        print(f"s={s:4d} threads={thr:4d} sweeps={sw:5.1f} cycles={cyc:10.0f} cycles/round={cyc / max(rounds, 1):8.0f}")
+    for var in (0, 1):
+        for thr in (256, 512):
+            out = (C.c_ulonglong * 2)()
+            N.check(N.lib().ifmm_dev_jacobi_bench(N.ctx(), s, C.c_void_p(dA.data_ptr()), 5,
+                                                  thr | (var << 16), out))
+            cyc, sw = out[0] / 5, out[1] / 5
+            rounds = sw * (s + (s & 1) - 1)
+            print(f"variant={var} s={s:4d} threads={thr:4d} sweeps={sw:5.1f} cycles={cyc:10.0f} "
+                  f"cycles/round={cyc / max(rounds, 1):8.0f}", flush=True)
