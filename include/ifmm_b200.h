@@ -130,9 +130,10 @@ long long ifmm_ctx_launches(void* ctx);
  * algorithmic work = flops or bytes, launch count); enable >= 0 also resets
  * and switches timing on (1) or off (0). */
 int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* count, int n);
-/* Diagnostics: union-kernel cycle counters (32 entries: [0..12] all unions --
- * ACA, QR, Q, Jacobi, output, steps, count, sum m, sum C, smem count,
- * sweeps, core sweeps, core cycles; [16..24] the same for m > 256);
+/* Diagnostics: union-kernel cycle counters (48 entries: [0..12] all unions --
+ * ACA, CholeskyQR, core, Jacobi, output, steps, count, sum m, sum C, smem
+ * count, sweeps, core sweeps, core cycles, [13] Householder fallbacks;
+ * [16..24] the first nine for 256 < m <= 600, [25..33] for m > 600);
  * reset != 0 clears. */
 int ifmm_union_profile(unsigned long long* out, int reset);
 /* Diagnostics: phase times (s) of the last factorize when IFMM_PROFILE=1. */

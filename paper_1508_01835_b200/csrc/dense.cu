@@ -20,7 +20,7 @@
 namespace ifmm {
 
 // per-phase cycle counters of the union kernel (diagnostics)
-__device__ unsigned long long g_uprof[32];
+__device__ unsigned long long g_uprof[48];
 
 __device__ __forceinline__ void cta_geqrf(double* A, int rows, int cols, int lda, double* tau, double* red);
 __device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, int lda, const double* tau,
@@ -279,70 +279,32 @@ __device__ __forceinline__ int cta_jacobi(double* W, int rows, int cols, int ldw
   return sweep + 1;
 }
 
-// Union-core Jacobi.  Z is col-major (2s x s, ld 2s): rows [0, s) hold the
-// matrix, rows [s, 2s) the accumulated rotations (set to I here), so one
-// rotation loop updates both.  The team width is chosen so that every pair
-// of a round runs in one pass (one barrier per round).
-template <int T>
-__device__ __forceinline__ void jac_z_round(double* Z, int s, int cp, int r, double tol_rot2,
-                                            double tol_conv2, int* sflag) {
-  const int tl = threadIdx.x & (T - 1);
-  const int team = threadIdx.x / T, nteam = blockDim.x / T;
-  const int first_team_of_warp = (threadIdx.x & ~31) / T;
-  const int ld = 2 * s, half = cp / 2;
-  for (int pi0 = 0; pi0 < half; pi0 += nteam) {
-    if (pi0 + first_team_of_warp >= half) break;  // whole warp idle this round
-    const int pi = pi0 + team;
-    int p = 0, q = s;
-    if (pi < half) {
-      if (pi == 0) { p = r; q = cp - 1; }
-      else { p = (r + pi) % (cp - 1); q = (r - pi + cp - 1) % (cp - 1); }
-      if (p > q) { const int t = p; p = q; q = t; }
-    }
-    const bool act = pi < half && q < s;
-    double a = 0.0, b = 0.0, g = 0.0;
-    double* x = Z + (size_t)p * ld;
-    double* y = Z + (size_t)(act ? q : p) * ld;
-    if (act)
-      for (int i = tl; i < s; i += T) {
-        const double u = x[i], v = y[i];
-        a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
-      }
-    a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
-    if (!act) continue;
-    const double ab = a * b, g2 = g * g;
-    if (g != 0.0 && g2 > tol_rot2 * ab) {
-      // t = tan(theta) = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)), d = b - a, gg = 2g
-      const double d = b - a, gg = 2.0 * g;
-      const double t = copysign(fabs(gg), d * gg) / (fabs(d) + sqrt(fma(d, d, gg * gg)));
-      const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-      for (int i = tl; i < ld; i += T) {
-        const double u = x[i], v = y[i];
-        x[i] = fma(c, u, -sn * v);
-        y[i] = fma(sn, u, c * v);
-      }
-      if (tl == 0 && g2 > tol_conv2 * ab) *sflag = 1;
-    }
-  }
-}
-
-// One full round-robin sweep of the union-core Jacobi with the column pair's
-// matrix part held in registers (NE rows per lane, teams of T lanes), an
-// incremental pair schedule (no modulo) and one barrier per round.  Returns
-// the per-thread "not yet converged" flag.
+// Union-core Jacobi (one-sided, Hestenes, round-robin).  W (s x s, col-major,
+// ld s) holds the matrix; V (s x s, ld s) accumulates the rotations (set to
+// I here).  W and V may live in different memory spaces (V goes to global
+// memory when 2 s^2 does not fit in shared memory).
+//
+// One sweep: s-1 (or s) rounds with one barrier each.  A team of T lanes
+// handles one column pair per pass, holding its NE rows per lane of the W
+// columns in registers between the dot products and the rotation; the
+// pair schedule of pass 0 advances incrementally, later passes use the
+// closed form.  Returns the per-thread "not yet converged" flag.
 template <int T, int NE>
-__device__ __forceinline__ bool jac_z_sweep(double* Z, int s, int cp, double tr2, double tc2) {
-  const int tl = threadIdx.x & (T - 1), team = threadIdx.x / T;
-  const int half = cp >> 1, ld = 2 * s;
-  const bool warp_on = ((threadIdx.x & ~31) / T) < half;
-  int p = team, q = team == 0 ? cp - 1 : cp - 1 - team;
+__device__ __forceinline__ bool jac_sweep(double* W, double* V, int s, int cp, double tr2, double tc2) {
+  const int tl = threadIdx.x & (T - 1), team = threadIdx.x / T, nteam = blockDim.x / T;
+  const int half = cp >> 1, m1 = cp - 1;
+  const int first_team_of_warp = (threadIdx.x & ~31) / T;
+  int p0 = team, q0 = team == 0 ? m1 : m1 - team;  // pass-0 pair, advanced each round
   bool again = false;
-  for (int r = 0; r < cp - 1; ++r) {
-    if (warp_on) {
+  for (int r = 0; r < m1; ++r) {
+    for (int pi = team, pass = 0; pi - team + first_team_of_warp < half; pi += nteam, ++pass) {
+      int p, q;
+      if (pass == 0) { p = p0; q = q0; }
+      else { p = (r + pi) % m1; q = (r - pi + m1) % m1; }
       const int lo = p < q ? p : q, hi = p < q ? q : p;
-      const bool act = team < half && hi < s;
-      double* x = Z + (size_t)(act ? lo : 0) * ld;
-      double* y = Z + (size_t)(act ? hi : 0) * ld;
+      const bool act = pi < half && hi < s;
+      double* x = W + (size_t)(act ? lo : 0) * s;
+      double* y = W + (size_t)(act ? hi : 0) * s;
       double xr[NE], yr[NE];
       double a = 0.0, b = 0.0, g = 0.0;
 #pragma unroll
@@ -353,9 +315,15 @@ __device__ __forceinline__ bool jac_z_sweep(double* Z, int s, int cp, double tr2
         yr[e] = in ? y[i] : 0.0;
         a = fma(xr[e], xr[e], a); b = fma(yr[e], yr[e], b); g = fma(xr[e], yr[e], g);
       }
+      if (act)  // rows beyond the register tile (s > NE T only)
+        for (int i = tl + NE * T; i < s; i += T) {
+          const double u = x[i], v = y[i];
+          a = fma(u, u, a); b = fma(v, v, b); g = fma(u, v, g);
+        }
       a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
       const double ab = a * b, g2 = g * g;
       if (act && g != 0.0 && g2 > tr2 * ab) {
+        // t = tan(theta) = sign(d gg) |gg| / (|d| + sqrt(d^2 + gg^2)), d = b - a, gg = 2g
         const double d = b - a, gg = 2.0 * g;
         const double t = copysign(fabs(gg), d * gg) / (fabs(d) + sqrt(fma(d, d, gg * gg)));
         const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
@@ -367,57 +335,67 @@ __device__ __forceinline__ bool jac_z_sweep(double* Z, int s, int cp, double tr2
             y[i] = fma(sn, xr[e], c * yr[e]);
           }
         }
-        for (int i = s + tl; i < ld; i += T) {
+        for (int i = tl + NE * T; i < s; i += T) {
           const double u = x[i], v = y[i];
           x[i] = fma(c, u, -sn * v);
           y[i] = fma(sn, u, c * v);
+        }
+        // V columns in batches of 4 rows per lane, all loads before the
+        // stores (a load after a possibly aliasing store would wait for it)
+        double* vx = V + (size_t)lo * s;
+        double* vy = V + (size_t)hi * s;
+        for (int i0 = tl; i0 < s; i0 += 4 * T) {
+          double u[4], v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = i0 + e * T;
+            u[e] = i < s ? vx[i] : 0.0;
+            v[e] = i < s ? vy[i] : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = i0 + e * T;
+            if (i < s) {
+              vx[i] = fma(c, u[e], -sn * v[e]);
+              vy[i] = fma(sn, u[e], c * v[e]);
+            }
+          }
         }
         again |= g2 > tc2 * ab;
       }
     }
     __syncthreads();
-    if (team == 0) p = r + 1;
-    else { p = p + 1 == cp - 1 ? 0 : p + 1; q = q + 1 == cp - 1 ? 0 : q + 1; }
+    if (team == 0) p0 = r + 1;
+    else { p0 = p0 + 1 == m1 ? 0 : p0 + 1; q0 = q0 + 1 == m1 ? 0 : q0 + 1; }
   }
   return again;
 }
 
-__device__ __forceinline__ int cta_jacobi_z(double* Z, int s, int* sflag) {
-  const int ld = 2 * s;
+// Returns the number of sweeps.  Rotations are applied whenever a pair is not
+// orthogonal to working precision; only rotations above the dot-product
+// rounding level (s * eps) keep the sweeps going.
+__device__ __forceinline__ int cta_jacobi_wv(double* W, double* V, int s) {
   for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
-    const int j = e / s, i = e % s;
-    Z[(size_t)j * ld + s + i] = (i == j) ? 1.0 : 0.0;
+    const int j = e / s, i = e - j * s;
+    V[e] = (i == j) ? 1.0 : 0.0;
   }
   const double tol_rot = kEps;
   const double tol_conv = fmax(kEps * (double)(s > 4 ? s : 4), 1e-13);
   const double tr2 = tol_rot * tol_rot, tc2 = tol_conv * tol_conv;
-  const int cp = s + (s & 1), half = cp / 2;
+  const int cp = s + (s & 1);
   __syncthreads();
   if (s < 2) return 0;
-  const int nthr = blockDim.x;
-  const int T = half * 32 <= nthr ? 32 : half * 16 <= nthr ? 16 : half * 8 <= nthr ? 8 : 4;
-  // register-resident variants: rows per lane NE = ceil(s / T)
-  const int kind = (T == 32 && s <= 32) ? 1 : (T == 16 && s <= 64) ? 2 : (T == 8 && s <= 128) ? 3 : 0;
+  // rows per lane NE <= 16 (xr, yr: 64 registers; union_svd_kernel has the
+  // budget); rows beyond NE T (s > 256) are streamed from memory
+  const int kind = s <= 32 ? 0 : s <= 64 ? 1 : s <= 128 ? 2 : 3;
   int sweep = 0;
   for (; sweep < 40; ++sweep) {
-    int again;
-    if (kind == 1) again = __syncthreads_or(jac_z_sweep<32, 1>(Z, s, cp, tr2, tc2));
-    else if (kind == 2) again = __syncthreads_or(jac_z_sweep<16, 4>(Z, s, cp, tr2, tc2));
-    else if (kind == 3) again = __syncthreads_or(jac_z_sweep<8, 16>(Z, s, cp, tr2, tc2));
-    else {
-      if (threadIdx.x == 0) *sflag = 0;
-      __syncthreads();
-      for (int r = 0; r < cp - 1; ++r) {
-        if (T == 32) jac_z_round<32>(Z, s, cp, r, tr2, tc2, sflag);
-        else if (T == 16) jac_z_round<16>(Z, s, cp, r, tr2, tc2, sflag);
-        else if (T == 8) jac_z_round<8>(Z, s, cp, r, tr2, tc2, sflag);
-        else jac_z_round<4>(Z, s, cp, r, tr2, tc2, sflag);
-        __syncthreads();
-      }
-      again = *sflag;
-      __syncthreads();
-    }
-    if (!again) break;
+    bool ag;
+    if (kind == 0) ag = jac_sweep<32, 1>(W, V, s, cp, tr2, tc2);
+    else if (kind == 1) ag = jac_sweep<16, 4>(W, V, s, cp, tr2, tc2);
+    else if (kind == 2) ag = jac_sweep<8, 16>(W, V, s, cp, tr2, tc2);
+    else ag = jac_sweep<32, 8>(W, V, s, cp, tr2, tc2);  // + memory tail
+    if (!__syncthreads_or(ag)) break;
   }
   return sweep + 1;
 }
@@ -798,22 +776,23 @@ __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f) {
   const size_t sp = s + (s & 1);
   // Mreg: ACA residual (m C), then 6 s x sp CholeskyQR matrices, or QA
   //       (m s) on the Householder path
-  // | Acol (m s) | Bt (C s) | QB (C s, Householder path) | Z (2 s^2)
+  // | Acol (m s) | Bt (C s) | QB (C s, Householder path) | W, V (2 s^2)
   // | D, tauA, tauB, sig (4 s) | order (s ints) | acts, pos (2 C ints)
   const size_t mreg = (size_t)m * C > 6 * s * sp ? (size_t)m * C : 6 * s * sp;
   return mreg + (size_t)m * s + 2 * C * s + 2 * s * s + 5 * s + C + 16;
 }
 
 void union_profile(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 32);
+  cudaMemcpyFromSymbol(out, g_uprof, sizeof(unsigned long long) * 48);
   if (reset) {
-    unsigned long long z[32] = {};
+    unsigned long long z[48] = {};
     cudaMemcpyToSymbol(g_uprof, z, sizeof z);
   }
 }
 
 namespace {
 constexpr int UNION_SMEM_DOUBLES = 28500;  // 228 KB
+constexpr int UNION_SVD_SMEM_DOUBLES = 28000;  // + 6 KB static
 
 // Interleaved Householder QR of two column-major matrices A (ra x s) and
 // B (rb x s): two barriers per column for both.  On exit: R in the upper
@@ -1082,7 +1061,6 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
   __shared__ double wv[32];
   __shared__ long long wi[32];
   __shared__ double pa[32], pb[32];
-  __shared__ int sflag;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const UnionDesc d = descs[bb];
@@ -1102,8 +1080,6 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     int* order = (int*)(sig + smax);
     int* acts = order + smax + 1;
     int* pos = acts + C;
-    // global variant: the core SVD's working set in shared memory when it fits
-    const bool jsm = !SM && 2 * smax * smax <= smem_doubles;
 
     // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
     // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
@@ -1179,40 +1155,75 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       if (threadIdx.x == 0) M[(size_t)q * m + p] = 0.0;
       const int na = nact;
       bv = -1.0;
-      if (on)
-        for (int i = i0; i < m; i += R) {
-          const double ci = cc[i];
-          int l = g0;
-          // UN independent loads in flight per thread (16 on the
-          // global-workspace variant, which streams M through L2 every step)
-          constexpr int UN = SM ? 8 : 16;
-          for (; l + (UN - 1) * G < na; l += UN * G) {
-            int jj[UN];
-            double v[UN];
+      if (SM) {
+        if (on)
+          for (int i = i0; i < m; i += R) {
+            const double ci = cc[i];
+            int l = g0;
+            for (; l + 7 * G < na; l += 8 * G) {
+              int jj[8];
+              double v[8];
 #pragma unroll
-            for (int u = 0; u < UN; ++u) { jj[u] = acts[l + u * G]; v[u] = M[(size_t)jj[u] * m + i]; }
+              for (int u = 0; u < 8; ++u) { jj[u] = acts[l + u * G]; v[u] = M[(size_t)jj[u] * m + i]; }
 #pragma unroll
-            for (int u = 0; u < UN; ++u) {
-              v[u] = fma(-ci, rr[jj[u]], v[u]);
-              M[(size_t)jj[u] * m + i] = v[u];
-              const double av = fabs(v[u]);
-              if (better(av, i, jj[u])) { bv = av; bi = i; bj = jj[u]; }
+              for (int u = 0; u < 8; ++u) {
+                v[u] = fma(-ci, rr[jj[u]], v[u]);
+                M[(size_t)jj[u] * m + i] = v[u];
+                const double av = fabs(v[u]);
+                if (better(av, i, jj[u])) { bv = av; bi = i; bj = jj[u]; }
+              }
+            }
+            for (; l < na; l += G) {
+              const int j = acts[l];
+              double* mp = M + (size_t)j * m + i;
+              const double v = fma(-ci, rr[j], *mp);
+              *mp = v;
+              const double av = fabs(v);
+              if (better(av, i, j)) { bv = av; bi = i; bj = j; }
             }
           }
-          for (; l < na; l += G) {
-            const int j = acts[l];
-            double* mp = M + (size_t)j * m + i;
-            const double v = fma(-ci, rr[j], *mp);
-            *mp = v;
-            const double av = fabs(v);
-            if (better(av, i, j)) { bv = av; bi = i; bj = j; }
+      } else {
+        // global workspace: M streams through L2 every step.  The m x na
+        // active block is flattened (row fastest, coalesced) and dealt out
+        // evenly; every batch issues all UN loads before any store, also in
+        // the last partial batch (a load after a possibly aliasing store
+        // would serialise on the L2 round trip).
+        constexpr int UN = 16;
+        const int total = m * na, nthr = blockDim.x;
+        const int di = nthr % m, dl = nthr / m;
+        int f = threadIdx.x, i = f % m, l = f / m;
+        while (f < total) {
+          int ii[UN], jj[UN];
+          double v[UN];
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const bool ok = f + u * nthr < total;
+            ii[u] = i;
+            jj[u] = ok ? acts[l] : -1;
+            v[u] = ok ? M[(size_t)jj[u] * m + i] : 0.0;
+            i += di; l += dl;
+            if (i >= m) { i -= m; ++l; }
           }
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            if (jj[u] < 0) break;
+            v[u] = fma(-cc[ii[u]], rr[jj[u]], v[u]);
+            M[(size_t)jj[u] * m + ii[u]] = v[u];
+            const double av = fabs(v[u]);
+            if (better(av, ii[u], jj[u])) { bv = av; bi = ii[u]; bj = jj[u]; }
+          }
+          f += UN * nthr;
         }
+      }
       ++steps;
     }
     __syncthreads();
     if (steps == 0) {
-      if (threadIdx.x == 0) *d.rank = 0;
+      if (threadIdx.x == 0) {
+        *d.rank = 0;
+        double* gW = d.work + mreg + (size_t)m * smax + 2 * (size_t)C * smax;
+        *(int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax) = 0;  // header: s = 0
+      }
       __syncthreads();
       continue;
     }
@@ -1248,25 +1259,39 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     const bool hh = force_hh || !(r1 > kCholFloor);
     const double* QAp;
     const double* QBp;
-    double* Z = (qsm || jsm) ? smem : core;
+    // W = core^T (s x s): in shared memory on the global variant when it fits
+    double* Wc = (!SM && (size_t)s * s <= (size_t)smem_doubles) ? smem : core;
     if (!hh) {
+      unsigned long long c0 = clock64();
       cta_trsm2(Acol, m, GA, ia, Bt, C, GB, ib, s, sp);
       for (int e = threadIdx.x; e < 2 * s * sp; e += blockDim.x) RA1s[e] = GA[e];  // park R1
       __syncthreads();
+      unsigned long long c1 = clock64();
       cta_gram2(Acol, m, Bt, C, s, sp, GA, GB);
       __syncthreads();
+      unsigned long long c2 = clock64();
       cta_chol2(GA, ia, GB, ib, s, sp);
+      unsigned long long c3 = clock64();
       cta_trsm2(Acol, m, GA, ia, Bt, C, GB, ib, s, sp);
       // R_A = R_A2 R_A1, R_B = R_B2 R_B1
       cta_trmul2(GA, RA1s, TA, GB, RB1s, TB, s, sp);
       __syncthreads();
-      // Z = [core^T ; I], core^T = R_B D R_A^T (see below)
+      unsigned long long c4 = clock64();
+      if (threadIdx.x == 0 && m > 400) {  // CholeskyQR sub-phases of large unions
+        atomicAdd(&g_uprof[34], c1 - c0);
+        atomicAdd(&g_uprof[35], c2 - c1);
+        atomicAdd(&g_uprof[36], c3 - c2);
+        atomicAdd(&g_uprof[37], c4 - c3);
+        atomicAdd(&g_uprof[38], c0 - t1);
+        atomicAdd(&g_uprof[39], 1ull);
+      }
+      // W = core^T = R_B D R_A^T
       for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
         const int j = e / s, i = e - j * s;
         double acc = 0.0;
         for (int l = (i > j ? i : j); l < s; ++l)
           acc = fma(TB[(size_t)i * sp + l] * Dp[l], TA[(size_t)j * sp + l], acc);
-        Z[(size_t)j * 2 * s + i] = acc;
+        Wc[(size_t)j * s + i] = acc;
       }
       QAp = Acol;
       QBp = Bt;
@@ -1279,7 +1304,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
         double acc = 0.0;
         for (int l = (i > j ? i : j); l < s; ++l)
           acc = fma(Bt[(size_t)l * C + i] * Dp[l], Acol[(size_t)l * m + j], acc);
-        Z[(size_t)j * 2 * s + i] = acc;
+        Wc[(size_t)j * s + i] = acc;
       }
       cta_orgqr2(Acol, m, tauA, M, Bt, C, tauB, QB, s);
       QAp = M;
@@ -1287,25 +1312,90 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       if (threadIdx.x == 0) atomicAdd(&g_uprof[13], 1ull);
     }
     unsigned long long t2 = clock64();
-    // ---- SVD of the core: one-sided Jacobi on its transpose.  The ACA
-    // pivots grade the core's rows, so its columns are graded in the
-    // transpose and the sweeps converge in ~4 instead of ~7 passes (measured
-    // on oracle unions).  On exit rows [s, 2s) of Z hold the core's left
-    // singular vectors (phi) and rows [0, s) its scaled right singular
-    // vectors (sigma psi).
+    // ---- hand-off to union_svd_kernel: QA, QB and W = core^T persist in the
+    // global workspace at fixed offsets, plus a header (s, QA / QB offsets)
+    {
+      double* g = d.work;
+      double* gQA = g + mreg;
+      double* gQB = gQA + (size_t)m * smax;
+      double* gW = gQB + 2 * (size_t)C * smax;
+      const double* QAsrc = QAp;
+      const double* QBsrc = QBp;
+      if (QAsrc != gQA)
+        for (long long e = threadIdx.x; e < (long long)m * s; e += blockDim.x) gQA[e] = QAsrc[e];
+      if (QBsrc != gQB)
+        for (long long e = threadIdx.x; e < (long long)C * s; e += blockDim.x) gQB[e] = QBsrc[e];
+      if (Wc != gW)
+        for (int e = threadIdx.x; e < s * s; e += blockDim.x) gW[e] = Wc[e];
+      if (threadIdx.x == 0) {
+        int* hdr = (int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax);  // the order slot
+        hdr[0] = s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_uprof[0], t1 - t0);
+      atomicAdd(&g_uprof[1], t2 - t1);
+      atomicAdd(&g_uprof[5], (unsigned long long)s);
+      atomicAdd(&g_uprof[6], 1ull);
+      atomicAdd(&g_uprof[7], (unsigned long long)m);
+      atomicAdd(&g_uprof[8], (unsigned long long)C);
+      atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));
+      if (m > 128) {  // larger unions separately: 128 < m <= 400 -> [16, 25), m > 400 -> [25, 34)
+        unsigned long long* u = g_uprof + (m > 400 ? 25 : 16);
+        atomicAdd(&u[0], t1 - t0);
+        atomicAdd(&u[1], t2 - t1);
+        atomicAdd(&u[5], (unsigned long long)s);
+        atomicAdd(&u[6], 1ull);
+        atomicAdd(&u[7], (unsigned long long)m);
+        atomicAdd(&u[8], (unsigned long long)C);
+      }
+    }
+  }
+}
+
+// Second half of the union: SVD of the core (one-sided Jacobi on its
+// transpose W = core^T with accumulated V) and the output products.  A
+// separate kernel so the Jacobi gets its own register budget (teams of 8
+// lanes holding 16 rows each run a round in one pass).  The ACA pivots grade
+// the core's rows, so its columns are graded in the transpose and the sweeps
+// converge in ~4-5 instead of ~7 passes (measured on oracle unions).  On
+// exit V holds the core's left singular vectors (phi) and W its scaled right
+// singular vectors (sigma psi):
+//   new basis = QA phi[:, :k],  maps = (QB sigma psi)[col][a] / weight[col].
+__global__ void __launch_bounds__(512)
+union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
+  extern __shared__ double smem[];
+  __shared__ double sig_s[512];
+  __shared__ int order_s[512];
+  for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
+    const UnionDesc d = descs[bb];
+    const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
+    const int smax = m < C ? m : C;
+    const int spx = smax + (smax & 1);
+    const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+    const double* gQA = d.work + mreg;
+    const double* gQB = gQA + (size_t)m * smax;
+    double* gW = (double*)gQB + 2 * (size_t)C * smax;
+    const int s = *(const int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax);
+    if (s == 0) continue;  // rank 0 already written by the first half
     unsigned long long t3 = clock64();
-    const int nsw = cta_jacobi_z(Z, s, &sflag);
+    double* Wc = (size_t)s * s <= (size_t)smem_doubles ? smem : gW;
+    double* Vc = 2 * (size_t)s * s <= (size_t)smem_doubles ? smem + (size_t)s * s : gW + (size_t)s * s;
+    if (Wc != gW)
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) Wc[e] = gW[e];
+    __syncthreads();
+    const int nsw = cta_jacobi_wv(Wc, Vc, s);
     unsigned long long t35 = clock64();
-    cta_sv_order(Z, s, s, 2 * s, sig, order);
+    double* sig = sig_s;
+    int* order = order_s;
+    cta_sv_order(Wc, s, s, s, sig, order);
     unsigned long long t4 = clock64();
-    if (threadIdx.x == 0) { atomicAdd(&g_uprof[11], (unsigned long long)nsw);
-                            atomicAdd(&g_uprof[12], t35 - t3); }
     int kk = 0;
     for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
     const int mr = d.min_rank < s ? d.min_rank : s;
     const int k = kk > mr ? kk : mr;
-    // new basis = QA * phi[:, :k] and maps = (QB (sigma psi))[col][a] /
-    // weight[col]; each thread owns one row and a strip of 4 output columns
+    // each thread owns one output row and a strip of 4 output columns
     // (every Q element is loaded once per strip)
     {
       const int kb = (k + 3) >> 2;
@@ -1313,13 +1403,13 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
         const int row = (int)(e % (m + C)), a0 = 4 * (int)(e / (m + C));
         const bool isA = row < m;
         const int i = isA ? row : row - m;
-        const double* Q = isA ? QAp + i : QBp + i;
+        const double* Q = isA ? gQA + i : gQB + i;
         const int ldq = isA ? m : C;
         const double* col[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = order[min(a0 + u, k - 1)];
-          col[u] = Z + (size_t)j * 2 * s + (isA ? s : 0);
+          col[u] = (isA ? Vc : Wc) + (size_t)j * s;
         }
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int l = 0; l < s; ++l) {
@@ -1342,26 +1432,15 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned long long t5 = clock64();
-      atomicAdd(&g_uprof[0], t1 - t0);
-      atomicAdd(&g_uprof[1], t2 - t1);
-      atomicAdd(&g_uprof[2], t3 - t2);
       atomicAdd(&g_uprof[3], t4 - t3);
       atomicAdd(&g_uprof[4], t5 - t4);
-      atomicAdd(&g_uprof[5], (unsigned long long)s);
-      atomicAdd(&g_uprof[6], 1ull);
-      atomicAdd(&g_uprof[7], (unsigned long long)m);
-      atomicAdd(&g_uprof[8], (unsigned long long)C);
-      atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));
-      if (m > 256) {  // large unions separately
-        atomicAdd(&g_uprof[16], t1 - t0);
-        atomicAdd(&g_uprof[17], t2 - t1);
-        atomicAdd(&g_uprof[18], t3 - t2);
-        atomicAdd(&g_uprof[19], t4 - t3);
-        atomicAdd(&g_uprof[20], t5 - t4);
-        atomicAdd(&g_uprof[21], (unsigned long long)s);
-        atomicAdd(&g_uprof[22], 1ull);
-        atomicAdd(&g_uprof[23], (unsigned long long)m);
-        atomicAdd(&g_uprof[24], (unsigned long long)C);
+      atomicAdd(&g_uprof[11], (unsigned long long)nsw);
+      atomicAdd(&g_uprof[12], t35 - t3);
+      if (m > 128) {
+        unsigned long long* u = g_uprof + (m > 400 ? 25 : 16);
+        atomicAdd(&u[3], t4 - t3);
+        atomicAdd(&u[4], t5 - t4);
+        atomicAdd(&u[2], (unsigned long long)nsw);  // sweeps (slot 2 is free)
       }
     }
   }
@@ -1394,6 +1473,12 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     const char* e = getenv("IFMM_UNION_HH");  // diagnostics: Householder QR path
     force_hh = e ? atoi(e) : 0;
   }
+  static bool attr3 = false;
+  if (!attr3) {
+    cudaFuncSetAttribute(union_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         UNION_SVD_SMEM_DOUBLES * 8);
+    attr3 = true;
+  }
   if (smem)
     union_kernel<true><<<n < 4096 ? n : 4096, nthr, (size_t)UNION_SMEM_DOUBLES * 8, s>>>(
         d_descs, n, thr, UNION_SMEM_DOUBLES, force_hh);
@@ -1409,6 +1494,8 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     const int jd = UNION_SMEM_DOUBLES;
     union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
+  union_svd_kernel<<<n < 4096 ? n : 4096, 512, (size_t)UNION_SVD_SMEM_DOUBLES * 8, s>>>(
+      d_descs, n, thr, UNION_SVD_SMEM_DOUBLES);
 }
 
 // ============================================================================
@@ -2073,15 +2160,8 @@ __global__ void __launch_bounds__(512) jacobi_bench_kernel(const double* A, int 
   for (int r = 0; r < reps; ++r) {
     for (int e = threadIdx.x; e < s * s; e += blockDim.x) W[e] = A[e];
     __syncthreads();
-    if (variant) {  // union-core layout: Z = [A; V] (2s x s)
-      for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
-        const int j = e / s, i = e % s;
-        W[(size_t)j * 2 * s + i] = A[e];
-      }
-      __syncthreads();
-    }
     const unsigned long long t0 = clock64();
-    sw += variant ? cta_jacobi_z(W, s, &sflag) : cta_jacobi(W, s, s, s, V, &sflag);
+    sw += variant ? cta_jacobi_wv(W, V, s) : cta_jacobi(W, s, s, s, V, &sflag);
     const unsigned long long t1 = clock64();
     tot += t1 - t0;
     __syncthreads();

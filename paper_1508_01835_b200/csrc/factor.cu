@@ -198,6 +198,15 @@ struct Eliminator {
     UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
     cudaEvent_t ka = nullptr;
+    static FILE* ulog = nullptr;
+    static bool ulog_init = false;
+    if (!ulog_init) {  // IFMM_UNION_LOG=<file>: one line per union launch (diagnostics)
+      ulog_init = true;
+      if (const char* f = getenv("IFMM_UNION_LOG")) ulog = fopen(f, "w");
+    }
+    auto tl0 = std::chrono::steady_clock::now();
+    if (ulog) CUDA_CHECK(cudaStreamSynchronize(C.st));
+    auto tl1 = std::chrono::steady_clock::now();
     C.kt_begin(K_UNION, uflops, &ka);
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
@@ -208,6 +217,18 @@ struct Eliminator {
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(dr, reqs.size());
+    if (ulog) {
+      auto tl2 = std::chrono::steady_clock::now();
+      int mm = 0, mc = 0, mk = 0;
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        mm = std::max(mm, reqs[i].bu->m);
+        mc = std::max(mc, reqs[i].bu->k_old + reqs[i].bu->k_f);
+        mk = std::max(mk, hr[i]);
+      }
+      fprintf(ulog, "%zu %zu %d %d %d %.3f %.3f\n", us.size(), ug.size(), mm, mc, mk,
+              std::chrono::duration<double, std::milli>(tl2 - tl1).count(),
+              std::chrono::duration<double, std::milli>(tl1 - tl0).count());
+    }
     for (size_t i = 0; i < reqs.size(); ++i) {
       reqs[i].bu->rank = hr[i];
       C.free(reqs[i].bu->W);

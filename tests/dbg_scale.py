@@ -22,15 +22,21 @@ l0 = NN.launches()
 t = time.perf_counter(); f = P.factorize(gr, 1e-6, sigma0=s0); tf = time.perf_counter() - t
 print("launches", NN.launches() - l0)
 import ctypes as CC
-up = (CC.c_ulonglong * 32)()
+up = (CC.c_ulonglong * 48)()
 NN.lib().ifmm_union_profile(up, 1)
 u = list(up); n_ = max(u[6], 1)
 print("union prof: per-union Mcycles aca %.3f qr %.3f q %.3f jac %.3f out %.3f | steps %.1f m %.1f C %.1f smem %d/%d sweeps/union %.2f" % (
     u[0]/n_/1e6, u[1]/n_/1e6, u[2]/n_/1e6, u[3]/n_/1e6, u[4]/n_/1e6, u[5]/n_, u[7]/n_, u[8]/n_, u[9], u[6], u[10]/n_))
 print("union core jacobi: sweeps/union %.2f  Mcycles/union %.3f" % (u[11]/n_, u[12]/n_/1e6))
-nb = max(u[22], 1)
-print("large unions (m>256): n %d  Mcycles aca %.3f qr %.3f q %.3f jac %.3f out %.3f | steps %.1f m %.1f C %.1f" % (
-    u[22], u[16]/nb/1e6, u[17]/nb/1e6, u[18]/nb/1e6, u[19]/nb/1e6, u[20]/nb/1e6, u[21]/nb, u[23]/nb, u[24]/nb))
+for lo, hi, b in ((128, 400, 16), (400, 1 << 30, 25)):
+    nb = max(u[b + 6], 1)
+    print("unions %d < m <= %s: n %d  Mcycles aca %.3f cholqr %.3f sweeps %.2f jac %.3f out %.3f | steps %.1f m %.1f C %.1f" % (
+        lo, hi if hi < 1 << 30 else "inf", u[b + 6], u[b]/nb/1e6, u[b + 1]/nb/1e6, u[b + 2]/nb, u[b + 3]/nb/1e6,
+        u[b + 4]/nb/1e6, u[b + 5]/nb, u[b + 7]/nb, u[b + 8]/nb))
+print("householder fallbacks", u[13])
+nq = max(u[39], 1)
+print("large-union CholeskyQR Mcycles: scale+gram1+chol1 %.3f trsm1+park %.3f gram2 %.3f chol2 %.3f trsm2+trmul %.3f" % (
+    u[38]/nq/1e6, u[34]/nq/1e6, u[35]/nq/1e6, u[36]/nq/1e6, u[37]/nq/1e6))
 if os.environ.get("KT") == "1":
     kt = NN.ktime(0); print("ktime", {k: (round(v[0], 3), v[2]) for k, v in kt.items() if v[2]}, "sum", round(sum(v[0] for v in kt.values()), 3))
 print(f"factorize {tf:.2f}s stats peak_edges={f.stats.peak_edges} events={f.event_counts} flops={f.flops}", flush=True)

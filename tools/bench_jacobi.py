@@ -25,3 +25,16 @@ for s in (16, 40, 86, 110):
             rounds = sw * (s + (s & 1) - 1)
             print(f"variant={var} s={s:4d} threads={thr:4d} sweeps={sw:5.1f} cycles={cyc:10.0f} "
                   f"cycles/round={cyc / max(rounds, 1):8.0f}", flush=True)
+
+# real union cores (transposed, as the kernel sees them) from oracle unions of
+# the c3 recipe at N=32768 (tools/micro/union_cores.npz)
+cores = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "micro", "union_cores.npz"))
+for name in sorted(cores.files):
+    A = cores[name]
+    s = A.shape[0]
+    dA = torch.from_numpy(np.asfortranarray(A).ravel(order="F").copy()).cuda()
+    out = (C.c_ulonglong * 2)()
+    N.check(N.lib().ifmm_dev_jacobi_bench(N.ctx(), s, C.c_void_p(dA.data_ptr()), 5, 512 | (1 << 16), out))
+    cyc, sw = out[0] / 5, out[1] / 5
+    print(f"real core {name}: s={s} sweeps={sw:.1f} cycles={cyc:.0f} cycles/round={cyc / max(sw * (s + (s & 1) - 1), 1):.0f}",
+          flush=True)
