@@ -1067,9 +1067,14 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
     const int spx = smax + (smax & 1);
-    double* M = SM ? smem : d.work;  // compile-time space: LDS/STS on the smem path
+    // Mw: the workspace's residual region.  M: where the ACA residual lives --
+    // shared memory on the smem variant, and on the global variant too when
+    // m x C fits (the rest of the workspace stays in global memory).
+    double* Mw = SM ? smem : d.work;  // compile-time space: LDS/STS on the smem path
+    const bool msm = !SM && (size_t)m * C <= (size_t)smem_doubles;
+    double* M = msm ? smem : Mw;
     const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
-    double* Acol = M + mreg;
+    double* Acol = Mw + mreg;
     double* Bt = Acol + (size_t)m * smax;
     double* QB = Bt + (size_t)C * smax;
     double* core = QB + (size_t)C * smax;
@@ -1240,9 +1245,9 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     // memory for the global variant when 2 s x sp fit; R1 and the products
     // T = R2 R1 live in the (dead) residual region.
     const bool qsm = !SM && 2 * (size_t)s * sp <= (size_t)smem_doubles;
-    double* GA = qsm ? smem : M;
+    double* GA = qsm ? smem : Mw;
     double* GB = GA + (size_t)s * sp;
-    double* RA1s = M + (qsm ? 0 : 2 * (size_t)s * sp);
+    double* RA1s = Mw + (qsm ? 0 : 2 * (size_t)s * sp);
     double* RB1s = RA1s + (size_t)s * sp;
     double* TA = RB1s + (size_t)s * sp;
     double* TB = TA + (size_t)s * sp;
@@ -1306,8 +1311,8 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
           acc = fma(Bt[(size_t)l * C + i] * Dp[l], Acol[(size_t)l * m + j], acc);
         Wc[(size_t)j * s + i] = acc;
       }
-      cta_orgqr2(Acol, m, tauA, M, Bt, C, tauB, QB, s);
-      QAp = M;
+      cta_orgqr2(Acol, m, tauA, Mw, Bt, C, tauB, QB, s);
+      QAp = Mw;
       QBp = QB;
       if (threadIdx.x == 0) atomicAdd(&g_uprof[13], 1ull);
     }
@@ -1340,7 +1345,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       atomicAdd(&g_uprof[6], 1ull);
       atomicAdd(&g_uprof[7], (unsigned long long)m);
       atomicAdd(&g_uprof[8], (unsigned long long)C);
-      atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));
+      atomicAdd(&g_uprof[9], (unsigned long long)(M == smem));  // residual on chip
       if (m > 128) {  // larger unions separately: 128 < m <= 400 -> [16, 25), m > 400 -> [25, 34)
         unsigned long long* u = g_uprof + (m > 400 ? 25 : 16);
         atomicAdd(&u[0], t1 - t0);
