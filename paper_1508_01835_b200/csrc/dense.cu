@@ -973,28 +973,51 @@ __device__ __forceinline__ double cta_chol2(double* GA, double* ia, double* GB, 
     mxA = fmax(mxA, GA[(size_t)k * sp + k]);
     mxB = fmax(mxB, GB[(size_t)k * sp + k]);
   }
+  const double imxA = 1.0 / mxA, imxB = 1.0 / mxB;
   __syncthreads();
   for (int k = 0; k <= s; ++k) {
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      double* G = w ? GB : GA;
-      double* iv = w ? ib : ia;
-      if (k > 0) {  // finalise row k-1 of R
-        double* gr = G + (size_t)(k - 1) * sp;
-        const double rinv = iv[k - 1];
-        for (int j = k - 1 + threadIdx.x; j < s; j += blockDim.x) gr[j] *= rinv;
+    if (k > 0) {  // finalise row k-1 of both R factors
+      const double ra = ia[k - 1], rb = ib[k - 1];
+      double* gra = GA + (size_t)(k - 1) * sp;
+      double* grb = GB + (size_t)(k - 1) * sp;
+      for (int j = k - 1 + threadIdx.x; j < s; j += blockDim.x) {
+        gra[j] *= ra;
+        grb[j] *= rb;
       }
-      if (k < s) {
-        const double* g = G + (size_t)k * sp;  // row k (final, unscaled)
-        const double gkk = g[k];
-        const double inv = 1.0 / gkk, rinv = 1.0 / sqrt(gkk);
-        const double ratio = gkk / (w ? mxB : mxA);
-        minr = (ratio > 0.0 && isfinite(gkk)) ? fmin(minr, ratio) : 0.0;
-        if (threadIdx.x == 0) iv[k] = rinv;
-        for (int i = k + 1 + wid; i < s; i += nwp) {
-          const double fi = g[i] * inv;
-          double* Gi = G + (size_t)i * sp;
-          for (int j = i + lane; j < s; j += 32) Gi[j] = fma(-fi, g[j], Gi[j]);
+    }
+    if (k < s) {
+      // both pivots' reciprocals first (independent long-latency chains)
+      const double* ga = GA + (size_t)k * sp;
+      const double* gb = GB + (size_t)k * sp;
+      const double pa = ga[k], pb = gb[k];
+      const double inva = 1.0 / pa, invb = 1.0 / pb;
+      const double ra = rsqrt(pa), rb = rsqrt(pb);
+      const double qa = pa * imxA, qb = pb * imxB;
+      minr = (qa > 0.0 && isfinite(pa)) ? fmin(minr, qa) : 0.0;
+      minr = (qb > 0.0 && isfinite(pb)) ? fmin(minr, qb) : 0.0;
+      if (threadIdx.x == 0) { ia[k] = ra; ib[k] = rb; }
+      // trailing rows i > k of both matrices, one warp per (matrix, row),
+      // lanes along the row; all loads of a row before its stores
+      const int nr = s - k - 1;
+      for (int t = wid; t < 2 * nr; t += nwp) {
+        const bool isA = t < nr;
+        const int i = k + 1 + (isA ? t : t - nr);
+        const double* g = isA ? ga : gb;
+        double* Gi = (isA ? GA : GB) + (size_t)i * sp;
+        const double fi = g[i] * (isA ? inva : invb);
+        for (int j0 = i + lane; j0 < s; j0 += 128) {
+          double gv[4], gw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + 32 * u;
+            gv[u] = j < s ? g[j] : 0.0;
+            gw[u] = j < s ? Gi[j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + 32 * u;
+            if (j < s) Gi[j] = fma(-fi, gv[u], gw[u]);
+          }
         }
       }
     }
@@ -1019,11 +1042,18 @@ __device__ __forceinline__ void cta_trsm2(double* A, int ra, const double* RA, c
       int cj[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) { cj[u] = min(j0 + u, s - 1); a[u] = X[(size_t)cj[u] * r + rr]; }
-      for (int i = 0; i < j0; ++i) {
-        const double xi = X[(size_t)i * r + rr];
-        const double* Ri = R + (size_t)i * sp;
+      // already-solved entries of the row, 8 independent loads per batch
+      // (X may sit in global memory: one L2 round trip per batch, not per entry)
+      for (int i0 = 0; i0 < j0; i0 += 8) {
+        double xv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = fma(-xi, Ri[cj[u]], a[u]);
+        for (int v = 0; v < 8; ++v) xv[v] = X[(size_t)(i0 + v) * r + rr];  // i0 + 8 <= j0
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double* Ri = R + (size_t)(i0 + v) * sp;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = fma(-xv[v], Ri[cj[u]], a[u]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -1236,10 +1266,16 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     const int sp = s + (s & 1);
     unsigned long long t1 = clock64();
     // ---- scale X columns by 1/pivot: L~ = X D^{-1} ----
-    for (long long e = threadIdx.x; e < (long long)m * s; e += blockDim.x) {
-      const int t = (int)(e / m);
-      Acol[e] /= Dp[t];
-    }
+    // thread per row, 8 columns per batch with all loads before the stores
+    for (int i = threadIdx.x; i < m; i += blockDim.x)
+      for (int t0 = 0; t0 < s; t0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = t0 + u < s ? Acol[(size_t)(t0 + u) * m + i] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u < s) Acol[(size_t)(t0 + u) * m + i] = v[u] / Dp[t0 + u];
+      }
     // ---- CholeskyQR2 of L~ (m x s) and Y (C x s); M is free now ----
     // CholeskyQR workspace: G_A, G_B (Cholesky in place -> R) in shared
     // memory for the global variant when 2 s x sp fit; R1 and the products
@@ -2165,6 +2201,24 @@ __global__ void __launch_bounds__(512) jacobi_bench_kernel(const double* A, int 
   for (int r = 0; r < reps; ++r) {
     for (int e = threadIdx.x; e < s * s; e += blockDim.x) W[e] = A[e];
     __syncthreads();
+    if (variant == 2) {  // CholeskyQR building block: in-place Cholesky of two s x s SPD copies
+      const int sp = s + (s & 1);
+      double* GA = sm;
+      double* GB = sm + (size_t)s * sp;
+      double* iv = sm + 2 * (size_t)s * sp;
+      for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int i = e / s, j = e - i * s;
+        GA[(size_t)i * sp + j] = A[e];
+        GB[(size_t)i * sp + j] = A[e];
+      }
+      __syncthreads();
+      const unsigned long long t0 = clock64();
+      cta_chol2(GA, iv, GB, iv + s, s, sp);
+      tot += clock64() - t0;
+      sw += s;
+      __syncthreads();
+      continue;
+    }
     const unsigned long long t0 = clock64();
     sw += variant ? cta_jacobi_wv(W, V, s) : cta_jacobi(W, s, s, s, V, &sflag);
     const unsigned long long t1 = clock64();
@@ -2178,7 +2232,7 @@ void jacobi_bench(const double* A, int s, int reps, int threads, unsigned long l
                   cudaStream_t st) {
   cudaFuncSetAttribute(jacobi_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        220 * 1024);
-  jacobi_bench_kernel<<<1, threads & 0xffff, (size_t)2 * s * s * 8, st>>>(A, s, reps, d_out,
+  jacobi_bench_kernel<<<1, threads & 0xffff, (size_t)(2 * (s + 1) * (s + 1) + s + 8) * 8, st>>>(A, s, reps, d_out,
                                                                           threads >> 16);
 }
 }  // namespace ifmm

@@ -38,3 +38,13 @@ for name in sorted(cores.files):
     cyc, sw = out[0] / 5, out[1] / 5
     print(f"real core {name}: s={s} sweeps={sw:.1f} cycles={cyc:.0f} cycles/round={cyc / max(sw * (s + (s & 1) - 1), 1):.0f}",
           flush=True)
+
+# in-place Cholesky (CholeskyQR building block): cycles per column step
+for s in (40, 64, 88, 120):
+    rng = np.random.default_rng(s)
+    X = rng.standard_normal((3 * s, s))
+    G = X.T @ X
+    dG = torch.from_numpy(G.ravel().copy()).cuda()
+    out = (C.c_ulonglong * 2)()
+    N.check(N.lib().ifmm_dev_jacobi_bench(N.ctx(), s, C.c_void_p(dG.data_ptr()), 5, 512 | (2 << 16), out))
+    print(f"chol2 s={s}: cycles={out[0] / 5:.0f} per column step={out[0] / 5 / (s + 1):.0f}", flush=True)
