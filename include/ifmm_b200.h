@@ -94,6 +94,17 @@ int ifmm_factor_timings(void* factor, double* out, int n_out);
  * order), host or device pointers.                                         */
 int ifmm_solve(void* factor, const double* b, double* x, int on_device);
 
+/* Morton-range partitioned h2_matvec, one rank's share (no reference
+ * counterpart: krylov.py:119-159 is single-process).  Device pointers in tree
+ * order; the rank owns points [p_lo, p_hi) (whole leaves).  phase 0 writes the
+ * partial multipoles of every cluster meeting the range into yv (length
+ * ifmm_h2_multipole_size, zero-initialised by the caller, summed over ranks
+ * by the caller); phase 1 reads the summed yv and the full xs (halo) and
+ * writes the rows [p_lo, p_hi) of ys. */
+int ifmm_h2_multipole_size(void* h2, long long* out);
+int ifmm_h2_matvec_part(void* h2, const double* xs, double* ys, double* yv, int phase,
+                        long long p_lo, long long p_hi);
+
 /* ---- exact dense matvec:  dense.py:23-32 / experiments.py:157-162 ------
  * y = A x, A_ij = K(|p_i - p_j|) evaluated on the fly (no storage), points
  * and vectors in the same (any) order.  Used for the residual criterion. */

@@ -40,6 +40,8 @@ _SIGS = {
     "ifmm_h2_weights": (C.c_int, [vp]),
     "ifmm_h2_block": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, ip, ip]),
     "ifmm_h2_matvec": (C.c_int, [vp, vp, vp, C.c_int]),
+    "ifmm_h2_multipole_size": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
+    "ifmm_h2_matvec_part": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_longlong, C.c_longlong]),
     "ifmm_graph_build": (vp, [vp, C.c_int]),
     "ifmm_graph_destroy": (None, [vp]),
     "ifmm_graph_info": (C.c_int, [vp, lp, lp, lp]),

@@ -268,6 +268,28 @@ int ifmm_h2_matvec(void* p, const double* x, double* y, int on_device) {
   ABI_CATCH
 }
 
+// Morton-range partitioned h2_matvec: one rank's share, device
+// pointers in tree (sorted) order; see H2::matvec_part.
+int ifmm_h2_multipole_size(void* p, long long* out) {
+  ABI_TRY
+  *out = ((H2*)p)->multipole_size();
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_h2_matvec_part(void* p, const double* xs, double* ys, double* yv, int phase, long long p_lo,
+                        long long p_hi) {
+  ABI_TRY
+  H2* h = (H2*)p;
+  if (h->consumed) throw Error(E_VALUE, "operators were consumed by a graph");
+  if (phase != 0 && phase != 1) throw Error(E_VALUE, "phase must be 0 or 1");
+  if (p_lo < 0 || p_hi > h->tree->n_points || p_lo > p_hi) throw Error(E_VALUE, "bad point range");
+  h->matvec_part(xs, ys, yv, phase, p_lo, p_hi);
+  h->ctx->sync();
+  return 0;
+  ABI_CATCH
+}
+
 // ---- graph ------------------------------------------------------------------
 void* ifmm_graph_build(void* h2, int consume) {
   ABI_TRY

@@ -57,6 +57,10 @@ struct H2 {
   void build();
   void weights();
   void matvec(const double* d_x_sorted, double* d_y_sorted);
+  // Morton-range partitioned matvec (one rank's share), see h2.cu
+  long long multipole_size() const;
+  void matvec_part(const double* d_x_sorted, double* d_y_sorted, double* d_yv, int phase,
+                   long long p_lo, long long p_hi);
 };
 
 // ---- extended graph (graph.py:30-216) ------------------------------------

@@ -468,4 +468,112 @@ void H2::matvec(const double* xs, double* ys) {
   C.flush();
 }
 
+// ---------------------------------------------------------------------------
+// Morton-range partitioned h2_matvec (one rank's share).  A rank
+// owns the points [p_lo, p_hi) of the tree order (whole leaves).
+//   phase 0: partial multipoles y of every cluster whose point range meets
+//            the rank's range (leaves: own only; parents: sum over children,
+//            out-of-range children contribute their -- zero -- local y).
+//            The caller sums yv over ranks (NCCL all-reduce).
+//   phase 1: locals z of the clusters meeting the range from the full y
+//            (M2L) and the parent's z (L2L, the parent meets the range too),
+//            then the rows of the own leaves: L2P + P2P over the neighbour
+//            leaves' x (xs must be the full sorted vector: the halo).  Rows
+//            outside the range are left untouched.
+// yv: device vector of length multipole_size(), offsets by cluster id.
+long long H2::multipole_size() const {
+  long long tot = 0;
+  for (int c = 0; c < tree->nc; ++c)
+    if (rank[c] > 0 && tree->level[c] >= 2) tot += rank[c];
+  return tot;
+}
+
+void H2::matvec_part(const double* xs, double* ys, double* yvp, int phase, long long p_lo,
+                     long long p_hi) {
+  Ctx& C = *ctx;
+  Tree& T = *tree;
+  std::vector<long long> off(T.nc, -1);
+  long long tot = 0;
+  for (int c = 0; c < T.nc; ++c)
+    if (rank[c] > 0 && T.level[c] >= 2) { off[c] = tot; tot += rank[c]; }
+  auto meets = [&](int c) { return T.start[c] < p_hi && T.stop[c] > p_lo; };
+  auto run = [&](std::vector<SpmvRow>& rows, std::vector<SpmvTerm>& terms) {
+    if (rows.empty()) return;
+    SpmvTerm* dt = C.stage.push_vec(C, terms);
+    SpmvRow* dr = C.stage.push_vec(C, rows);
+    launch_spmv(dr, (int)rows.size(), dt, 1, 1, C.st);
+    rows.clear(); terms.clear();
+  };
+  std::vector<SpmvRow> rows;
+  std::vector<SpmvTerm> terms;
+  const bool has_far = T.depth >= 2;
+  if (phase == 0) {
+    if (!has_far) return;
+    for (int c : T.leaves()) {
+      if (!(T.start[c] >= p_lo && T.stop[c] <= p_hi) || off[c] < 0) continue;
+      SpmvRow r{yvp + off[c], rank[c], (int)terms.size(), 1, 0};
+      terms.push_back({leaf_v[c].p, leaf_v[c].r, leaf_v[c].c, leaf_v[c].c, 1, xs + T.start[c]});
+      rows.push_back(r);
+    }
+    run(rows, terms);
+    for (int l = T.depth - 1; l >= 2; --l) {
+      for (int p : T.levels[l]) {
+        if (!meets(p) || off[p] < 0) continue;
+        SpmvRow r{yvp + off[p], rank[p], (int)terms.size(), 0, 0};
+        for (int c : T.children[p]) {
+          if (!meets(c) || off[c] < 0) continue;
+          terms.push_back({tvt[c].p, tvt[c].r, tvt[c].c, tvt[c].c, 0, yvp + off[c]});
+          r.nt++;
+        }
+        rows.push_back(r);
+      }
+      run(rows, terms);
+    }
+    CUDA_CHECK(cudaGetLastError());
+    C.flush();
+    return;
+  }
+  Blk zv = C.alloc(1, (int)std::max<long long>(tot, 1));
+  if (has_far) {
+    for (int l = 2; l <= T.depth; ++l) {
+      for (int c : T.levels[l]) {
+        if (!meets(c) || off[c] < 0) continue;
+        SpmvRow r{zv.p + off[c], rank[c], (int)terms.size(), 0, 0};
+        for (int q : T.inters[c]) {
+          if (off[q] < 0) continue;
+          const Blk& K = coupling.at(key2(c, q));
+          terms.push_back({K.p, K.r, K.c, K.c, 0, yvp + off[q]});
+          r.nt++;
+        }
+        if (l > 2) {
+          const int p = T.parent[c];
+          terms.push_back({tu[c].p, tu[c].r, tu[c].c, tu[c].c, 0, zv.p + off[p]});
+          r.nt++;
+        }
+        rows.push_back(r);
+      }
+      run(rows, terms);
+    }
+  }
+  for (int c : T.leaves()) {
+    if (!(T.start[c] >= p_lo && T.stop[c] <= p_hi)) continue;
+    const int m = T.stop[c] - T.start[c];
+    SpmvRow r{ys + T.start[c], m, (int)terms.size(), 0, 0};
+    for (int q : T.nbrs[c]) {
+      const Blk& S = near.at(key2(c, q));
+      terms.push_back({S.p, S.r, S.c, S.c, 0, xs + T.start[q]});
+      r.nt++;
+    }
+    if (has_far && off[c] >= 0) {
+      terms.push_back({leaf_u[c].p, leaf_u[c].r, leaf_u[c].c, leaf_u[c].c, 0, zv.p + off[c]});
+      r.nt++;
+    }
+    rows.push_back(r);
+  }
+  run(rows, terms);
+  C.free(zv);
+  CUDA_CHECK(cudaGetLastError());
+  C.flush();
+}
+
 }  // namespace ifmm
