@@ -792,7 +792,7 @@ void union_profile(unsigned long long* out, int reset) {
 
 namespace {
 constexpr int UNION_SMEM_DOUBLES = 28500;  // 228 KB
-constexpr int UNION_SVD_SMEM_DOUBLES = 28000;  // + 6 KB static
+constexpr int UNION_SVD_SMEM_DOUBLES = 28900;  // 231 KB
 
 // Interleaved Householder QR of two column-major matrices A (ra x s) and
 // B (rb x s): two barriers per column for both.  On exit: R in the upper
@@ -1101,7 +1101,11 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     // shared memory on the smem variant, and on the global variant too when
     // m x C fits (the rest of the workspace stays in global memory).
     double* Mw = SM ? smem : d.work;  // compile-time space: LDS/STS on the smem path
-    const bool msm = !SM && (size_t)m * C <= (size_t)smem_doubles;
+    // global variant: the ACA's per-step vectors (pivot column, pivot row /
+    // piv) and the active-column list live in shared memory after the
+    // residual (when that fits) -- they are read for every residual entry
+    const size_t scr_d = (size_t)m + C + C + 8;  // cc, rr, acts+pos (ints)
+    const bool msm = !SM && (size_t)m * C + scr_d <= (size_t)smem_doubles;
     double* M = msm ? smem : Mw;
     const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
     double* Acol = Mw + mreg;
@@ -1115,6 +1119,15 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     int* order = (int*)(sig + smax);
     int* acts = order + smax + 1;
     int* pos = acts + C;
+    double* ccs = nullptr;  // on-chip copies of the current pivot column / row (global variant)
+    double* rrs = nullptr;
+    if (!SM) {
+      double* scr = smem + (msm ? (size_t)m * C : 0);
+      ccs = scr;
+      rrs = scr + m;
+      acts = (int*)(rrs + C);
+      pos = acts + C;
+    }
 
     // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
     // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
@@ -1170,11 +1183,16 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       // (the pivot entry itself is cleared after the barrier: every thread
       // reads it above)
       for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        cc[i] = M[(size_t)q * m + i];
+        const double v = M[(size_t)q * m + i];
+        cc[i] = v;
+        if (!SM) ccs[i] = v;
         if (i != p) M[(size_t)q * m + i] = 0.0;
       }
-      for (int j = threadIdx.x; j < C; j += blockDim.x)
-        rr[j] = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
+      for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        const double v = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
+        rr[j] = v;
+        if (!SM) rrs[j] = v;
+      }
       if (threadIdx.x == 0) {  // swap-remove q from the active list
         const int k = pos[q], last = acts[nact - 1];
         if (k < 0 || k >= nact || acts[k] != q) {
@@ -1242,7 +1260,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
 #pragma unroll
           for (int u = 0; u < UN; ++u) {
             if (jj[u] < 0) break;
-            v[u] = fma(-cc[ii[u]], rr[jj[u]], v[u]);
+            v[u] = fma(-ccs[ii[u]], rrs[jj[u]], v[u]);
             M[(size_t)jj[u] * m + ii[u]] = v[u];
             const double av = fabs(v[u]);
             if (better(av, ii[u], jj[u])) { bv = av; bi = ii[u]; bj = jj[u]; }
@@ -1257,7 +1275,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       if (threadIdx.x == 0) {
         *d.rank = 0;
         double* gW = d.work + mreg + (size_t)m * smax + 2 * (size_t)C * smax;
-        *(int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax) = 0;  // header: s = 0
+        *(int*)(gW + 2 * (size_t)smax * smax) = 0;  // header: s = 0
       }
       __syncthreads();
       continue;
@@ -1368,8 +1386,9 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
         for (long long e = threadIdx.x; e < (long long)C * s; e += blockDim.x) gQB[e] = QBsrc[e];
       if (Wc != gW)
         for (int e = threadIdx.x; e < s * s; e += blockDim.x) gW[e] = Wc[e];
+      __syncthreads();  // W formation read Dp
       if (threadIdx.x == 0) {
-        int* hdr = (int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax);  // the order slot
+        int* hdr = (int*)(gW + 2 * (size_t)smax * smax);  // the (dead) pivot slot
         hdr[0] = s;
       }
     }
@@ -1407,8 +1426,6 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
 __global__ void __launch_bounds__(512)
 union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_doubles) {
   extern __shared__ double smem[];
-  __shared__ double sig_s[512];
-  __shared__ int order_s[512];
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const UnionDesc d = descs[bb];
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
@@ -1418,7 +1435,9 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     const double* gQA = d.work + mreg;
     const double* gQB = gQA + (size_t)m * smax;
     double* gW = (double*)gQB + 2 * (size_t)C * smax;
-    const int s = *(const int*)(gW + 2 * (size_t)smax * smax + 4 * (size_t)smax);
+    const int s = *(const int*)(gW + 2 * (size_t)smax * smax);
+    double* sig = gW + 2 * (size_t)smax * smax + smax;           // tauA slot
+    int* order = (int*)(gW + 2 * (size_t)smax * smax + 2 * (size_t)smax);  // tauB slot
     if (s == 0) continue;  // rank 0 already written by the first half
     unsigned long long t3 = clock64();
     double* Wc = (size_t)s * s <= (size_t)smem_doubles ? smem : gW;
@@ -1428,8 +1447,6 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     __syncthreads();
     const int nsw = cta_jacobi_wv(Wc, Vc, s);
     unsigned long long t35 = clock64();
-    double* sig = sig_s;
-    int* order = order_s;
     cta_sv_order(Wc, s, s, s, sig, order);
     unsigned long long t4 = clock64();
     int kk = 0;
