@@ -225,9 +225,12 @@ struct Eliminator {
         mc = std::max(mc, reqs[i].bu->k_old + reqs[i].bu->k_f);
         mk = std::max(mk, hr[i]);
       }
-      fprintf(ulog, "%zu %zu %d %d %d %.3f %.3f\n", us.size(), ug.size(), mm, mc, mk,
+      static auto prev = tl0;
+      fprintf(ulog, "%zu %zu %d %d %d %.3f %.3f %.3f\n", us.size(), ug.size(), mm, mc, mk,
               std::chrono::duration<double, std::milli>(tl2 - tl1).count(),
-              std::chrono::duration<double, std::milli>(tl1 - tl0).count());
+              std::chrono::duration<double, std::milli>(tl1 - tl0).count(),
+              std::chrono::duration<double, std::milli>(tl0 - prev).count());
+      prev = tl2;
     }
     for (size_t i = 0; i < reqs.size(); ++i) {
       reqs[i].bu->rank = hr[i];
