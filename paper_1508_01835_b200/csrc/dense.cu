@@ -13,6 +13,8 @@
 // many matrices per launch.
 #include "common.cuh"
 #include "dense.h"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #include <cstdio>
 #include <cstdlib>
@@ -1440,12 +1442,14 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     int* order = (int*)(gW + 2 * (size_t)smax * smax + 2 * (size_t)smax);  // tauB slot
     if (s == 0) continue;  // rank 0 already written by the first half
     unsigned long long t3 = clock64();
-    double* Wc = (size_t)s * s <= (size_t)smem_doubles ? smem : gW;
-    double* Vc = 2 * (size_t)s * s <= (size_t)smem_doubles ? smem + (size_t)s * s : gW + (size_t)s * s;
+    double* Wc = (!d.giant && (size_t)s * s <= (size_t)smem_doubles) ? smem : gW;
+    double* Vc = (!d.giant && 2 * (size_t)s * s <= (size_t)smem_doubles) ? smem + (size_t)s * s
+                                                                          : gW + (size_t)s * s;
     if (Wc != gW)
       for (int e = threadIdx.x; e < s * s; e += blockDim.x) Wc[e] = gW[e];
     __syncthreads();
-    const int nsw = cta_jacobi_wv(Wc, Vc, s);
+    // giant unions: the multi-CTA Jacobi (union_jacobi_coop) already ran
+    const int nsw = d.giant ? 0 : cta_jacobi_wv(Wc, Vc, s);
     unsigned long long t35 = clock64();
     cta_sv_order(Wc, s, s, s, sig, order);
     unsigned long long t4 = clock64();
@@ -1505,6 +1509,143 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
 }
 }  // namespace
 
+namespace {
+// Multi-CTA one-sided Jacobi for the cores of giant unions (s > 160: the
+// level-2 unions of c3/c4 reach s ~ 400).  One cooperative launch covers
+// every giant union of a pair wave, gper CTAs per union; W and V stay in
+// global memory (L2-resident).  The rounds, pairs and per-pair arithmetic are
+// those of cta_jacobi_wv (one warp per pair, 16 rows per lane in registers,
+// streamed tail beyond), so the result is bitwise the single-CTA one; a grid
+// barrier separates the rounds.  flags[u * 64 + sweep] collects "not yet
+// converged" per union and sweep.
+__global__ void __launch_bounds__(256)
+union_jacobi_coop(const UnionDesc* __restrict__ descs, int n, int gper, unsigned* flags, int max_m1) {
+  cg::grid_group grid = cg::this_grid();
+  const int u = blockIdx.x / gper, bl = blockIdx.x % gper;
+  const UnionDesc d = descs[u < n ? u : n - 1];
+  const int m = d.m, C = d.k_old + d.k_f;
+  const int smax = m < C ? m : C;
+  const int spx = smax + (smax & 1);
+  const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+  double* gW = d.work + mreg + (size_t)m * smax + 2 * (size_t)C * smax;
+  const int s = u < n ? *(const int*)(gW + 2 * (size_t)smax * smax) : 0;
+  double* W = gW;
+  double* V = gW + (size_t)s * s;
+  for (int e = bl * blockDim.x + threadIdx.x; e < s * s; e += gper * blockDim.x) {
+    const int j = e / s, i = e - j * s;
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  const double tol_rot = kEps;
+  const double tol_conv = fmax(kEps * (double)(s > 4 ? s : 4), 1e-13);
+  const double tr2 = tol_rot * tol_rot, tc2 = tol_conv * tol_conv;
+  const int cp = s + (s & 1), half = cp >> 1, m1 = cp - 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  constexpr int T = 32, NE = 16;
+  bool live = s >= 2;
+  grid.sync();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool again = false;
+    for (int r = 0; r < max_m1; ++r) {
+      if (live && r < m1)
+        for (int pi = bl * nwb + warp; pi < half; pi += gper * nwb) {
+          int p, q;
+          if (pi == 0) { p = r; q = m1; }
+          else { p = (r + pi) % m1; q = (r - pi + m1) % m1; }
+          const int lo = p < q ? p : q, hi = p < q ? q : p;
+          if (hi >= s) continue;  // warp-uniform
+          double* x = W + (size_t)lo * s;
+          double* y = W + (size_t)hi * s;
+          double xr[NE], yr[NE];
+          double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int i = lane + e * T;
+            xr[e] = i < s ? x[i] : 0.0;
+            yr[e] = i < s ? y[i] : 0.0;
+            a = fma(xr[e], xr[e], a); b = fma(yr[e], yr[e], b); g = fma(xr[e], yr[e], g);
+          }
+          for (int i = lane + NE * T; i < s; i += T) {
+            const double uu = x[i], vv = y[i];
+            a = fma(uu, uu, a); b = fma(vv, vv, b); g = fma(uu, vv, g);
+          }
+          a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
+          const double ab = a * b, g2 = g * g;
+          if (g != 0.0 && g2 > tr2 * ab) {
+            const double dd = b - a, gg = 2.0 * g;
+            const double t = copysign(fabs(gg), dd * gg) / (fabs(dd) + sqrt(fma(dd, dd, gg * gg)));
+            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+              const int i = lane + e * T;
+              if (i < s) {
+                x[i] = fma(c, xr[e], -sn * yr[e]);
+                y[i] = fma(sn, xr[e], c * yr[e]);
+              }
+            }
+            for (int i = lane + NE * T; i < s; i += T) {
+              const double uu = x[i], vv = y[i];
+              x[i] = fma(c, uu, -sn * vv);
+              y[i] = fma(sn, uu, c * vv);
+            }
+            double* vx = V + (size_t)lo * s;
+            double* vy = V + (size_t)hi * s;
+            for (int i0 = lane; i0 < s; i0 += 4 * T) {
+              double uu[4], vv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = i0 + e * T;
+                uu[e] = i < s ? vx[i] : 0.0;
+                vv[e] = i < s ? vy[i] : 0.0;
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = i0 + e * T;
+                if (i < s) {
+                  vx[i] = fma(c, uu[e], -sn * vv[e]);
+                  vy[i] = fma(sn, uu[e], c * vv[e]);
+                }
+              }
+            }
+            again |= g2 > tc2 * ab;
+          }
+        }
+      grid.sync();
+    }
+    if (again && lane == 0) atomicOr(&flags[u * 64 + sweep], 1u);
+    grid.sync();
+    bool any = false;
+    for (int v = 0; v < n; ++v) {
+      const bool lv = flags[v * 64 + sweep] != 0u;
+      if (v == u) live = live && lv;
+      any |= lv;
+    }
+    if (!any) {
+      if (bl == 0 && threadIdx.x == 0 && u < n) atomicAdd(&g_uprof[14], (unsigned long long)(sweep + 1));
+      break;
+    }
+  }
+}
+}  // namespace
+
+void launch_union_jacobi_coop(const UnionDesc* d_descs, int n, int max_s, unsigned* d_flags,
+                              cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_union_jacobi_coop"};
+  if (n <= 0) return;
+  int per = 148 / n;
+  const int half = (max_s + 1) / 2;
+  const int need = (half + 7) / 8;  // 8 warps (pairs) per CTA and round
+  if (per > need) per = need;
+  if (per < 1) per = 1;
+  int max_m1 = max_s + (max_s & 1) - 1;
+  cudaMemsetAsync(d_flags, 0, sizeof(unsigned) * 64 * (size_t)n, s);
+  void* args[] = {(void*)&d_descs, (void*)&n, (void*)&per, (void*)&d_flags, (void*)&max_m1};
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel((void*)union_jacobi_coop, dim3(per * n), dim3(256), args, 0, s);
+  if (e != cudaSuccess) {  // surfaces through the caller's cudaGetLastError check
+    fprintf(stderr, "[ifmm] cooperative Jacobi launch failed: %s\n", cudaGetErrorString(e));
+  }
+}
+
 bool union_fits_smem(int m, int k_old, int k_f) {
   return union_work_doubles(m, k_old, k_f) <= (size_t)UNION_SMEM_DOUBLES;
 }
@@ -1512,7 +1653,8 @@ bool union_fits_smem(int m, int k_old, int k_f) {
 // smem != 0: every desc's workspace fits shared memory (caller partitions);
 // smem == 0: workspaces in global memory with the full L1 as cache.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
-                  int jac_smem_doubles) {
+                  int jac_smem_doubles, const UnionDesc* d_giants, int n_giants, int max_giant_s,
+                  unsigned* d_flags) {
   DbgSync dbg_sync_{s, "launch_union"};
   if (n <= 0) return;
   static bool attr = false;
@@ -1552,6 +1694,7 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     const int jd = UNION_SMEM_DOUBLES;
     union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
+  if (n_giants > 0) launch_union_jacobi_coop(d_giants, n_giants, max_giant_s, d_flags, s);
   union_svd_kernel<<<n < 4096 ? n : 4096, 512, (size_t)UNION_SVD_SMEM_DOUBLES * 8, s>>>(
       d_descs, n, thr, UNION_SVD_SMEM_DOUBLES);
 }

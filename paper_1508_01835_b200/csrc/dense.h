@@ -68,6 +68,7 @@ struct UnionDesc {
   double* FM;
   int* rank;
   double* work;
+  int giant;  // set by the launcher: core SVD by the multi-CTA Jacobi
 };
 
 __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f);
@@ -85,8 +86,13 @@ void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim,
 bool union_fits_smem(int m, int k_old, int k_f);
 // smem: all workspaces fit shared memory; otherwise jac_smem_doubles (<= 28500)
 // of dynamic shared memory hold the core SVD when 2 s^2 fits.
+// d_giants / n_giants: the subset (giant != 0) whose core SVD runs on several
+// CTAs (cooperative launch between the two halves); d_flags: 64 uints per giant.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
-                  int jac_smem_doubles = 0);
+                  int jac_smem_doubles = 0, const UnionDesc* d_giants = nullptr, int n_giants = 0,
+                  int max_giant_s = 0, unsigned* d_flags = nullptr);
+// s_max above which a union is "giant" (multi-CTA core SVD)
+constexpr int kGiantUnion = 160;
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to

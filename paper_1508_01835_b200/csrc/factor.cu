@@ -188,15 +188,28 @@ struct Eliminator {
     }
     Phase ph(C, PH_UNION);
     std::vector<UnionDesc> us, ug;  // shared-memory vs global-workspace unions
+    std::vector<UnionDesc> giants;  // global-workspace unions with a multi-CTA core SVD
     int jsd = 0;                    // shared memory for the large unions' core SVD
+    int max_gs = 0;
     for (auto& u : ud) {
-      if (union_fits_smem(u.m, u.k_old, u.k_f)) { us.push_back(u); continue; }
-      ug.push_back(u);
       const int sm = std::min(u.m, u.k_old + u.k_f);
+      u.giant = 0;
+      if (union_fits_smem(u.m, u.k_old, u.k_f)) { us.push_back(u); continue; }
+      if (sm > kGiantUnion) {
+        u.giant = 1;
+        giants.push_back(u);
+        max_gs = std::max(max_gs, sm);
+      }
+      ug.push_back(u);
       if (2 * sm * sm <= 28500) jsd = std::max(jsd, 2 * sm * sm);
     }
     UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
+    UnionDesc* dgi = giants.empty() ? nullptr : C.stage.push_vec(C, giants);
+    Blk gflags;
+    if (!giants.empty()) gflags = C.alloc(1, 32 * (int)giants.size());
+    unsigned* dfl = giants.empty() ? nullptr : reinterpret_cast<unsigned*>(gflags.p);
+    const int ngi = (int)giants.size();
     cudaEvent_t ka = nullptr;
     static FILE* ulog = nullptr;
     static bool ulog_init = false;
@@ -210,9 +223,11 @@ struct Eliminator {
     C.kt_begin(K_UNION, uflops, &ka);
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
-              [&](cudaStream_t s) { launch_union(dug, (int)ug.size(), thr, s, 0, jsd); });
+              [&](cudaStream_t s) {
+                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl);
+              });
     else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
-    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd);
+    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd, dgi, ngi, max_gs, dfl);
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
@@ -236,6 +251,7 @@ struct Eliminator {
       reqs[i].bu->rank = hr[i];
       C.free(reqs[i].bu->W);
     }
+    if (!giants.empty()) C.free(gflags);
   }
 
   void make_identity(BU& b, int m, int k, const Blk& w) {

@@ -158,3 +158,34 @@ def test_exact_matvec_matches_dense(N):
         A = K.block(pts, pts)
         y = P.exact_matvec(pts, K, x)
         np.testing.assert_allclose(y, A @ x, rtol=1e-11, atol=1e-11 * np.abs(A @ x).max())
+
+
+def test_union_giant_matches_oracle(N):
+    """A union whose core (s > 160) runs the multi-CTA cooperative Jacobi."""
+    from oracle import ifmm_np as O
+    rng = np.random.default_rng(11)
+    m, ko, kf = 420, 190, 24
+    B, _ = np.linalg.qr(rng.standard_normal((m, ko)))
+    F, _ = np.linalg.qr(rng.standard_normal((m, kf)))
+    w = np.sort(10.0 ** (-7 * rng.random(ko)))[::-1]
+    wf = np.sort(10.0 ** (-7 * rng.random(kf)))[::-1] * 0.5
+    thr = 1e-6 * w[0]
+    ref = O.basis_union(B, w, F, wf, thr)
+    assert min(m, ko + kf) > 160
+    cap = min(m, ko + kf)
+    dB, dw, dF, dwf = _dev(B), _dev(w), _dev(F), _dev(wf)
+    NB = torch.zeros(m * cap, dtype=torch.float64, device="cuda")
+    NW = torch.zeros(cap, dtype=torch.float64, device="cuda")
+    OM = torch.zeros(cap * ko, dtype=torch.float64, device="cuda")
+    FM = torch.zeros(cap * kf, dtype=torch.float64, device="cuda")
+    dr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().ifmm_dev_union(N.ctx(), m, ko, kf, _p(dB), _p(dw), _p(dF), _p(dwf), thr, 0,
+                                   _p(NB), _p(NW), _p(OM), _p(FM), _p(dr)))
+    r = int(dr.item())
+    assert r == ref.rank
+    nb = NB.cpu().numpy()[:m * r].reshape(r, m).T
+    np.testing.assert_allclose(NW.cpu().numpy()[:r], ref.weights, rtol=1e-10, atol=1e-13 * w[0])
+    om = OM.cpu().numpy()[:r * ko].reshape(r, ko)
+    fm = FM.cpu().numpy()[:r * kf].reshape(r, kf)
+    np.testing.assert_allclose(nb @ om, ref.basis @ ref.old_map, atol=1e-9)
+    np.testing.assert_allclose(nb @ fm, ref.basis @ ref.fill_map, atol=1e-9)
