@@ -562,9 +562,9 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
   const bool fits = union_fits_smem(m, k_old, k_f);
   d[0].giant = (!fits && smax > kGiantUnion) ? 1 : 0;
   UnionDesc* dd = C.stage.push_vec(C, d);
-  Blk fl = C.alloc(1, 32);
+  Blk fl = C.alloc(1, union_giant_scratch_doubles(1));
   launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant ? dd : nullptr, d[0].giant,
-               smax, reinterpret_cast<unsigned*>(fl.p));
+               smax, fl.p, m, k_old + k_f);
   C.free(fl);
   CUDA_CHECK(cudaGetLastError());
   C.sync();

@@ -906,9 +906,14 @@ constexpr double kCholFloor = 1e-12;
 
 // Upper triangles of G_A = A^T A and G_B = B^T B (A: ra x s, B: rb x s,
 // col-major), row-major with ld sp.  One warp per 4x4 tile, lanes split rows.
+// wbase / wstride: this CTA's first warp index and the warp stride over the
+// tiles (one CTA: 0 / warps per CTA; several CTAs share the tiles otherwise)
 __device__ __forceinline__ void cta_gram2(const double* A, int ra, const double* B, int rb, int s,
-                                          int sp, double* GA, double* GB) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                                          int sp, double* GA, double* GB, int wbase = 0,
+                                          int wstride = 0) {
+  const int lane = threadIdx.x & 31;
+  const int warp = wbase + (threadIdx.x >> 5);
+  const int nw = wstride > 0 ? wstride : (blockDim.x >> 5);
   const int nb = (s + 3) >> 2, ntile = nb * (nb + 1) / 2;
   for (int t = warp; t < 2 * ntile; t += nw) {
     const bool isA = t < ntile;
@@ -1032,8 +1037,9 @@ __device__ __forceinline__ double cta_chol2(double* GA, double* ia, double* GB, 
 // rinv = 1 / diag), both matrices at once; 8-column register blocks.
 __device__ __forceinline__ void cta_trsm2(double* A, int ra, const double* RA, const double* ia,
                                           double* B, int rb, const double* RB, const double* ib,
-                                          int s, int sp) {
-  for (int row = threadIdx.x; row < ra + rb; row += blockDim.x) {
+                                          int s, int sp, int tbase = 0, int tstride = 0) {
+  const int t0 = tbase + threadIdx.x, ts = tstride > 0 ? tstride : blockDim.x;
+  for (int row = t0; row < ra + rb; row += ts) {
     const bool isA = row < ra;
     double* X = isA ? A : B;
     const int r = isA ? ra : rb, rr = isA ? row : row - ra;
@@ -1073,8 +1079,10 @@ __device__ __forceinline__ void cta_trsm2(double* A, int ra, const double* RA, c
 
 // T = R2 R1 (row-major upper, ld sp) for two pairs at once.
 __device__ __forceinline__ void cta_trmul2(const double* A2, const double* A1, double* TA, const double* B2,
-                                           const double* B1, double* TB, int s, int sp) {
-  for (int e = threadIdx.x; e < 2 * s * s; e += blockDim.x) {
+                                           const double* B1, double* TB, int s, int sp,
+                                           int tbase = 0, int tstride = 0) {
+  const int t0 = tbase + threadIdx.x, ts = tstride > 0 ? tstride : blockDim.x;
+  for (int e = t0; e < 2 * s * s; e += ts) {
     const bool isA = e < s * s;
     const int f = isA ? e : e - s * s;
     const int i = f / s, j = f - i * s;
@@ -1131,146 +1139,157 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       pos = acts + C;
     }
 
-    // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
-    // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
-    // column groups over the list of active (unpivoted) columns; the flat
-    // (row-major, numpy) index only breaks exact ties.
-    const int R = m < (int)blockDim.x ? m : (int)blockDim.x;
-    const int G = blockDim.x / R;
-    const int i0 = threadIdx.x % R, g0 = threadIdx.x / R;
-    const bool on = g0 < G;
-    double bv = -1.0;
-    int bi = 0, bj = 0;
-    auto better = [&](double av, int i, int j) {
-      return av > bv || (av == bv && (long long)i * C + j < (long long)bi * C + bj);
-    };
-    for (int j = threadIdx.x; j < C; j += blockDim.x) { acts[j] = j; pos[j] = j; }
-    int nact = C;  // every thread tracks the active count
-    if (on)
-      for (int i = i0; i < m; i += R)
-        for (int j = g0; j < C; j += G) {
-          const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
-                                  : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
-          M[(size_t)j * m + i] = v;
-          const double av = fabs(v);
-          if (better(av, i, j)) { bv = av; bi = i; bj = j; }
-        }
-    // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step.
-    // A pivoted column becomes exactly zero (its row factor entry is piv/piv
-    // = 1), so it leaves the active list; pivoted rows keep their rounding
-    // residue and stay, as in the reference.
-    unsigned long long t0 = clock64();
-    const double floor_ = thr / 8.0;
     int steps = 0;
-    for (int it = 0; it < smax; ++it) {
-      long long bflat = bv < 0.0 ? (1LL << 62) : (long long)bi * C + bj;
-      warp_argmax(bv, bflat);
-      if (lane == 0) { wv[warp] = bv; wi[warp] = bflat; }
-      __syncthreads();
-      double gv = lane < nw ? wv[lane] : -1.0;
-      long long gi = lane < nw ? wi[lane] : (1LL << 62);
-      warp_argmax(gv, gi);  // every lane of every warp: the block's pivot
-      const int p = (int)(gi / C), q = (int)(gi - (long long)p * C);
-      if (p < 0 || p >= m || q < 0 || q >= C) {
-        if (threadIdx.x == 0)
-          printf("[union] bad pivot m=%d C=%d step=%d nact=%d gi=%lld gv=%g\n", m, C, steps, nact, gi, gv);
-        __trap();
-      }
-      const double piv = M[(size_t)q * m + p];
-      if (piv == 0.0 || (fabs(piv) <= floor_ && steps >= d.min_rank)) break;  // uniform
-      double* cc = Acol + (size_t)steps * m;
-      double* rr = Bt + (size_t)steps * C;
-      // column q leaves the active list: its residual is exactly zero from
-      // here on (q's row factor entry is piv / piv = 1), stored as such
-      // (the pivot entry itself is cleared after the barrier: every thread
-      // reads it above)
-      for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const double v = M[(size_t)q * m + i];
-        cc[i] = v;
-        if (!SM) ccs[i] = v;
-        if (i != p) M[(size_t)q * m + i] = 0.0;
-      }
-      for (int j = threadIdx.x; j < C; j += blockDim.x) {
-        const double v = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
-        rr[j] = v;
-        if (!SM) rrs[j] = v;
-      }
-      if (threadIdx.x == 0) {  // swap-remove q from the active list
-        const int k = pos[q], last = acts[nact - 1];
-        if (k < 0 || k >= nact || acts[k] != q) {
-          printf("[union] bad active list m=%d C=%d step=%d nact=%d q=%d k=%d\n", m, C, steps, nact, q, k);
+    unsigned long long t0 = clock64();
+    bool giant_hh = false;
+    if (d.giant) {
+      // the ACA (union_aca_coop) and CholeskyQR (union_cholqr_coop) ran on
+      // several CTAs; only a Householder fallback (hdr[1]) or s = 0 is left here
+      const int* hg = (const int*)(Dp + 4 * (size_t)smax);
+      steps = hg[0];
+      if (steps > 0 && hg[1] == 0) continue;  // uniform per CTA
+      giant_hh = steps > 0;
+    } else {
+      // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
+      // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
+      // column groups over the list of active (unpivoted) columns; the flat
+      // (row-major, numpy) index only breaks exact ties.
+      const int R = m < (int)blockDim.x ? m : (int)blockDim.x;
+      const int G = blockDim.x / R;
+      const int i0 = threadIdx.x % R, g0 = threadIdx.x / R;
+      const bool on = g0 < G;
+      double bv = -1.0;
+      int bi = 0, bj = 0;
+      auto better = [&](double av, int i, int j) {
+        return av > bv || (av == bv && (long long)i * C + j < (long long)bi * C + bj);
+      };
+      for (int j = threadIdx.x; j < C; j += blockDim.x) { acts[j] = j; pos[j] = j; }
+      int nact = C;  // every thread tracks the active count
+      if (on)
+        for (int i = i0; i < m; i += R)
+          for (int j = g0; j < C; j += G) {
+            const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
+                                    : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+            M[(size_t)j * m + i] = v;
+            const double av = fabs(v);
+            if (better(av, i, j)) { bv = av; bi = i; bj = j; }
+          }
+      // ---- ACA, full pivoting, floor thr/8 (lowrank.py:128-151): 2 barriers/step.
+      // A pivoted column becomes exactly zero (its row factor entry is piv/piv
+      // = 1), so it leaves the active list; pivoted rows keep their rounding
+      // residue and stay, as in the reference.
+      t0 = clock64();
+      const double floor_ = thr / 8.0;
+      for (int it = 0; it < smax; ++it) {
+        long long bflat = bv < 0.0 ? (1LL << 62) : (long long)bi * C + bj;
+        warp_argmax(bv, bflat);
+        if (lane == 0) { wv[warp] = bv; wi[warp] = bflat; }
+        __syncthreads();
+        double gv = lane < nw ? wv[lane] : -1.0;
+        long long gi = lane < nw ? wi[lane] : (1LL << 62);
+        warp_argmax(gv, gi);  // every lane of every warp: the block's pivot
+        const int p = (int)(gi / C), q = (int)(gi - (long long)p * C);
+        if (p < 0 || p >= m || q < 0 || q >= C) {
+          if (threadIdx.x == 0)
+            printf("[union] bad pivot m=%d C=%d step=%d nact=%d gi=%lld gv=%g\n", m, C, steps, nact, gi, gv);
           __trap();
         }
-        acts[k] = last;
-        pos[last] = k;
-        Dp[steps] = piv;
-      }
-      --nact;
-      __syncthreads();
-      if (threadIdx.x == 0) M[(size_t)q * m + p] = 0.0;
-      const int na = nact;
-      bv = -1.0;
-      if (SM) {
-        if (on)
-          for (int i = i0; i < m; i += R) {
-            const double ci = cc[i];
-            int l = g0;
-            for (; l + 7 * G < na; l += 8 * G) {
-              int jj[8];
-              double v[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) { jj[u] = acts[l + u * G]; v[u] = M[(size_t)jj[u] * m + i]; }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                v[u] = fma(-ci, rr[jj[u]], v[u]);
-                M[(size_t)jj[u] * m + i] = v[u];
-                const double av = fabs(v[u]);
-                if (better(av, i, jj[u])) { bv = av; bi = i; bj = jj[u]; }
+        const double piv = M[(size_t)q * m + p];
+        if (piv == 0.0 || (fabs(piv) <= floor_ && steps >= d.min_rank)) break;  // uniform
+        double* cc = Acol + (size_t)steps * m;
+        double* rr = Bt + (size_t)steps * C;
+        // column q leaves the active list: its residual is exactly zero from
+        // here on (q's row factor entry is piv / piv = 1), stored as such
+        // (the pivot entry itself is cleared after the barrier: every thread
+        // reads it above)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const double v = M[(size_t)q * m + i];
+          cc[i] = v;
+          if (!SM) ccs[i] = v;
+          if (i != p) M[(size_t)q * m + i] = 0.0;
+        }
+        for (int j = threadIdx.x; j < C; j += blockDim.x) {
+          const double v = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
+          rr[j] = v;
+          if (!SM) rrs[j] = v;
+        }
+        if (threadIdx.x == 0) {  // swap-remove q from the active list
+          const int k = pos[q], last = acts[nact - 1];
+          if (k < 0 || k >= nact || acts[k] != q) {
+            printf("[union] bad active list m=%d C=%d step=%d nact=%d q=%d k=%d\n", m, C, steps, nact, q, k);
+            __trap();
+          }
+          acts[k] = last;
+          pos[last] = k;
+          Dp[steps] = piv;
+        }
+        --nact;
+        __syncthreads();
+        if (threadIdx.x == 0) M[(size_t)q * m + p] = 0.0;
+        const int na = nact;
+        bv = -1.0;
+        if (SM) {
+          if (on)
+            for (int i = i0; i < m; i += R) {
+              const double ci = cc[i];
+              int l = g0;
+              for (; l + 7 * G < na; l += 8 * G) {
+                int jj[8];
+                double v[8];
+  #pragma unroll
+                for (int u = 0; u < 8; ++u) { jj[u] = acts[l + u * G]; v[u] = M[(size_t)jj[u] * m + i]; }
+  #pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  v[u] = fma(-ci, rr[jj[u]], v[u]);
+                  M[(size_t)jj[u] * m + i] = v[u];
+                  const double av = fabs(v[u]);
+                  if (better(av, i, jj[u])) { bv = av; bi = i; bj = jj[u]; }
+                }
+              }
+              for (; l < na; l += G) {
+                const int j = acts[l];
+                double* mp = M + (size_t)j * m + i;
+                const double v = fma(-ci, rr[j], *mp);
+                *mp = v;
+                const double av = fabs(v);
+                if (better(av, i, j)) { bv = av; bi = i; bj = j; }
               }
             }
-            for (; l < na; l += G) {
-              const int j = acts[l];
-              double* mp = M + (size_t)j * m + i;
-              const double v = fma(-ci, rr[j], *mp);
-              *mp = v;
-              const double av = fabs(v);
-              if (better(av, i, j)) { bv = av; bi = i; bj = j; }
+        } else {
+          // global workspace: M streams through L2 every step.  The m x na
+          // active block is flattened (row fastest, coalesced) and dealt out
+          // evenly; every batch issues all UN loads before any store, also in
+          // the last partial batch (a load after a possibly aliasing store
+          // would serialise on the L2 round trip).
+          constexpr int UN = 16;
+          const int total = m * na, nthr = blockDim.x;
+          const int di = nthr % m, dl = nthr / m;
+          int f = threadIdx.x, i = f % m, l = f / m;
+          while (f < total) {
+            int ii[UN], jj[UN];
+            double v[UN];
+  #pragma unroll
+            for (int u = 0; u < UN; ++u) {
+              const bool ok = f + u * nthr < total;
+              ii[u] = i;
+              jj[u] = ok ? acts[l] : -1;
+              v[u] = ok ? M[(size_t)jj[u] * m + i] : 0.0;
+              i += di; l += dl;
+              if (i >= m) { i -= m; ++l; }
             }
+  #pragma unroll
+            for (int u = 0; u < UN; ++u) {
+              if (jj[u] < 0) break;
+              v[u] = fma(-ccs[ii[u]], rrs[jj[u]], v[u]);
+              M[(size_t)jj[u] * m + ii[u]] = v[u];
+              const double av = fabs(v[u]);
+              if (better(av, ii[u], jj[u])) { bv = av; bi = ii[u]; bj = jj[u]; }
+            }
+            f += UN * nthr;
           }
-      } else {
-        // global workspace: M streams through L2 every step.  The m x na
-        // active block is flattened (row fastest, coalesced) and dealt out
-        // evenly; every batch issues all UN loads before any store, also in
-        // the last partial batch (a load after a possibly aliasing store
-        // would serialise on the L2 round trip).
-        constexpr int UN = 16;
-        const int total = m * na, nthr = blockDim.x;
-        const int di = nthr % m, dl = nthr / m;
-        int f = threadIdx.x, i = f % m, l = f / m;
-        while (f < total) {
-          int ii[UN], jj[UN];
-          double v[UN];
-#pragma unroll
-          for (int u = 0; u < UN; ++u) {
-            const bool ok = f + u * nthr < total;
-            ii[u] = i;
-            jj[u] = ok ? acts[l] : -1;
-            v[u] = ok ? M[(size_t)jj[u] * m + i] : 0.0;
-            i += di; l += dl;
-            if (i >= m) { i -= m; ++l; }
-          }
-#pragma unroll
-          for (int u = 0; u < UN; ++u) {
-            if (jj[u] < 0) break;
-            v[u] = fma(-ccs[ii[u]], rrs[jj[u]], v[u]);
-            M[(size_t)jj[u] * m + ii[u]] = v[u];
-            const double av = fabs(v[u]);
-            if (better(av, ii[u], jj[u])) { bv = av; bi = ii[u]; bj = jj[u]; }
-          }
-          f += UN * nthr;
         }
+        ++steps;
       }
-      ++steps;
     }
     __syncthreads();
     if (steps == 0) {
@@ -1287,6 +1306,8 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     unsigned long long t1 = clock64();
     // ---- scale X columns by 1/pivot: L~ = X D^{-1} ----
     // thread per row, 8 columns per batch with all loads before the stores
+    // (giant unions: already scaled by union_cholqr_coop)
+    if (!d.giant)
     for (int i = threadIdx.x; i < m; i += blockDim.x)
       for (int t0 = 0; t0 < s; t0 += 8) {
         double v[8];
@@ -1311,13 +1332,13 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     double* ib = tauB;
     __syncthreads();
     double r1 = 0.0;
-    if (!force_hh) {
+    if (!force_hh && !giant_hh) {
       cta_gram2(Acol, m, Bt, C, s, sp, GA, GB);
       __syncthreads();
       r1 = cta_chol2(GA, ia, GB, ib, s, sp);
     }
     // cond(L~) or cond(Y) above ~1e6: Householder path instead
-    const bool hh = force_hh || !(r1 > kCholFloor);
+    const bool hh = force_hh || giant_hh || !(r1 > kCholFloor);
     const double* QAp;
     const double* QBp;
     // W = core^T (s x s): in shared memory on the global variant when it fits
@@ -1627,6 +1648,277 @@ union_jacobi_coop(const UnionDesc* __restrict__ descs, int n, int gper, unsigned
 }
 }  // namespace
 
+namespace {
+// Multi-CTA full-pivot ACA for giant unions (s > 160), one cooperative launch
+// for all giants of a pair wave, gper CTAs per union.  CTA bl owns a slab of
+// rows of the residual M (global memory, the union's workspace); per pivot
+// step: slab argmax -> global candidates -> grid barrier -> every CTA
+// derives the same pivot (max |value|, ties to the smallest row-major index,
+// as the single-CTA kernel and numpy) and copies the pivot row / piv and its
+// slab of the pivot column -> grid barrier -> slab update.  The arithmetic
+// is element for element that of union_kernel, so X, Y, D are bitwise the
+// same; union_kernel then skips its ACA for these unions.
+__global__ void __launch_bounds__(512)
+union_aca_coop(const UnionDesc* __restrict__ descs, int n, int gper, double thr, double* cand,
+               int* done_count, int max_smax) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sh[];
+  __shared__ double wv[32];
+  __shared__ long long wi[32];
+  const int u = blockIdx.x / gper, bl = blockIdx.x % gper;
+  const bool real = u < n;
+  const UnionDesc d = descs[real ? u : n - 1];
+  const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
+  const int smax = m < C ? m : C;
+  const int spx = smax + (smax & 1);
+  const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+  double* M = d.work;
+  double* Acol = M + mreg;
+  double* Bt = Acol + (size_t)m * smax;
+  double* core = Bt + 2 * (size_t)C * smax;
+  double* Dp = core + 2 * (size_t)smax * smax;
+  int* hdr = (int*)(Dp + 4 * (size_t)smax);  // s for union_kernel
+  const int rpc = (m + gper - 1) / gper;
+  const int r0 = bl * rpc, r1 = min(m, r0 + rpc), nr = max(0, r1 - r0);
+  double* rrs = sh;            // C
+  double* ccs = rrs + C;       // nr
+  int* acts = (int*)(ccs + rpc + 1);
+  int* pos = acts + C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double bv = -1.0;
+  int bi = 0, bj = 0;
+  auto better = [&](double av, int i, int j) {
+    return av > bv || (av == bv && (long long)i * C + j < (long long)bi * C + bj);
+  };
+  for (int j = threadIdx.x; j < C; j += blockDim.x) { acts[j] = j; pos[j] = j; }
+  // concat [B*diag(w) | F*diag(wf)] for the own rows + first local argmax
+  for (long long e = threadIdx.x; e < (long long)nr * C; e += blockDim.x) {
+    const int i = r0 + (int)(e % nr), j = (int)(e / nr);
+    const double v = j < ko ? d.B[(size_t)i * d.b_r + (size_t)j * d.b_c] * d.w[j]
+                            : d.F[(size_t)i * d.f_r + (size_t)(j - ko) * d.f_c] * d.wf[j - ko];
+    M[(size_t)j * m + i] = v;
+    if (better(fabs(v), i, j)) { bv = fabs(v); bi = i; bj = j; }
+  }
+  const double floor_ = thr / 8.0;
+  int steps = 0, nact = C;
+  bool done = !real;
+  for (int it = 0; it < max_smax; ++it) {
+    // ---- publish the slab candidate
+    long long bflat = bv < 0.0 ? (1LL << 62) : (long long)bi * C + bj;
+    warp_argmax(bv, bflat);
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bflat; }
+    __syncthreads();
+    if (warp == 0) {
+      double gv = lane < nw ? wv[lane] : -1.0;
+      long long gi = lane < nw ? wi[lane] : (1LL << 62);
+      warp_argmax(gv, gi);
+      if (lane == 0) {
+        cand[2 * (size_t)blockIdx.x] = gv;
+        reinterpret_cast<long long*>(cand)[2 * (size_t)blockIdx.x + 1] = gi;
+      }
+    }
+    grid.sync();
+    // ---- the union's pivot (identical in all of its CTAs)
+    int p = 0, q = 0;
+    double piv = 0.0;
+    if (!done) {
+      double gv = -1.0;
+      long long gi = (1LL << 62);
+      for (int b = lane; b < gper; b += 32) {
+        const double ov = cand[2 * (size_t)(u * gper + b)];
+        const long long oi = reinterpret_cast<const long long*>(cand)[2 * (size_t)(u * gper + b) + 1];
+        if (ov > gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+      }
+      warp_argmax(gv, gi);
+      p = (int)(gi / C);
+      q = (int)(gi - (long long)p * C);
+      if (it >= smax || gv < 0.0) done = true;
+      else {
+        piv = M[(size_t)q * m + p];
+        if (piv == 0.0 || (fabs(piv) <= floor_ && steps >= d.min_rank)) done = true;
+      }
+      if (done && bl == 0 && threadIdx.x == 0) { *hdr = steps; atomicAdd(done_count, 1); }
+    }
+    if (!done) {
+      for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const double v = M[(size_t)q * m + i];
+        ccs[i - r0] = v;
+        Acol[(size_t)steps * m + i] = v;
+        if (i != p) M[(size_t)q * m + i] = 0.0;
+      }
+      for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        const double v = j == q ? 1.0 : M[(size_t)j * m + p] / piv;
+        rrs[j] = v;
+        if (bl == 0) Bt[(size_t)steps * C + j] = v;
+      }
+      if (threadIdx.x == 0) {
+        const int k = pos[q], last = acts[nact - 1];
+        acts[k] = last;
+        pos[last] = k;
+        if (bl == 0) Dp[steps] = piv;
+      }
+      --nact;
+    }
+    grid.sync();  // every CTA has read row p / piv before the slabs change
+    if (*(volatile int*)done_count >= n) break;
+    if (done) continue;
+    if (threadIdx.x == 0 && p >= r0 && p < r1) M[(size_t)q * m + p] = 0.0;
+    __syncthreads();
+    bv = -1.0;
+    constexpr int UN = 16;
+    const int total = nr * nact, nthr = blockDim.x;
+    if (nr > 0) {
+      const int di = nthr % nr, dl = nthr / nr;
+      int f = threadIdx.x, i = f % nr, l = f / nr;
+      while (f < total) {
+        int ii[UN], jj[UN];
+        double v[UN];
+#pragma unroll
+        for (int uu = 0; uu < UN; ++uu) {
+          const bool ok = f + uu * nthr < total;
+          ii[uu] = i;
+          jj[uu] = ok ? acts[l] : -1;
+          v[uu] = ok ? M[(size_t)jj[uu] * m + r0 + i] : 0.0;
+          i += di; l += dl;
+          if (i >= nr) { i -= nr; ++l; }
+        }
+#pragma unroll
+        for (int uu = 0; uu < UN; ++uu) {
+          if (jj[uu] < 0) break;
+          v[uu] = fma(-ccs[ii[uu]], rrs[jj[uu]], v[uu]);
+          M[(size_t)jj[uu] * m + r0 + ii[uu]] = v[uu];
+          const double av = fabs(v[uu]);
+          if (better(av, r0 + ii[uu], jj[uu])) { bv = av; bi = r0 + ii[uu]; bj = jj[uu]; }
+        }
+        f += UN * nthr;
+      }
+    }
+    ++steps;
+  }
+  if (real && !done && bl == 0 && threadIdx.x == 0) *hdr = steps;  // ran to max_smax
+}
+}  // namespace
+
+namespace {
+// Multi-CTA CholeskyQR2 + core formation for giant unions, after
+// union_aca_coop: pivot scaling, Gram tiles and row-wise triangular solves
+// are spread over the union's CTAs, the two Cholesky factorisations run in its
+// first CTA, grid barriers in between.  Same arithmetic per element as
+// union_kernel (same tiles, same Cholesky, same per-row solves), so the
+// factors are bitwise those of the single-CTA path.  Writes QA / QB in place,
+// W = core^T and the hand-off header; flags the union for union_kernel's
+// Householder path when a Cholesky pivot ratio signals cond > ~1e6.
+__global__ void __launch_bounds__(512)
+union_cholqr_coop(const UnionDesc* __restrict__ descs, int n, int gper) {
+  cg::grid_group grid = cg::this_grid();
+  const int u = blockIdx.x / gper, bl = blockIdx.x % gper;
+  const bool real = u < n;
+  const UnionDesc d = descs[real ? u : n - 1];
+  const int m = d.m, C = d.k_old + d.k_f;
+  const int smax = m < C ? m : C;
+  const int spx = smax + (smax & 1);
+  const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+  double* Mw = d.work;
+  double* Acol = Mw + mreg;
+  double* Bt = Acol + (size_t)m * smax;
+  double* core = Bt + 2 * (size_t)C * smax;
+  double* Dp = core + 2 * (size_t)smax * smax;
+  double* tauA = Dp + smax;
+  double* tauB = tauA + smax;
+  int* hdr_aca = (int*)(Dp + 4 * (size_t)smax);  // s from union_aca_coop; [1]: fallback flag
+  const int s = real ? hdr_aca[0] : 0;
+  const int sp = s + (s & 1);
+  const int nthr_all = gper * blockDim.x, tb = bl * blockDim.x;
+  const int nw = blockDim.x >> 5, wb = bl * nw, wall = gper * nw;
+  double* GA = Mw;
+  double* GB = GA + (size_t)s * sp;
+  double* RA1s = Mw + 2 * (size_t)s * sp;
+  double* RB1s = RA1s + (size_t)s * sp;
+  double* TA = RB1s + (size_t)s * sp;
+  double* TB = TA + (size_t)s * sp;
+  // every CTA of the grid runs the same barrier sequence; the work is
+  // predicated on the union's state
+  if (bl == 0 && threadIdx.x == 0 && real) hdr_aca[1] = 0;
+  // pivot scaling L~ = X D^{-1}: rows over all threads of the union
+  if (s > 0)
+    for (int i = tb + threadIdx.x; i < m; i += nthr_all)
+      for (int t0 = 0; t0 < s; t0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = t0 + k < s ? Acol[(size_t)(t0 + k) * m + i] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (t0 + k < s) Acol[(size_t)(t0 + k) * m + i] = v[k] / Dp[t0 + k];
+      }
+  grid.sync();
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool act = s > 0 && hdr_aca[1] == 0;  // uniform per union
+    if (act) cta_gram2(Acol, m, Bt, C, s, sp, GA, GB, wb, wall);
+    grid.sync();
+    if (act && bl == 0) {
+      const double r = cta_chol2(GA, tauA, GB, tauB, s, sp);
+      if (pass == 0) {
+        if (!(r > kCholFloor)) {
+          if (threadIdx.x == 0) hdr_aca[1] = 1;  // union_kernel runs the Householder path
+        } else {
+          for (int e = threadIdx.x; e < 2 * s * sp; e += blockDim.x) RA1s[e] = GA[e];  // park R1
+        }
+      }
+    }
+    grid.sync();
+    if (s > 0 && hdr_aca[1] == 0) cta_trsm2(Acol, m, GA, tauA, Bt, C, GB, tauB, s, sp, tb, nthr_all);
+    grid.sync();
+  }
+  const bool ok = s > 0 && hdr_aca[1] == 0;
+  if (ok) cta_trmul2(GA, RA1s, TA, GB, RB1s, TB, s, sp, tb, nthr_all);
+  grid.sync();
+  if (ok)
+    for (int e = tb + threadIdx.x; e < s * s; e += nthr_all) {
+      const int j = e / s, i = e - j * s;
+      double acc = 0.0;
+      for (int l = (i > j ? i : j); l < s; ++l)
+        acc = fma(TB[(size_t)i * sp + l] * Dp[l], TA[(size_t)j * sp + l], acc);
+      core[(size_t)j * s + i] = acc;  // W = core^T at the hand-off location
+    }
+  grid.sync();
+  if (ok && bl == 0 && threadIdx.x == 0) *(int*)(core + 2 * (size_t)smax * smax) = s;  // header
+}
+}  // namespace
+
+void launch_union_cholqr_coop(const UnionDesc* d_descs, int n, int gper, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_union_cholqr_coop"};
+  if (n <= 0) return;
+  void* args[] = {(void*)&d_descs, (void*)&n, (void*)&gper};
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel((void*)union_cholqr_coop, dim3(gper * n), dim3(512), args, 0, s);
+  if (e != cudaSuccess)
+    fprintf(stderr, "[ifmm] cooperative CholeskyQR launch failed: %s\n", cudaGetErrorString(e));
+}
+
+size_t union_aca_coop_smem(int max_C, int max_rpc) {
+  return (size_t)(max_C + max_rpc + 1) * 8 + (size_t)2 * max_C * 4 + 64;
+}
+
+void launch_union_aca_coop(const UnionDesc* d_descs, int n, double thr, int gper, int max_C, int max_m,
+                           int max_smax, double* d_cand, int* d_done, cudaStream_t s) {
+  DbgSync dbg_sync_{s, "launch_union_aca_coop"};
+  if (n <= 0) return;
+  const int rpc = (max_m + gper - 1) / gper;
+  const size_t sh = union_aca_coop_smem(max_C, rpc);
+  static size_t attr = 0;
+  if (sh > attr) {
+    cudaFuncSetAttribute(union_aca_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+    attr = sh;
+  }
+  cudaMemsetAsync(d_done, 0, sizeof(int), s);
+  void* args[] = {(void*)&d_descs, (void*)&n, (void*)&gper, (void*)&thr, (void*)&d_cand,
+                  (void*)&d_done, (void*)&max_smax};
+  const cudaError_t e =
+      cudaLaunchCooperativeKernel((void*)union_aca_coop, dim3(gper * n), dim3(512), args, sh, s);
+  if (e != cudaSuccess)
+    fprintf(stderr, "[ifmm] cooperative ACA launch failed: %s\n", cudaGetErrorString(e));
+}
+
 void launch_union_jacobi_coop(const UnionDesc* d_descs, int n, int max_s, unsigned* d_flags,
                               cudaStream_t s) {
   DbgSync dbg_sync_{s, "launch_union_jacobi_coop"};
@@ -1654,7 +1946,10 @@ bool union_fits_smem(int m, int k_old, int k_f) {
 // smem == 0: workspaces in global memory with the full L1 as cache.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
                   int jac_smem_doubles, const UnionDesc* d_giants, int n_giants, int max_giant_s,
-                  unsigned* d_flags) {
+                  double* d_scratch, int max_giant_m, int max_giant_C) {
+  unsigned* d_flags = reinterpret_cast<unsigned*>(d_scratch);              // 64 per giant
+  int* d_done = reinterpret_cast<int*>(d_scratch + 32 * (size_t)n_giants);  // 1
+  double* d_cand = d_scratch + 32 * (size_t)n_giants + 8;                   // 2 per CTA
   DbgSync dbg_sync_{s, "launch_union"};
   if (n <= 0) return;
   static bool attr = false;
@@ -1692,6 +1987,15 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     // shared memory for the CholeskyQR matrices and the core SVD
     (void)jac_smem_doubles;
     const int jd = UNION_SMEM_DOUBLES;
+    if (n_giants > 0) {  // the giants' ACA on several CTAs each (union_kernel skips it)
+      int gper = 148 / n_giants;
+      const int want = (max_giant_m + 63) / 64;
+      if (gper > want) gper = want;
+      if (gper < 1) gper = 1;
+      launch_union_aca_coop(d_giants, n_giants, thr, gper, max_giant_C, max_giant_m, max_giant_s,
+                            d_cand, d_done, s);
+      launch_union_cholqr_coop(d_giants, n_giants, gper, s);
+    }
     union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
   if (n_giants > 0) launch_union_jacobi_coop(d_giants, n_giants, max_giant_s, d_flags, s);

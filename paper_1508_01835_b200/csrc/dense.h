@@ -88,9 +88,12 @@ bool union_fits_smem(int m, int k_old, int k_f);
 // of dynamic shared memory hold the core SVD when 2 s^2 fits.
 // d_giants / n_giants: the subset (giant != 0) whose core SVD runs on several
 // CTAs (cooperative launch between the two halves); d_flags: 64 uints per giant.
+// d_scratch: union_giant_scratch_doubles(n_giants) doubles.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
                   int jac_smem_doubles = 0, const UnionDesc* d_giants = nullptr, int n_giants = 0,
-                  int max_giant_s = 0, unsigned* d_flags = nullptr);
+                  int max_giant_s = 0, double* d_scratch = nullptr, int max_giant_m = 0,
+                  int max_giant_C = 0);
+inline int union_giant_scratch_doubles(int n_giants) { return 32 * n_giants + 2 * 160 + 8; }
 // s_max above which a union is "giant" (multi-CTA core SVD)
 constexpr int kGiantUnion = 160;
 

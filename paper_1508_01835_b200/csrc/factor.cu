@@ -207,9 +207,11 @@ struct Eliminator {
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
     UnionDesc* dgi = giants.empty() ? nullptr : C.stage.push_vec(C, giants);
     Blk gflags;
-    if (!giants.empty()) gflags = C.alloc(1, 32 * (int)giants.size());
-    unsigned* dfl = giants.empty() ? nullptr : reinterpret_cast<unsigned*>(gflags.p);
+    if (!giants.empty()) gflags = C.alloc(1, union_giant_scratch_doubles((int)giants.size()));
+    double* dfl = giants.empty() ? nullptr : gflags.p;
     const int ngi = (int)giants.size();
+    int max_gm = 0, max_gc = 0;
+    for (auto& u : giants) { max_gm = std::max(max_gm, u.m); max_gc = std::max(max_gc, u.k_old + u.k_f); }
     cudaEvent_t ka = nullptr;
     static FILE* ulog = nullptr;
     static bool ulog_init = false;
@@ -224,10 +226,10 @@ struct Eliminator {
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
               [&](cudaStream_t s) {
-                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl);
+                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc);
               });
     else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
-    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd, dgi, ngi, max_gs, dfl);
+    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc);
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
