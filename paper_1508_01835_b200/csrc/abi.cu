@@ -560,7 +560,7 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
   d[0].NW = NW; d[0].OM = OM; d[0].FM = FM; d[0].rank = rank; d[0].work = wk.p;
   const int smax = std::min(m, k_old + k_f);
   const bool fits = union_fits_smem(m, k_old, k_f);
-  d[0].giant = (!fits && smax > kGiantUnion) ? 1 : 0;
+  d[0].giant = (!fits && smax > giant_union_threshold()) ? 1 : 0;
   UnionDesc* dd = C.stage.push_vec(C, d);
   Blk fl = C.alloc(1, union_giant_scratch_doubles(1));
   launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant ? dd : nullptr, d[0].giant,

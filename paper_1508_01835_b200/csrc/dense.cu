@@ -1437,6 +1437,64 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
   }
 }
 
+// new basis = QA phi[:, :k] and maps = (QB sigma psi)[col][a] / weight[col]:
+// each thread owns one output row and a strip of 4 output columns (every Q
+// element is loaded once per strip); threads tbase + threadIdx.x, stride tstride.
+__device__ __forceinline__ void union_output(const UnionDesc& d, int s, int k, const double* gQA,
+                                             const double* gQB, const double* Wc, const double* Vc,
+                                             const int* order, int tbase, int tstride) {
+  const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
+  const int kb = (k + 3) >> 2;
+  for (long long e = tbase + threadIdx.x; e < (long long)(m + C) * kb; e += tstride) {
+    const int row = (int)(e % (m + C)), a0 = 4 * (int)(e / (m + C));
+    const bool isA = row < m;
+    const int i = isA ? row : row - m;
+    const double* Q = isA ? gQA + i : gQB + i;
+    const int ldq = isA ? m : C;
+    const double* col[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = order[min(a0 + u, k - 1)];
+      col[u] = (isA ? Vc : Wc) + (size_t)j * s;
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < s; ++l) {
+      const double q = Q[(size_t)l * ldq];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(q, col[u][l], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int a = a0 + u;
+      if (a >= k) break;
+      if (isA) d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc[u];
+      else if (i < ko) d.OM[(size_t)a * ko + i] = acc[u] / d.w[i];
+      else d.FM[(size_t)a * d.k_f + (i - ko)] = acc[u] / d.wf[i - ko];
+    }
+  }
+}
+
+// Output products of the giant unions, gper CTAs each (after union_svd_kernel
+// wrote the rank, the order and the singular values).
+__global__ void __launch_bounds__(256)
+union_output_kernel(const UnionDesc* __restrict__ descs, int n, int gper) {
+  const int u = blockIdx.x / gper, bl = blockIdx.x % gper;
+  if (u >= n) return;
+  const UnionDesc d = descs[u];
+  const int m = d.m, C = d.k_old + d.k_f;
+  const int smax = m < C ? m : C;
+  const int spx = smax + (smax & 1);
+  const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
+  const double* gQA = d.work + mreg;
+  const double* gQB = gQA + (size_t)m * smax;
+  const double* gW = gQB + 2 * (size_t)C * smax;
+  const int s = *(const int*)(gW + 2 * (size_t)smax * smax);
+  const int* order = (const int*)(gW + 2 * (size_t)smax * smax + 2 * (size_t)smax);
+  const int k = *d.rank;
+  if (s == 0 || k == 0) return;
+  union_output(d, s, k, gQA, gQB, gW, gW + (size_t)s * s, order, bl * blockDim.x, gper * blockDim.x);
+}
+
 // Second half of the union: SVD of the core (one-sided Jacobi on its
 // transpose W = core^T with accumulated V) and the output products.  A
 // separate kernel so the Jacobi gets its own register budget (teams of 8
@@ -1451,7 +1509,7 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
   extern __shared__ double smem[];
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const UnionDesc d = descs[bb];
-    const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
+    const int m = d.m, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
     const int spx = smax + (smax & 1);
     const size_t mreg = (size_t)m * C > 6 * (size_t)smax * spx ? (size_t)m * C : 6 * (size_t)smax * spx;
@@ -1478,38 +1536,8 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     for (int j = 0; j < s; ++j) kk += sig[order[j]] > thr;
     const int mr = d.min_rank < s ? d.min_rank : s;
     const int k = kk > mr ? kk : mr;
-    // each thread owns one output row and a strip of 4 output columns
-    // (every Q element is loaded once per strip)
-    {
-      const int kb = (k + 3) >> 2;
-      for (long long e = threadIdx.x; e < (long long)(m + C) * kb; e += blockDim.x) {
-        const int row = (int)(e % (m + C)), a0 = 4 * (int)(e / (m + C));
-        const bool isA = row < m;
-        const int i = isA ? row : row - m;
-        const double* Q = isA ? gQA + i : gQB + i;
-        const int ldq = isA ? m : C;
-        const double* col[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = order[min(a0 + u, k - 1)];
-          col[u] = (isA ? Vc : Wc) + (size_t)j * s;
-        }
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int l = 0; l < s; ++l) {
-          const double q = Q[(size_t)l * ldq];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) acc[u] = fma(q, col[u][l], acc[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int a = a0 + u;
-          if (a >= k) break;
-          if (isA) d.NB[(size_t)i * d.nb_r + (size_t)a * d.nb_c] = acc[u];
-          else if (i < ko) d.OM[(size_t)a * ko + i] = acc[u] / d.w[i];
-          else d.FM[(size_t)a * d.k_f + (i - ko)] = acc[u] / d.wf[i - ko];
-        }
-      }
-    }
+    // output products (giant unions: union_output_kernel on several CTAs)
+    if (!d.giant) union_output(d, s, k, gQA, gQB, Wc, Vc, order, 0, blockDim.x);
     for (int a = threadIdx.x; a < k; a += blockDim.x) d.NW[a] = sig[order[a]];
     if (threadIdx.x == 0) *d.rank = k;
     __syncthreads();
@@ -1938,6 +1966,15 @@ void launch_union_jacobi_coop(const UnionDesc* d_descs, int n, int max_s, unsign
   }
 }
 
+int giant_union_threshold() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("IFMM_GIANT");
+    t = e ? atoi(e) : 160;
+  }
+  return t;
+}
+
 bool union_fits_smem(int m, int k_old, int k_f) {
   return union_work_doubles(m, k_old, k_f) <= (size_t)UNION_SMEM_DOUBLES;
 }
@@ -2001,6 +2038,10 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
   if (n_giants > 0) launch_union_jacobi_coop(d_giants, n_giants, max_giant_s, d_flags, s);
   union_svd_kernel<<<n < 4096 ? n : 4096, 512, (size_t)UNION_SVD_SMEM_DOUBLES * 8, s>>>(
       d_descs, n, thr, UNION_SVD_SMEM_DOUBLES);
+  if (n_giants > 0) {
+    const int gper = 148 / n_giants > 0 ? 148 / n_giants : 1;
+    union_output_kernel<<<gper * n_giants, 256, 0, s>>>(d_giants, n_giants, gper);
+  }
 }
 
 // ============================================================================

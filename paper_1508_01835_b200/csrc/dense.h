@@ -94,8 +94,9 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
                   int max_giant_s = 0, double* d_scratch = nullptr, int max_giant_m = 0,
                   int max_giant_C = 0);
 inline int union_giant_scratch_doubles(int n_giants) { return 32 * n_giants + 2 * 160 + 8; }
-// s_max above which a union is "giant" (multi-CTA core SVD)
-constexpr int kGiantUnion = 160;
+// s_max above which a global-workspace union is "giant" (multi-CTA ACA,
+// CholeskyQR, core SVD and output); IFMM_GIANT overrides (diagnostics)
+int giant_union_threshold();
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to

@@ -195,7 +195,7 @@ struct Eliminator {
       const int sm = std::min(u.m, u.k_old + u.k_f);
       u.giant = 0;
       if (union_fits_smem(u.m, u.k_old, u.k_f)) { us.push_back(u); continue; }
-      if (sm > kGiantUnion) {
+      if (sm > giant_union_threshold()) {
         u.giant = 1;
         giants.push_back(u);
         max_gs = std::max(max_gs, sm);
