@@ -154,9 +154,38 @@ struct Eliminator {
     int min_rank;
   };
 
+  // IFMM_UNION_LOG=<file>: one line per union launch (diagnostics)
+  static FILE* union_log() {
+    static FILE* f = nullptr;
+    static bool init = false;
+    if (!init) {
+      init = true;
+      if (const char* n = getenv("IFMM_UNION_LOG")) f = fopen(n, "w");
+    }
+    return f;
+  }
+  // In-flight union launch of one pair wave (readback pending).
+  struct UnionsInFlight {
+    std::vector<UReq> reqs;
+    int* dr = nullptr;
+    Blk gflags;
+    bool giants = false;
+    std::chrono::steady_clock::time_point tl0, tl1;
+    size_t ns = 0, ng = 0;
+    bool active = false;
+  };
   void launch_unions(std::vector<UReq>& reqs) {
+    UnionsInFlight f;
+    launch_unions_async(reqs, f);
+    complete_unions(f);
+  }
+  void launch_unions_async(std::vector<UReq>& reqs, UnionsInFlight& fl) {
+    fl.active = false;
     if (reqs.empty()) return;
+    fl.reqs = reqs;
+    fl.active = true;
     int* dr = ranks_buf((int)reqs.size());
+    fl.dr = dr;
     std::vector<UnionDesc> ud;
     double uflops = 0;
     for (size_t i = 0; i < reqs.size(); ++i) {
@@ -213,12 +242,7 @@ struct Eliminator {
     int max_gm = 0, max_gc = 0;
     for (auto& u : giants) { max_gm = std::max(max_gm, u.m); max_gc = std::max(max_gc, u.k_old + u.k_f); }
     cudaEvent_t ka = nullptr;
-    static FILE* ulog = nullptr;
-    static bool ulog_init = false;
-    if (!ulog_init) {  // IFMM_UNION_LOG=<file>: one line per union launch (diagnostics)
-      ulog_init = true;
-      if (const char* f = getenv("IFMM_UNION_LOG")) ulog = fopen(f, "w");
-    }
+    FILE* ulog = union_log();
     auto tl0 = std::chrono::steady_clock::now();
     if (ulog) CUDA_CHECK(cudaStreamSynchronize(C.st));
     auto tl1 = std::chrono::steady_clock::now();
@@ -233,7 +257,21 @@ struct Eliminator {
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
-    const int* hr = C.readback_ints(dr, reqs.size());
+    fl.gflags = gflags;
+    fl.giants = !giants.empty();
+    fl.tl0 = tl0;
+    fl.tl1 = tl1;
+    fl.ns = us.size();
+    fl.ng = ug.size();
+  }
+  void complete_unions(UnionsInFlight& fl) {
+    if (!fl.active) return;
+    fl.active = false;
+    std::vector<UReq>& reqs = fl.reqs;
+    FILE* ulog = union_log();
+    const auto tl0 = fl.tl0, tl1 = fl.tl1;
+    const size_t nus = fl.ns, nug = fl.ng;
+    const int* hr = C.readback_ints(fl.dr, reqs.size());
     if (ulog) {
       auto tl2 = std::chrono::steady_clock::now();
       int mm = 0, mc = 0, mk = 0;
@@ -243,7 +281,7 @@ struct Eliminator {
         mk = std::max(mk, hr[i]);
       }
       static auto prev = tl0;
-      fprintf(ulog, "%zu %zu %d %d %d %.3f %.3f %.3f\n", us.size(), ug.size(), mm, mc, mk,
+      fprintf(ulog, "%zu %zu %d %d %d %.3f %.3f %.3f\n", nus, nug, mm, mc, mk,
               std::chrono::duration<double, std::milli>(tl2 - tl1).count(),
               std::chrono::duration<double, std::milli>(tl1 - tl0).count(),
               std::chrono::duration<double, std::milli>(tl0 - prev).count());
@@ -253,7 +291,7 @@ struct Eliminator {
       reqs[i].bu->rank = hr[i];
       C.free(reqs[i].bu->W);
     }
-    if (!giants.empty()) C.free(gflags);
+    if (fl.giants) C.free(fl.gflags);
   }
 
   void make_identity(BU& b, int m, int k, const Blk& w) {
@@ -287,7 +325,9 @@ struct Eliminator {
     BU* bu;
     BU* bv;
   };
-  void rebase_many(std::vector<RebaseReq>& reqs);
+  void rebase_basis(std::vector<RebaseReq>& reqs);
+  void rebase_edges(std::vector<RebaseReq>& reqs);
+  void rebase_many(std::vector<RebaseReq>& reqs) { rebase_basis(reqs); rebase_edges(reqs); }
   struct PairJob {
     int cj, ck;
     const FillFac* f_kj;
@@ -301,6 +341,10 @@ struct Eliminator {
   bool exact_order = false;
   void process_pairs(std::vector<PairJob>& pairs, LevelStats& st);
   void run_wave(std::vector<PairJob*>& jobs, LevelStats& st);
+  void wave_launch(std::vector<PairJob*>& jobs, LevelStats& st, UnionsInFlight& fl);
+  void wave_complete(std::vector<PairJob*>& jobs, LevelStats& st, UnionsInFlight& fl);
+  void wave_basis(std::vector<PairJob*>& jobs, std::vector<RebaseReq>& reqs);
+  void wave_rest(std::vector<PairJob*>& jobs, std::vector<RebaseReq>& reqs, LevelStats& st);
   void eliminate_wave(const std::vector<int>& cs, LevelStats& st);
   bool exact_fill = false;
   unsigned long long rsvd_calls = 0;
@@ -430,16 +474,14 @@ void Eliminator::finish_unions(int c, BU& bu, BU& bv, const double* fu, int fu_r
 // E t^T read the already row-updated blocks, so an edge between two clusters
 // of the wave receives r_j E t_l^T (the reference applies the same two
 // products in pair order; matrix products associate).
-void Eliminator::rebase_many(std::vector<RebaseReq>& reqs) {
+void Eliminator::rebase_basis(std::vector<RebaseReq>& reqs) {
   Phase ph(C, PH_REBASE);
   CopyBatch cb;
-  GemmBatch rowg, colg;
   for (auto& q : reqs) {
     const int c = q.c;
     BU& bu = *q.bu;
     BU& bv = *q.bv;
-    const int nxn = g.nx[c], nzn = g.nz[c], nyn = g.ny[c];
-    const int py = g.ny[q.partner];
+    const int nxn = g.nx[c], nzn = g.nz[c];
     const int m = g.size[nxn];
     const int kn = bu.rank, ko = bu.k_old;
     IFMM_ASSERT(bu.rank == bv.rank, "unequal U/V ranks in rebase");
@@ -462,6 +504,21 @@ void Eliminator::rebase_many(std::vector<RebaseReq>& reqs) {
       C.free(g.sv[c]);
       g.sv[c] = w;
     }
+  }
+  cb.run(C);
+}
+
+// _apply_rebase (factor.py:395-430), edge part: every y-edge of the rebased
+// clusters (rebase_basis already swapped the bases and weights).
+void Eliminator::rebase_edges(std::vector<RebaseReq>& reqs) {
+  Phase ph(C, PH_REBASE);
+  GemmBatch rowg, colg;
+  for (auto& q : reqs) {
+    const int c = q.c;
+    BU& bu = *q.bu;
+    const int nzn = g.nz[c], nyn = g.ny[c];
+    const int py = g.ny[q.partner];
+    const int kn = bu.rank, ko = bu.k_old;
     IFMM_ASSERT(!g.get(nyn, nyn), "live cluster with a y-y self edge");
     if (!(bu.identity && kn == ko)) {
       std::vector<int> rs(g.rows[nyn].begin(), g.rows[nyn].end());
@@ -474,7 +531,6 @@ void Eliminator::rebase_many(std::vector<RebaseReq>& reqs) {
       }
     }
   }
-  cb.run(C);
   run_gemm(rowg);
   for (auto& q : reqs) {
     const int c = q.c;
@@ -566,21 +622,37 @@ void Eliminator::process_pairs(std::vector<PairJob>& pairs, LevelStats& st) {
   }
   std::vector<std::vector<PairJob*>> waves(maxw + 1);
   for (size_t i = 0; i < live.size(); ++i) waves[wave[i]].push_back(live[i]);
-  for (int w = 1; w <= maxw; ++w) run_wave(waves[w], st);
+  // Pipelined: wave w+1's unions (which read only the bases swapped by
+  // rebase_basis of wave w) run on the device while the host builds wave w's
+  // edge rebases and K rewrite.  Device work stays in the sequential order's
+  // data dependencies (stream order); results are identical.
+  UnionsInFlight fl[2];
+  wave_launch(waves[1], st, fl[1]);
+  wave_complete(waves[1], st, fl[1]);
+  std::vector<RebaseReq> reqs;
+  for (int w = 1; w <= maxw; ++w) {
+    wave_basis(waves[w], reqs);
+    UnionsInFlight& nx = fl[(w + 1) & 1];
+    if (w < maxw) wave_launch(waves[w + 1], st, nx);
+    wave_rest(waves[w], reqs, st);
+    if (w < maxw) wave_complete(waves[w + 1], st, nx);
+  }
 }
 
 void Eliminator::run_wave(std::vector<PairJob*>& jobs, LevelStats& st) {
+  UnionsInFlight fl;
+  wave_launch(jobs, st, fl);
+  wave_complete(jobs, st, fl);
+  std::vector<RebaseReq> reqs;
+  wave_basis(jobs, reqs);
+  wave_rest(jobs, reqs, st);
+}
+
+void Eliminator::wave_launch(std::vector<PairJob*>& jobs, LevelStats& st, UnionsInFlight& fl) {
   // ---- unions of every cluster of the wave, one launch ----
   std::vector<UReq> pend;
   for (PairJob* pj : jobs) {
     PairJob& p = *pj;
-    const int yj = g.ny[p.cj], yk = g.ny[p.ck];
-    Blk* pkj = g.get(yk, yj);
-    Blk* pjk = g.get(yj, yk);
-    p.has_kj = pkj != nullptr;
-    p.has_jk = pjk != nullptr;
-    if (p.has_kj) p.old_kj = *pkj;
-    if (p.has_jk) p.old_jk = *pjk;
     const int r1 = p.r1, r2 = p.r2;
     if (!p.ej && !p.ek) {
       cluster_unions(p.cj, r2 ? p.f_jk->U : nullptr, 1, r2 ? p.f_jk->m : 0, r2,
@@ -599,7 +671,11 @@ void Eliminator::run_wave(std::vector<PairJob*>& jobs, LevelStats& st) {
                      p.vj, st, pend);
     }
   }
-  launch_unions(pend);
+  launch_unions_async(pend, fl);
+}
+
+void Eliminator::wave_complete(std::vector<PairJob*>& jobs, LevelStats& st, UnionsInFlight& fl) {
+  complete_unions(fl);
   // ---- rank equalisation (rare relaunches) ----
   for (PairJob* pj : jobs) {
     PairJob& p = *pj;
@@ -621,13 +697,12 @@ void Eliminator::run_wave(std::vector<PairJob*>& jobs, LevelStats& st) {
                     rv ? fv->S : nullptr, st);
     }
   }
-  // ---- rebases ----
-  std::vector<int> kjo(jobs.size()), kko(jobs.size());
-  std::vector<RebaseReq> reqs;
+}
+
+void Eliminator::wave_basis(std::vector<PairJob*>& jobs, std::vector<RebaseReq>& reqs) {
+  reqs.clear();
   for (size_t i = 0; i < jobs.size(); ++i) {
     PairJob& p = *jobs[i];
-    kjo[i] = g.size[g.ny[p.cj]];
-    kko[i] = g.size[g.ny[p.ck]];
     if (!p.ej && !p.ek) {
       reqs.push_back({p.cj, p.ck, &p.uj, &p.vj});
       reqs.push_back({p.ck, p.cj, &p.uk, &p.vk});
@@ -636,7 +711,27 @@ void Eliminator::run_wave(std::vector<PairJob*>& jobs, LevelStats& st) {
       reqs.push_back({live, deadc, &p.uj, &p.vj});
     }
   }
-  rebase_many(reqs);
+  rebase_basis(reqs);
+}
+
+void Eliminator::wave_rest(std::vector<PairJob*>& jobs, std::vector<RebaseReq>& reqs, LevelStats& st) {
+  (void)st;
+  // K-rewrite inputs: the current (y_k, y_j) / (y_j, y_k) blocks and y sizes,
+  // taken after every earlier wave's edge rebases
+  std::vector<int> kjo(jobs.size()), kko(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    PairJob& p = *jobs[i];
+    const int yj = g.ny[p.cj], yk = g.ny[p.ck];
+    Blk* pkj = g.get(yk, yj);
+    Blk* pjk = g.get(yj, yk);
+    p.has_kj = pkj != nullptr;
+    p.has_jk = pjk != nullptr;
+    if (p.has_kj) p.old_kj = *pkj;
+    if (p.has_jk) p.old_jk = *pjk;
+    kjo[i] = g.size[g.ny[p.cj]];
+    kko[i] = g.size[g.ny[p.ck]];
+  }
+  rebase_edges(reqs);
   // ---- K-edge rewrite ----
   Phase ph(C, PH_NEWK);
   GemmBatch ga, gb2, gc;
