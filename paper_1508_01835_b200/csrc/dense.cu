@@ -1948,10 +1948,10 @@ void launch_union_aca_coop(const UnionDesc* d_descs, int n, double thr, int gper
 }
 
 void launch_union_jacobi_coop(const UnionDesc* d_descs, int n, int max_s, unsigned* d_flags,
-                              cudaStream_t s) {
+                              cudaStream_t s, int sm_free) {
   DbgSync dbg_sync_{s, "launch_union_jacobi_coop"};
   if (n <= 0) return;
-  int per = 148 / n;
+  int per = sm_free / n;
   const int half = (max_s + 1) / 2;
   const int need = (half + 7) / 8;  // 8 warps (pairs) per CTA and round
   if (per > need) per = need;
@@ -1970,7 +1970,7 @@ int giant_union_threshold() {
   static int t = -1;
   if (t < 0) {
     const char* e = getenv("IFMM_GIANT");
-    t = e ? atoi(e) : 160;
+    t = e ? atoi(e) : 100;
   }
   return t;
 }
@@ -1983,7 +1983,10 @@ bool union_fits_smem(int m, int k_old, int k_f) {
 // smem == 0: workspaces in global memory with the full L1 as cache.
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
                   int jac_smem_doubles, const UnionDesc* d_giants, int n_giants, int max_giant_s,
-                  double* d_scratch, int max_giant_m, int max_giant_C) {
+                  double* d_scratch, int max_giant_m, int max_giant_C, int sm_reserved) {
+  // SMs left for the cooperative giant kernels: the concurrent shared-memory
+  // union launch holds one SM per union (228 KB each)
+  const int sm_free = 148 - (sm_reserved < 120 ? sm_reserved : 120);
   unsigned* d_flags = reinterpret_cast<unsigned*>(d_scratch);              // 64 per giant
   int* d_done = reinterpret_cast<int*>(d_scratch + 32 * (size_t)n_giants);  // 1
   double* d_cand = d_scratch + 32 * (size_t)n_giants + 8;                   // 2 per CTA
@@ -2025,7 +2028,7 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     (void)jac_smem_doubles;
     const int jd = UNION_SMEM_DOUBLES;
     if (n_giants > 0) {  // the giants' ACA on several CTAs each (union_kernel skips it)
-      int gper = 148 / n_giants;
+      int gper = sm_free / n_giants;
       const int want = (max_giant_m + 63) / 64;
       if (gper > want) gper = want;
       if (gper < 1) gper = 1;
@@ -2035,11 +2038,11 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
     }
     union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
-  if (n_giants > 0) launch_union_jacobi_coop(d_giants, n_giants, max_giant_s, d_flags, s);
+  if (n_giants > 0) launch_union_jacobi_coop(d_giants, n_giants, max_giant_s, d_flags, s, sm_free);
   union_svd_kernel<<<n < 4096 ? n : 4096, 512, (size_t)UNION_SVD_SMEM_DOUBLES * 8, s>>>(
       d_descs, n, thr, UNION_SVD_SMEM_DOUBLES);
   if (n_giants > 0) {
-    const int gper = 148 / n_giants > 0 ? 148 / n_giants : 1;
+    const int gper = sm_free / n_giants > 0 ? sm_free / n_giants : 1;
     union_output_kernel<<<gper * n_giants, 256, 0, s>>>(d_giants, n_giants, gper);
   }
 }

@@ -92,7 +92,7 @@ bool union_fits_smem(int m, int k_old, int k_f);
 void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, int smem,
                   int jac_smem_doubles = 0, const UnionDesc* d_giants = nullptr, int n_giants = 0,
                   int max_giant_s = 0, double* d_scratch = nullptr, int max_giant_m = 0,
-                  int max_giant_C = 0);
+                  int max_giant_C = 0, int sm_reserved = 0);
 inline int union_giant_scratch_doubles(int n_giants) { return 32 * n_giants + 2 * 160 + 8; }
 // s_max above which a global-workspace union is "giant" (multi-CTA ACA,
 // CholeskyQR, core SVD and output); IFMM_GIANT overrides (diagnostics)

@@ -250,7 +250,8 @@ struct Eliminator {
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
               [&](cudaStream_t s) {
-                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc);
+                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc,
+                             (int)us.size());
               });
     else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
     else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc);

@@ -1,6 +1,6 @@
 """Per-level kernel-category profile of one factorize at a BASELINE config.
 
-    IFMM_MEMTRACE=1 python tools/diag_level_profile.py c4
+    IFMM_MEMTRACE=1 python tools/diag_level_profile.py c4 [N]
 Prints, after each level, arena usage and cumulative device time per kernel
 category (CUDA events per launch -- diagnostics, not bench numbers)."""
 import os
@@ -16,10 +16,11 @@ import paper_1508_01835_b200 as P  # noqa: E402
 from paper_1508_01835_b200 import _native as NN  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
+n_override = int(sys.argv[2]) if len(sys.argv) > 2 else None
 import torch  # noqa: E402
 free, _ = torch.cuda.mem_get_info()
 os.environ.setdefault("IFMM_ARENA_GB", f"{max(0.5 * free, free - 22 * 2**30) / 2**30:.1f}")
-inp = bench.inputs(cfg)
+inp = bench.inputs(cfg, n_override)
 K = P.exp_kernel() if inp["kern"] == "exp" else P.imq_kernel(inp["h"])
 t0 = time.perf_counter()
 tree, _ = P.build_octree(inp["pts"], inp["leaf"])
