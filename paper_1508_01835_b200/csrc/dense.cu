@@ -1559,7 +1559,8 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
 }  // namespace
 
 namespace {
-// Multi-CTA one-sided Jacobi for the cores of giant unions (s > 160: the
+// Multi-CTA one-sided Jacobi for the cores of giant unions (s above
+// giant_union_threshold(), 100; the
 // level-2 unions of c3/c4 reach s ~ 400).  One cooperative launch covers
 // every giant union of a pair wave, gper CTAs per union; W and V stay in
 // global memory (L2-resident).  The rounds, pairs and per-pair arithmetic are
@@ -1677,7 +1678,7 @@ union_jacobi_coop(const UnionDesc* __restrict__ descs, int n, int gper, unsigned
 }  // namespace
 
 namespace {
-// Multi-CTA full-pivot ACA for giant unions (s > 160), one cooperative launch
+// Multi-CTA full-pivot ACA for giant unions (s > giant_union_threshold()), one cooperative launch
 // for all giants of a pair wave, gper CTAs per union.  CTA bl owns a slab of
 // rows of the residual M (global memory, the union's workspace); per pivot
 // step: slab argmax -> global candidates -> grid barrier -> every CTA
