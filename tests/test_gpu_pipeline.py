@@ -120,3 +120,22 @@ def test_partitioned_matvec_device_phases(world):
     if world == 1:  # the public entry without a process group
         y1 = h2_matvec_distributed(ops, x)
         assert float(torch.linalg.norm(y1 - ref) / torch.linalg.norm(ref)) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["imq3d_n2048", "exp2d_n2048_n6"])
+def test_exact_order_parity(name):
+    """Strict reference pair order (one pair per wave, still pipelined):
+    same statistics and x as the reference."""
+    import paper_1508_01835_b200 as P
+    g = load_golden(name)
+    eps = float(g["eps"])
+    tree, topo, ops = _pipeline(P, g)
+    graph = P.assemble_extended_graph(ops)
+    fct = P.factorize(graph, eps, seed=0, sigma0=float(g["sigma0"]), exact_order=True)
+    st = fct.stats
+    np.testing.assert_array_equal([s.compressed_pairs for s in st.levels], g["lv_compressed"])
+    np.testing.assert_array_equal([sum(s.ranks) for s in st.levels], g["lv_ranksum"])
+    assert st.peak_edges == int(g["peak_edges"])
+    x = fct.solve(g["b"])
+    rel = np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"])
+    assert rel <= 10 * max(eps, 1e-12), rel
