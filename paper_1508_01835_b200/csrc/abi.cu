@@ -50,6 +50,9 @@ void* ifmm_ctx_create(int device, unsigned long long arena_bytes) {
   c->device = device;
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   CUDA_CHECK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&c->side_done, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
   if (arena_bytes == 0) {
@@ -74,6 +77,9 @@ void ifmm_ctx_destroy(void* p) {
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_pinned_i) cudaFreeHost(c->h_pinned_i);
   cudaStreamDestroy(c->st2);
+  cudaStreamDestroy(c->st3);
+  cudaEventDestroy(c->side_ev);
+  cudaEventDestroy(c->side_done);
   cudaStreamDestroy(c->st);
   delete c;
 }

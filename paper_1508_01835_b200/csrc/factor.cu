@@ -627,15 +627,27 @@ void Eliminator::process_pairs(std::vector<PairJob>& pairs, LevelStats& st) {
   // rebase_basis of wave w) run on the device while the host builds wave w's
   // edge rebases and K rewrite.  Device work stays in the sequential order's
   // data dependencies (stream order); results are identical.
+  //
+  // Wave w's rebases and K rewrite also run on a side stream (st3), so their
+  // small GEMMs overlap wave w+1's unions on the device.  st3 starts after
+  // wave w's basis swap; the engine stream waits for st3 before it reads
+  // wave w+1's ranks (after which wave w's freed blocks may be reused) and
+  // at the end of the pairs.
   UnionsInFlight fl[2];
   wave_launch(waves[1], st, fl[1]);
   wave_complete(waves[1], st, fl[1]);
   std::vector<RebaseReq> reqs;
   for (int w = 1; w <= maxw; ++w) {
     wave_basis(waves[w], reqs);
+    CUDA_CHECK(cudaEventRecord(C.side_ev, C.st));
     UnionsInFlight& nx = fl[(w + 1) & 1];
     if (w < maxw) wave_launch(waves[w + 1], st, nx);
+    CUDA_CHECK(cudaStreamWaitEvent(C.st3, C.side_ev, 0));
+    std::swap(C.st, C.st3);
     wave_rest(waves[w], reqs, st);
+    std::swap(C.st, C.st3);
+    CUDA_CHECK(cudaEventRecord(C.side_done, C.st3));
+    CUDA_CHECK(cudaStreamWaitEvent(C.st, C.side_done, 0));
     if (w < maxw) wave_complete(waves[w + 1], st, nx);
   }
 }

@@ -198,8 +198,9 @@ void* Staging::push(Ctx& ctx, const void* src, size_t bytes) {
   const size_t nb = (bytes + 255) / 256 * 256;
   if (nb > cap_) throw Error(E_OOM, "descriptor batch larger than staging ring");
   if (off_ + nb > cap_) {
-    // ring wrap: all earlier copies/kernels reading the ring must be done
-    ctx.sync();
+    // ring wrap: all earlier copies/kernels reading the ring must be done,
+    // on every stream that takes descriptors (engine, forked, side)
+    CUDA_CHECK(cudaDeviceSynchronize());
     off_ = 0;
   }
   std::memcpy(h_ + off_, src, bytes);

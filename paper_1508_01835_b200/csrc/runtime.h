@@ -104,6 +104,8 @@ struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;        // forked side stream (concurrent variants)
+  cudaStream_t st3 = nullptr;        // side stream for a pair wave's rebases / K rewrite
+  cudaEvent_t side_ev = nullptr, side_done = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // run `a` on st and `b` on st2 concurrently; st waits for both afterwards
   template <class FA, class FB>
