@@ -1838,7 +1838,7 @@ namespace {
 // W = core^T and the hand-off header; flags the union for union_kernel's
 // Householder path when a Cholesky pivot ratio signals cond > ~1e6.
 __global__ void __launch_bounds__(512)
-union_cholqr_coop(const UnionDesc* __restrict__ descs, int n, int gper) {
+union_cholqr_coop(const UnionDesc* __restrict__ descs, int n, int gper, int max_s) {
   cg::grid_group grid = cg::this_grid();
   const int u = blockIdx.x / gper, bl = blockIdx.x % gper;
   const bool real = u < n;
@@ -1884,15 +1884,73 @@ union_cholqr_coop(const UnionDesc* __restrict__ descs, int n, int gper) {
     const bool act = s > 0 && hdr_aca[1] == 0;  // uniform per union
     if (act) cta_gram2(Acol, m, Bt, C, s, sp, GA, GB, wb, wall);
     grid.sync();
-    if (act && bl == 0) {
-      const double r = cta_chol2(GA, tauA, GB, tauB, s, sp);
-      if (pass == 0) {
-        if (!(r > kCholFloor)) {
+    // in-place Cholesky of both Grams on all of the union's CTAs: one grid
+    // barrier per column (the same per-element arithmetic as cta_chol2)
+    {
+      double mxA = 0.0, mxB = 0.0, minr = 1.0;
+      if (act)
+        for (int k = 0; k < s; ++k) {
+          mxA = fmax(mxA, GA[(size_t)k * sp + k]);
+          mxB = fmax(mxB, GB[(size_t)k * sp + k]);
+        }
+      const double imxA = act ? 1.0 / mxA : 0.0, imxB = act ? 1.0 / mxB : 0.0;
+      grid.sync();  // every CTA read the original diagonals
+      const int lane = threadIdx.x & 31;
+      for (int k = 0; k <= max_s; ++k) {
+        if (act && k <= s) {
+          if (k > 0) {  // finalise row k-1 of both R factors
+            const double ra = tauA[k - 1], rb = tauB[k - 1];
+            double* gra = GA + (size_t)(k - 1) * sp;
+            double* grb = GB + (size_t)(k - 1) * sp;
+            for (int j = k - 1 + tb + threadIdx.x; j < s; j += nthr_all) {
+              gra[j] *= ra;
+              grb[j] *= rb;
+            }
+          }
+          if (k < s) {
+            const double* ga = GA + (size_t)k * sp;
+            const double* gbp = GB + (size_t)k * sp;
+            const double pa = ga[k], pb = gbp[k];
+            const double inva = 1.0 / pa, invb = 1.0 / pb;
+            const double ra = rsqrt(pa), rb = rsqrt(pb);
+            const double qa = pa * imxA, qb = pb * imxB;
+            minr = (qa > 0.0 && isfinite(pa)) ? fmin(minr, qa) : 0.0;
+            minr = (qb > 0.0 && isfinite(pb)) ? fmin(minr, qb) : 0.0;
+            if (bl == 0 && threadIdx.x == 0) { tauA[k] = ra; tauB[k] = rb; }
+            const int nr = s - k - 1;
+            for (int t = wb + (threadIdx.x >> 5); t < 2 * nr; t += wall) {
+              const bool isA = t < nr;
+              const int i = k + 1 + (isA ? t : t - nr);
+              const double* g = isA ? ga : gbp;
+              double* Gi = (isA ? GA : GB) + (size_t)i * sp;
+              const double fi = g[i] * (isA ? inva : invb);
+              for (int j0 = i + lane; j0 < s; j0 += 128) {
+                double gv[4], gw[4];
+#pragma unroll
+                for (int u2 = 0; u2 < 4; ++u2) {
+                  const int j = j0 + 32 * u2;
+                  gv[u2] = j < s ? g[j] : 0.0;
+                  gw[u2] = j < s ? Gi[j] : 0.0;
+                }
+#pragma unroll
+                for (int u2 = 0; u2 < 4; ++u2) {
+                  const int j = j0 + 32 * u2;
+                  if (j < s) Gi[j] = fma(-fi, gv[u2], gw[u2]);
+                }
+              }
+            }
+          }
+        }
+        grid.sync();
+      }
+      if (act && pass == 0 && bl == 0) {
+        if (!(minr > kCholFloor)) {
           if (threadIdx.x == 0) hdr_aca[1] = 1;  // union_kernel runs the Householder path
-        } else {
-          for (int e = threadIdx.x; e < 2 * s * sp; e += blockDim.x) RA1s[e] = GA[e];  // park R1
         }
       }
+      grid.sync();
+      if (act && pass == 0 && hdr_aca[1] == 0)  // park R1
+        for (int e = tb + threadIdx.x; e < 2 * s * sp; e += nthr_all) RA1s[e] = GA[e];
     }
     grid.sync();
     if (s > 0 && hdr_aca[1] == 0) cta_trsm2(Acol, m, GA, tauA, Bt, C, GB, tauB, s, sp, tb, nthr_all);
@@ -1914,10 +1972,10 @@ union_cholqr_coop(const UnionDesc* __restrict__ descs, int n, int gper) {
 }
 }  // namespace
 
-void launch_union_cholqr_coop(const UnionDesc* d_descs, int n, int gper, cudaStream_t s) {
+void launch_union_cholqr_coop(const UnionDesc* d_descs, int n, int gper, int max_s, cudaStream_t s) {
   DbgSync dbg_sync_{s, "launch_union_cholqr_coop"};
   if (n <= 0) return;
-  void* args[] = {(void*)&d_descs, (void*)&n, (void*)&gper};
+  void* args[] = {(void*)&d_descs, (void*)&n, (void*)&gper, (void*)&max_s};
   const cudaError_t e =
       cudaLaunchCooperativeKernel((void*)union_cholqr_coop, dim3(gper * n), dim3(512), args, 0, s);
   if (e != cudaSuccess)
@@ -2035,7 +2093,7 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
       if (gper < 1) gper = 1;
       launch_union_aca_coop(d_giants, n_giants, thr, gper, max_giant_C, max_giant_m, max_giant_s,
                             d_cand, d_done, s);
-      launch_union_cholqr_coop(d_giants, n_giants, gper, s);
+      launch_union_cholqr_coop(d_giants, n_giants, gper, max_giant_s, s);
     }
     union_kernel<false><<<n < 4096 ? n : 4096, nthr, (size_t)jd * 8, s>>>(d_descs, n, thr, jd, force_hh);
   }
