@@ -1563,10 +1563,9 @@ namespace {
 // giant_union_threshold(), 100; the
 // level-2 unions of c3/c4 reach s ~ 400).  One cooperative launch covers
 // every giant union of a pair wave, gper CTAs per union; W and V stay in
-// global memory (L2-resident).  The rounds, pairs and per-pair arithmetic are
-// those of cta_jacobi_wv (one warp per pair, 16 rows per lane in registers,
-// streamed tail beyond), so the result is bitwise the single-CTA one; a grid
-// barrier separates the rounds.  flags[u * 64 + sweep] collects "not yet
+// global memory (L2-resident).  Block-cyclic ordering (see below); the
+// per-pair arithmetic is that of cta_jacobi_wv (one warp per pair, 16 rows
+// per lane in registers, streamed tail beyond).  flags[u * 64 + sweep] collects "not yet
 // converged" per union and sweep.
 __global__ void __launch_bounds__(256)
 union_jacobi_coop(const UnionDesc* __restrict__ descs, int n, int gper, unsigned* flags, int max_m1) {
@@ -1593,72 +1592,91 @@ union_jacobi_coop(const UnionDesc* __restrict__ descs, int n, int gper, unsigned
   constexpr int T = 32, NE = 16;
   bool live = s >= 2;
   grid.sync();
+  // block-cyclic Jacobi: the columns form nb = 2 gper blocks; a block round
+  // pairs the blocks round-robin (one block pair per CTA) and each CTA runs a
+  // full inner round-robin sweep over the columns of its two blocks with CTA
+  // barriers; one grid barrier per block round (nb - 1 per sweep instead of
+  // s - 1).  Every column pair still meets once per sweep.
+  const int nb = 2 * gper, bsz = (s + nb - 1) / nb;
+  (void)max_m1; (void)half; (void)m1;
   for (int sweep = 0; sweep < 40; ++sweep) {
     bool again = false;
-    for (int r = 0; r < max_m1; ++r) {
-      if (live && r < m1)
-        for (int pi = bl * nwb + warp; pi < half; pi += gper * nwb) {
-          int p, q;
-          if (pi == 0) { p = r; q = m1; }
-          else { p = (r + pi) % m1; q = (r - pi + m1) % m1; }
-          const int lo = p < q ? p : q, hi = p < q ? q : p;
-          if (hi >= s) continue;  // warp-uniform
-          double* x = W + (size_t)lo * s;
-          double* y = W + (size_t)hi * s;
-          double xr[NE], yr[NE];
-          double a = 0.0, b = 0.0, g = 0.0;
-#pragma unroll
-          for (int e = 0; e < NE; ++e) {
-            const int i = lane + e * T;
-            xr[e] = i < s ? x[i] : 0.0;
-            yr[e] = i < s ? y[i] : 0.0;
-            a = fma(xr[e], xr[e], a); b = fma(yr[e], yr[e], b); g = fma(xr[e], yr[e], g);
-          }
-          for (int i = lane + NE * T; i < s; i += T) {
-            const double uu = x[i], vv = y[i];
-            a = fma(uu, uu, a); b = fma(vv, vv, b); g = fma(uu, vv, g);
-          }
-          a = team_sum<T>(a); b = team_sum<T>(b); g = team_sum<T>(g);
-          const double ab = a * b, g2 = g * g;
-          if (g != 0.0 && g2 > tr2 * ab) {
-            const double dd = b - a, gg = 2.0 * g;
-            const double t = copysign(fabs(gg), dd * gg) / (fabs(dd) + sqrt(fma(dd, dd, gg * gg)));
-            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+    for (int r = 0; r < nb - 1; ++r) {
+      if (live) {
+        int P, Q;
+        if (bl == 0) { P = r; Q = nb - 1; }
+        else { P = (r + bl) % (nb - 1); Q = (r - bl + nb - 1) % (nb - 1); }
+        const int p0 = P * bsz, q0 = Q * bsz;
+        const int np = max(0, min(bsz, s - p0)), nq = max(0, min(bsz, s - q0));
+        const int nc = np + nq, ncp = nc + (nc & 1);
+        for (int sr = 0; sr < ncp - 1; ++sr) {
+          for (int pi = warp; pi < ncp / 2; pi += nwb) {
+            int a2, b2;
+            if (pi == 0) { a2 = sr; b2 = ncp - 1; }
+            else { a2 = (sr + pi) % (ncp - 1); b2 = (sr - pi + ncp - 1) % (ncp - 1); }
+            if (a2 >= nc || b2 >= nc) continue;  // warp-uniform
+            const int ga2 = a2 < np ? p0 + a2 : q0 + (a2 - np);
+            const int gb2 = b2 < np ? p0 + b2 : q0 + (b2 - np);
+            const int lo = ga2 < gb2 ? ga2 : gb2, hi = ga2 < gb2 ? gb2 : ga2;
+            double* x = W + (size_t)lo * s;
+            double* y = W + (size_t)hi * s;
+            double xr[NE], yr[NE];
+            double a = 0.0, bb = 0.0, g = 0.0;
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
               const int i = lane + e * T;
-              if (i < s) {
-                x[i] = fma(c, xr[e], -sn * yr[e]);
-                y[i] = fma(sn, xr[e], c * yr[e]);
-              }
+              xr[e] = i < s ? x[i] : 0.0;
+              yr[e] = i < s ? y[i] : 0.0;
+              a = fma(xr[e], xr[e], a); bb = fma(yr[e], yr[e], bb); g = fma(xr[e], yr[e], g);
             }
             for (int i = lane + NE * T; i < s; i += T) {
               const double uu = x[i], vv = y[i];
-              x[i] = fma(c, uu, -sn * vv);
-              y[i] = fma(sn, uu, c * vv);
+              a = fma(uu, uu, a); bb = fma(vv, vv, bb); g = fma(uu, vv, g);
             }
-            double* vx = V + (size_t)lo * s;
-            double* vy = V + (size_t)hi * s;
-            for (int i0 = lane; i0 < s; i0 += 4 * T) {
-              double uu[4], vv[4];
+            a = team_sum<T>(a); bb = team_sum<T>(bb); g = team_sum<T>(g);
+            const double ab = a * bb, g2 = g * g;
+            if (g != 0.0 && g2 > tr2 * ab) {
+              const double dd = bb - a, gg = 2.0 * g;
+              const double t = copysign(fabs(gg), dd * gg) / (fabs(dd) + sqrt(fma(dd, dd, gg * gg)));
+              const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = i0 + e * T;
-                uu[e] = i < s ? vx[i] : 0.0;
-                vv[e] = i < s ? vy[i] : 0.0;
-              }
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = i0 + e * T;
+              for (int e = 0; e < NE; ++e) {
+                const int i = lane + e * T;
                 if (i < s) {
-                  vx[i] = fma(c, uu[e], -sn * vv[e]);
-                  vy[i] = fma(sn, uu[e], c * vv[e]);
+                  x[i] = fma(c, xr[e], -sn * yr[e]);
+                  y[i] = fma(sn, xr[e], c * yr[e]);
                 }
               }
+              for (int i = lane + NE * T; i < s; i += T) {
+                const double uu = x[i], vv = y[i];
+                x[i] = fma(c, uu, -sn * vv);
+                y[i] = fma(sn, uu, c * vv);
+              }
+              double* vx = V + (size_t)lo * s;
+              double* vy = V + (size_t)hi * s;
+              for (int i0 = lane; i0 < s; i0 += 4 * T) {
+                double uu[4], vv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i = i0 + e * T;
+                  uu[e] = i < s ? vx[i] : 0.0;
+                  vv[e] = i < s ? vy[i] : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int i = i0 + e * T;
+                  if (i < s) {
+                    vx[i] = fma(c, uu[e], -sn * vv[e]);
+                    vy[i] = fma(sn, uu[e], c * vv[e]);
+                  }
+                }
+              }
+              again |= g2 > tc2 * ab;
             }
-            again |= g2 > tc2 * ab;
           }
+          __syncthreads();  // the CTA's columns are private to it this block round
         }
+      }
       grid.sync();
     }
     if (again && lane == 0) atomicOr(&flags[u * 64 + sweep], 1u);
