@@ -161,7 +161,8 @@ def test_exact_matvec_matches_dense(N):
 
 
 def test_union_giant_matches_oracle(N):
-    """A union whose core (s > 160) runs the multi-CTA cooperative Jacobi."""
+    """A giant union (min(m, C) above the giant threshold): cooperative multi-CTA
+    ACA, CholeskyQR2 and block-cyclic Jacobi."""
     from oracle import ifmm_np as O
     rng = np.random.default_rng(11)
     m, ko, kf = 420, 190, 24
