@@ -111,6 +111,22 @@ int ifmm_h2_matvec_part(void* h2, const double* xs, double* ys, double* yv, int 
 int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double* points,
                       const double* x, double* y, int on_device);
 
+/* ---- GMRES Arnoldi on the device:  krylov.py:32-116 -------------------
+ * Device pointers on the context's stream; V holds the Krylov vectors as
+ * rows (row stride ldv >= n).  The Givens rotations and the triangular solve
+ * stay with the caller (host scalars).
+ *   ifmm_krylov_mgs: modified Gram-Schmidt of w against V[0..k1) in order
+ *     (krylov.py:73-75: h_i = <V_i, w>; w -= h_i V_i), then h[k1] = ||w||
+ *     (krylov.py:76).  h is a HOST array of k1+1 doubles; synchronizes.
+ *   ifmm_krylov_div: out = w / hs (krylov.py:104, the next basis vector).
+ *   ifmm_krylov_combine: u = sum_{i<k} y_i V_i in basis order
+ *     (krylov.py:113); y is a HOST array of k doubles.               */
+int ifmm_krylov_mgs(void* ctx, const double* V, long long ldv, int k1, long long n, double* w,
+                    double* h);
+int ifmm_krylov_div(void* ctx, const double* w, long long n, double hs, double* out);
+int ifmm_krylov_combine(void* ctx, const double* V, long long ldv, int k, const double* y,
+                        long long n, double* u);
+
 /* ---- device micro-kernel entry points (tests and benchmarks) ---------- */
 /* C[M,N] = alpha*op(A)op(B) + beta*C on device pointers (row-major). */
 int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,

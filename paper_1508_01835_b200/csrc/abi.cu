@@ -587,4 +587,32 @@ int ifmm_dev_sync(void* ctx) {
   ABI_CATCH
 }
 
+// ---- GMRES Arnoldi on the device (krylov.py:32-116) -----------------------------
+int ifmm_krylov_mgs(void* ctx, const double* V, long long ldv, int k1, long long n, double* w,
+                    double* h) {
+  ABI_TRY
+  if (!ctx || !V || !w || !h || k1 < 0 || n < 1 || ldv < n) throw Error(E_VALUE, "bad MGS arguments");
+  krylov_mgs(*(Ctx*)ctx, V, ldv, k1, n, w, h);
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_krylov_div(void* ctx, const double* w, long long n, double hs, double* out) {
+  ABI_TRY
+  if (!ctx || !w || !out || n < 1) throw Error(E_VALUE, "bad normalisation arguments");
+  krylov_div(*(Ctx*)ctx, w, n, hs, out);
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_krylov_combine(void* ctx, const double* V, long long ldv, int k, const double* y,
+                        long long n, double* u) {
+  ABI_TRY
+  if (!ctx || !V || !u || (k > 0 && !y) || k < 0 || n < 1 || ldv < n)
+    throw Error(E_VALUE, "bad combine arguments");
+  krylov_combine(*(Ctx*)ctx, V, ldv, k, y, n, u);
+  return 0;
+  ABI_CATCH
+}
+
 }  // extern "C"

@@ -187,4 +187,11 @@ Factor* factorize(Graph* g, double eps, double sigma0, int flags);
 void lu_blocked(Ctx& ctx, double* A, int n, int lda, int* piv, int tag);
 void lu_any(Ctx& ctx, double* A, int n, int* piv, int tag);
 
+// device Arnoldi pieces of GMRES (krylov.cu; krylov.py:32-116)
+void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
+                double* h_host);
+void krylov_div(Ctx& C, const double* w, long long n, double hs, double* out);
+void krylov_combine(Ctx& C, const double* V, long long ldv, int k, const double* y_host,
+                    long long n, double* u);
+
 }  // namespace ifmm

@@ -1,0 +1,129 @@
+// Device Arnoldi pieces of the non-restarted GMRES (krylov.py:32-116):
+// modified Gram-Schmidt against the resident basis V (one row per Krylov
+// vector, fp64, row stride ldv), the normalisation V[k+1] = w / h, and the
+// final combination u = sum_i y_i V[i].  The Givens rotations and the
+// triangular solve stay on the host, as SURVEY A18 prescribes (O(k) scalars).
+//
+// HBM-bound: step k of MGS reads V[0..k] once and w (k+1) times; the fused
+// kernel below does "w -= h[i-1] V[i-1]; partial dot(V[i], w)" in one pass, so
+// each projection costs 2 reads + 1 write of n doubles.  Reductions are
+// deterministic (fixed grid, warp shuffles, fixed-order finalisation), so
+// repeated runs are bitwise identical.  The elementwise updates use explicit
+// _rn intrinsics (no FMA contraction) to round exactly like the reference's
+// numpy expressions w - h*V[i], w / h and u + y_i*V[i].
+#include "engine.h"
+
+namespace ifmm {
+namespace {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += red[j];
+  return s;
+}
+
+// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; part[b] = sum over the
+// block's elements of a*c, where (a, c) = (V[i], w) or (w, w) for the norm.
+__global__ void __launch_bounds__(kThreads) k_mgs_pass(const double* __restrict__ V, long long ldv,
+                                                       int i, int norm, long long n,
+                                                       double* __restrict__ w,
+                                                       const double* __restrict__ h,
+                                                       double* __restrict__ part) {
+  __shared__ double red[kThreads / 32];
+  const double* vp = (i > 0) ? V + (long long)(i - 1) * ldv : nullptr;
+  const double* vi = norm ? nullptr : V + (long long)i * ldv;
+  const double hp = (i > 0) ? h[i - 1] : 0.0;
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    double x = w[e];
+    if (vp) {
+      x = __dsub_rn(x, __dmul_rn(hp, vp[e]));
+      w[e] = x;
+    }
+    acc = __fma_rn(norm ? x : vi[e], x, acc);
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// h[slot] = sum(part[0..nb)) in a fixed order (sqrt for the norm slot).
+__global__ void k_mgs_finish(const double* __restrict__ part, int nb, int slot, int norm,
+                             double* __restrict__ h) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) acc += part[j];
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) h[slot] = norm ? sqrt(s) : s;
+}
+
+__global__ void k_div(const double* __restrict__ w, long long n, double hs,
+                      double* __restrict__ out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = __ddiv_rn(w[e], hs);
+}
+
+// u[e] = (((0 + y0 V0) + y1 V1) + ...) in basis order, per element.
+__global__ void k_combine(const double* __restrict__ V, long long ldv, int k,
+                          const double* __restrict__ y, long long n, double* __restrict__ u) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc = __dadd_rn(acc, __dmul_rn(y[i], V[(long long)i * ldv + e]));
+    u[e] = acc;
+  }
+}
+
+int grid_for(long long n) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  long long want = (n + kThreads - 1) / kThreads;
+  long long cap = 4LL * sms;  // 4 resident 512-thread CTAs per SM
+  return (int)std::max(1LL, std::min(want, cap));
+}
+
+}  // namespace
+
+void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
+                double* h_host) {
+  const int nb = grid_for(n);
+  Blk part = C.alloc(1, nb), h = C.alloc(1, k1 + 1);
+  for (int i = 0; i <= k1; ++i) {
+    const int norm = (i == k1);
+    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, norm, n, w, h.p, part.p);
+    k_mgs_finish<<<1, 1024, 0, C.st>>>(part.p, nb, i, norm, h.p);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemcpyAsync(h_host, h.p, 8 * (size_t)(k1 + 1), cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  C.free(part);
+  C.free(h);
+  C.flush();
+}
+
+void krylov_div(Ctx& C, const double* w, long long n, double hs, double* out) {
+  k_div<<<grid_for(n), kThreads, 0, C.st>>>(w, n, hs, out);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+}
+
+void krylov_combine(Ctx& C, const double* V, long long ldv, int k, const double* y_host,
+                    long long n, double* u) {
+  Blk y = C.alloc(1, std::max(k, 1));
+  CUDA_CHECK(cudaMemcpyAsync(y.p, y_host, 8 * (size_t)k, cudaMemcpyHostToDevice, C.st));
+  k_combine<<<grid_for(n), kThreads, 0, C.st>>>(V, ldv, k, y.p, n, u);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  C.free(y);
+  C.flush();
+}
+
+}  // namespace ifmm

@@ -2,9 +2,12 @@
 
 ``h2_matvec`` (krylov.py:119-159) runs on the device (deterministic
 block-sparse products).  ``gmres`` (krylov.py:32-116) is the reference's
-non-restarted MGS/Givens loop written against an array namespace, so it
-runs on numpy arrays or on CUDA torch tensors (``apply_A`` / ``precond``
-decide where the vectors live).
+non-restarted MGS/Givens loop.  With a CUDA torch ``b`` the Krylov basis V is
+resident in HBM and the Arnoldi step (MGS projections + norm), the basis
+normalisation and the final combination run in the engine's kernels
+(``csrc/krylov.cu``); the Givens rotations and the k x k triangular solve stay
+on the host, as in SURVEY A18.  A numpy ``b`` runs the same loop on the host
+(the reference's own array path, for callers whose apply_A is host-side).
 """
 
 from __future__ import annotations
@@ -66,6 +69,8 @@ def gmres(apply_A, b, tol: float = 1e-10, max_iters: int = 500, precond=None,
         is_t = isinstance(b, torch.Tensor)
     except Exception:
         is_t = False
+    if is_t and b.is_cuda:
+        return _gmres_device(apply_A, b, tol, max_iters, precond, side, trace)
     if is_t:
         def dot(u, v): return float(torch.dot(u, v))
         def norm(u): return float(torch.linalg.vector_norm(u))
@@ -131,6 +136,98 @@ def gmres(apply_A, b, tol: float = 1e-10, max_iters: int = 500, precond=None,
         u = zeros(n)
         for i in range(k):
             u = u + float(y[i]) * V[i]
+        x = precond(u) if side == "right" else u
+    trace.iterations = k
+    return x, trace
+
+
+def _gmres_device(apply_A, b, tol, max_iters, precond, side, trace):
+    """krylov.py:32-116 with V resident on the device (rows = Krylov vectors,
+    grown by doubling up to the reference's (max_iters+1) x n), MGS / norm /
+    normalisation / combination in ``csrc/krylov.cu``."""
+    import torch
+    import scipy.linalg as sla
+    lib, ctx = N.lib(), N.ctx()
+    b = b.to(torch.float64).contiguous()
+    n = b.numel()
+
+    def cur_sync():
+        torch.cuda.current_stream().synchronize()
+
+    def ptr(t):
+        return C.c_void_p(t.data_ptr())
+
+    r0 = (precond(b) if side == "left" else b).contiguous()
+    cur_sync()
+    hb = np.zeros(1)
+    N.check(lib.ifmm_krylov_mgs(ctx, ptr(r0), n, 0, n, ptr(r0.clone()),
+                                hb.ctypes.data_as(C.c_void_p)))
+    beta = float(hb[0])
+    if beta == 0.0:
+        trace.converged = True
+        return torch.zeros(n, dtype=torch.float64, device=b.device), trace
+    cap = min(max_iters + 1, 32)
+    V = torch.empty((cap, n), dtype=torch.float64, device=b.device)
+    N.check(lib.ifmm_krylov_div(ctx, ptr(r0), n, beta, ptr(V[0])))
+    H = np.zeros((max_iters + 1, max_iters))
+    cs, sn = np.zeros(max_iters), np.zeros(max_iters)
+    g = np.zeros(max_iters + 1)
+    g[0] = beta
+    hcol = np.zeros(max_iters + 2)
+    k_done, breakdown = 0, False
+    for k in range(max_iters):
+        vk = V[k]
+        if side == "right":
+            w = apply_A(precond(vk))
+        elif side == "left":
+            w = precond(apply_A(vk))
+        else:
+            w = apply_A(vk)
+        w = w.to(torch.float64).contiguous()
+        if w.data_ptr() == vk.data_ptr():
+            w = w.clone()
+        cur_sync()
+        N.check(lib.ifmm_krylov_mgs(ctx, ptr(V), n, k + 1, n, ptr(w),
+                                    hcol.ctypes.data_as(C.c_void_p)))
+        H[:k + 2, k] = hcol[:k + 2]
+        h_sub = H[k + 1, k]
+        for i in range(k):
+            h0 = cs[i] * H[i, k] + sn[i] * H[i + 1, k]
+            H[i + 1, k] = -sn[i] * H[i, k] + cs[i] * H[i + 1, k]
+            H[i, k] = h0
+        nu = np.hypot(H[k, k], H[k + 1, k])
+        if nu == 0.0:
+            k_done, breakdown = k, True
+            break
+        cs[k], sn[k] = H[k, k] / nu, H[k + 1, k] / nu
+        H[k, k], H[k + 1, k] = nu, 0.0
+        g[k + 1] = -sn[k] * g[k]
+        g[k] = cs[k] * g[k]
+        rel = abs(g[k + 1]) / beta
+        trace.residual_history.append(float(rel))
+        k_done = k + 1
+        if rel <= tol:
+            trace.converged = True
+            break
+        if h_sub == 0.0:
+            breakdown = True
+            break
+        if k + 1 >= V.shape[0]:
+            grown = torch.empty((min(max_iters + 1, 2 * V.shape[0]), n), dtype=torch.float64,
+                                device=b.device)
+            grown[:V.shape[0]].copy_(V)
+            torch.cuda.current_stream().synchronize()
+            V = grown
+        N.check(lib.ifmm_krylov_div(ctx, ptr(w), n, float(h_sub), ptr(V[k + 1])))
+    if breakdown and trace.residual_history:
+        trace.converged = trace.residual_history[-1] <= tol
+    k = k_done
+    x = torch.zeros(n, dtype=torch.float64, device=b.device)
+    if k > 0:
+        y = np.ascontiguousarray(sla.solve_triangular(H[:k, :k], g[:k]))
+        u = torch.empty(n, dtype=torch.float64, device=b.device)
+        N.check(lib.ifmm_krylov_combine(ctx, ptr(V), n, k, y.ctypes.data_as(C.c_void_p), n,
+                                        ptr(u)))
         x = precond(u) if side == "right" else u
     trace.iterations = k
     return x, trace
