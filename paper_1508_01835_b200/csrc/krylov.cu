@@ -4,10 +4,11 @@
 // final combination u = sum_i y_i V[i].  The Givens rotations and the
 // triangular solve stay on the host, as SURVEY A18 prescribes (O(k) scalars).
 //
-// HBM-bound: step k of MGS reads V[0..k] once and w (k+1) times; the fused
-// kernel below does "w -= h[i-1] V[i-1]; partial dot(V[i], w)" in one pass, so
-// each projection costs 2 reads + 1 write of n doubles.  Reductions are
-// deterministic (fixed grid, warp shuffles, fixed-order finalisation), so
+// HBM-bound: step k of MGS reads V[0..k] and w (k+1) times; the fused
+// kernel below does "w -= h[i-1] V[i-1]; dot(V[i], w)" in one launch, so
+// each projection costs 3 reads + 1 write of n doubles (V[i-1] mostly from
+// L2).  Reductions are deterministic (fixed grid, warp shuffles, the last
+// block adding the partials in a fixed order), so
 // repeated runs are bitwise identical.  The elementwise updates use explicit
 // _rn intrinsics (no FMA contraction) to round exactly like the reference's
 // numpy expressions w - h*V[i], w / h and u + y_i*V[i].
@@ -29,14 +30,19 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; part[b] = sum over the
-// block's elements of a*c, where (a, c) = (V[i], w) or (w, w) for the norm.
+// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; then the block's partial
+// sum of a*c, where (a, c) = (V[i], w), or (w, w) for the norm pass.  The last
+// block to finish (ticket counter) adds the partials in a fixed order and
+// writes h[i] (sqrt for the norm), so one launch per projection and the
+// result is bitwise reproducible.
 __global__ void __launch_bounds__(kThreads) k_mgs_pass(const double* __restrict__ V, long long ldv,
                                                        int i, int norm, long long n,
                                                        double* __restrict__ w,
-                                                       const double* __restrict__ h,
-                                                       double* __restrict__ part) {
+                                                       double* __restrict__ h,
+                                                       double* __restrict__ part,
+                                                       unsigned int* __restrict__ ticket) {
   __shared__ double red[kThreads / 32];
+  __shared__ bool last;
   const double* vp = (i > 0) ? V + (long long)(i - 1) * ldv : nullptr;
   const double* vi = norm ? nullptr : V + (long long)i * ldv;
   const double hp = (i > 0) ? h[i - 1] : 0.0;
@@ -51,17 +57,21 @@ __global__ void __launch_bounds__(kThreads) k_mgs_pass(const double* __restrict_
     acc = __fma_rn(norm ? x : vi[e], x, acc);
   }
   const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-}
-
-// h[slot] = sum(part[0..nb)) in a fixed order (sqrt for the norm slot).
-__global__ void k_mgs_finish(const double* __restrict__ part, int nb, int slot, int norm,
-                             double* __restrict__ h) {
-  __shared__ double red[32];
-  double acc = 0.0;
-  for (int j = threadIdx.x; j < nb; j += blockDim.x) acc += part[j];
-  const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) h[slot] = norm ? sqrt(s) : s;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int j = threadIdx.x; j < (int)gridDim.x; j += blockDim.x) t += __ldcg(part + j);
+  const double tot = block_sum(t, red);
+  if (threadIdx.x == 0) {
+    h[i] = norm ? sqrt(tot) : tot;
+    *ticket = 0u;  // ready for the next pass (stream order)
+  }
 }
 
 __global__ void k_div(const double* __restrict__ w, long long n, double hs,
@@ -95,12 +105,11 @@ int grid_for(long long n) {
 void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
                 double* h_host) {
   const int nb = grid_for(n);
-  Blk part = C.alloc(1, nb), h = C.alloc(1, k1 + 1);
-  for (int i = 0; i <= k1; ++i) {
-    const int norm = (i == k1);
-    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, norm, n, w, h.p, part.p);
-    k_mgs_finish<<<1, 1024, 0, C.st>>>(part.p, nb, i, norm, h.p);
-  }
+  Blk part = C.alloc(1, nb + 1), h = C.alloc(1, k1 + 1);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(part.p + nb);
+  CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(double), C.st));
+  for (int i = 0; i <= k1; ++i)
+    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, i == k1, n, w, h.p, part.p, ticket);
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaMemcpyAsync(h_host, h.p, 8 * (size_t)(k1 + 1), cudaMemcpyDeviceToHost, C.st));
   C.sync();
