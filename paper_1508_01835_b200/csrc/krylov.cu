@@ -5,10 +5,10 @@
 // triangular solve stay on the host, as SURVEY A18 prescribes (O(k) scalars).
 //
 // HBM-bound: step k of MGS reads V[0..k] and w (k+1) times; the fused
-// kernel below does "w -= h[i-1] V[i-1]; dot(V[i], w)" in one launch, so
+// kernel below does "w -= h[i-1] V[i-1]; partial dot(V[i], w)" in one pass, so
 // each projection costs 3 reads + 1 write of n doubles (V[i-1] mostly from
-// L2).  Reductions are deterministic (fixed grid, warp shuffles, the last
-// block adding the partials in a fixed order), so
+// L2).  Reductions are deterministic (fixed grid, warp shuffles, a one-CTA
+// fixed-order finish), so
 // repeated runs are bitwise identical.  The elementwise updates use explicit
 // _rn intrinsics (no FMA contraction) to round exactly like the reference's
 // numpy expressions w - h*V[i], w / h and u + y_i*V[i].
@@ -30,19 +30,18 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; then the block's partial
-// sum of a*c, where (a, c) = (V[i], w), or (w, w) for the norm pass.  The last
-// block to finish (ticket counter) adds the partials in a fixed order and
-// writes h[i] (sqrt for the norm), so one launch per projection and the
-// result is bitwise reproducible.
-__global__ void __launch_bounds__(kThreads) k_mgs_pass(const double* __restrict__ V, long long ldv,
-                                                       int i, int norm, long long n,
-                                                       double* __restrict__ w,
-                                                       double* __restrict__ h,
-                                                       double* __restrict__ part,
-                                                       unsigned int* __restrict__ ticket) {
+// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; part[b] = sum over the
+// block's elements of a*c, where (a, c) = (V[i], w), or (w, w) for the norm
+// pass.  4 CTAs x 512 threads per SM (32 registers) make the 4 x SMs grid one
+// wave.  A single-launch variant (last block finishing the sum through a
+// ticket counter) measured 2.5% slower at n = 8.4M, so the finish is its own
+// one-CTA launch.
+__global__ void __launch_bounds__(kThreads, 4) k_mgs_pass(const double* __restrict__ V, long long ldv,
+                                                          int i, int norm, long long n,
+                                                          double* __restrict__ w,
+                                                          const double* __restrict__ h,
+                                                          double* __restrict__ part) {
   __shared__ double red[kThreads / 32];
-  __shared__ bool last;
   const double* vp = (i > 0) ? V + (long long)(i - 1) * ldv : nullptr;
   const double* vi = norm ? nullptr : V + (long long)i * ldv;
   const double hp = (i > 0) ? h[i - 1] : 0.0;
@@ -57,24 +56,20 @@ __global__ void __launch_bounds__(kThreads) k_mgs_pass(const double* __restrict_
     acc = __fma_rn(norm ? x : vi[e], x, acc);
   }
   const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = s;
-    __threadfence();
-    last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double t = 0.0;
-  for (int j = threadIdx.x; j < (int)gridDim.x; j += blockDim.x) t += __ldcg(part + j);
-  const double tot = block_sum(t, red);
-  if (threadIdx.x == 0) {
-    h[i] = norm ? sqrt(tot) : tot;
-    *ticket = 0u;  // ready for the next pass (stream order)
-  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void k_div(const double* __restrict__ w, long long n, double hs,
+// h[slot] = sum(part[0..nb)) in a fixed order (sqrt for the norm slot).
+__global__ void k_mgs_finish(const double* __restrict__ part, int nb, int slot, int norm,
+                             double* __restrict__ h) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) acc += part[j];
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) h[slot] = norm ? sqrt(s) : s;
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_div(const double* __restrict__ w, long long n, double hs,
                       double* __restrict__ out) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x)
@@ -105,11 +100,11 @@ int grid_for(long long n) {
 void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
                 double* h_host) {
   const int nb = grid_for(n);
-  Blk part = C.alloc(1, nb + 1), h = C.alloc(1, k1 + 1);
-  unsigned int* ticket = reinterpret_cast<unsigned int*>(part.p + nb);
-  CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(double), C.st));
-  for (int i = 0; i <= k1; ++i)
-    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, i == k1, n, w, h.p, part.p, ticket);
+  Blk part = C.alloc(1, nb), h = C.alloc(1, k1 + 1);
+  for (int i = 0; i <= k1; ++i) {
+    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, i == k1, n, w, h.p, part.p);
+    k_mgs_finish<<<1, 1024, 0, C.st>>>(part.p, nb, i, i == k1, h.p);
+  }
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaMemcpyAsync(h_host, h.p, 8 * (size_t)(k1 + 1), cudaMemcpyDeviceToHost, C.st));
   C.sync();
