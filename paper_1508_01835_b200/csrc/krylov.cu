@@ -12,12 +12,19 @@
 // repeated runs are bitwise identical.  The elementwise updates use explicit
 // _rn intrinsics (no FMA contraction) to round exactly like the reference's
 // numpy expressions w - h*V[i], w / h and u + y_i*V[i].
+#include <cooperative_groups.h>
+
 #include "engine.h"
+
+namespace cg = cooperative_groups;
 
 namespace ifmm {
 namespace {
 
 constexpr int kThreads = 512;
+// vectors up to 32 MB (8 MB rows x the handful touched per pass stay in the
+// 126 MB L2): one cooperative launch per MGS call; above, a launch per pass.
+constexpr long long kCoopMaxN = 1LL << 22;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -69,6 +76,52 @@ __global__ void k_mgs_finish(const double* __restrict__ part, int nb, int slot, 
   if (threadIdx.x == 0) h[slot] = norm ? sqrt(s) : s;
 }
 
+// All k1+1 passes of one MGS call in one cooperative launch (vectors that fit
+// in L2, where the per-pass launch cost dominates).  Same arithmetic as
+// k_mgs_pass + k_mgs_finish: every CTA adds the partials in the same fixed
+// order after a grid barrier, so all CTAs hold the identical h[i].  The
+// partials are double-buffered: pass i+2 overwrites buffer i%2 only after
+// barrier i+1, which every CTA reaches after reading it.
+__global__ void __launch_bounds__(kThreads, 4) k_mgs_coop(const double* __restrict__ V, long long ldv,
+                                                          int k1, long long n, double* __restrict__ w,
+                                                          double* __restrict__ h,
+                                                          double* __restrict__ part) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kThreads / 32];
+  __shared__ double hs;
+  const int nb = gridDim.x;
+  double hp = 0.0;
+  for (int i = 0; i <= k1; ++i) {
+    const int norm = (i == k1);
+    const double* vp = (i > 0) ? V + (long long)(i - 1) * ldv : nullptr;
+    const double* vi = norm ? nullptr : V + (long long)i * ldv;
+    double acc = 0.0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+      double x = w[e];
+      if (vp) {
+        x = __dsub_rn(x, __dmul_rn(hp, vp[e]));
+        w[e] = x;
+      }
+      acc = __fma_rn(norm ? x : vi[e], x, acc);
+    }
+    double* pb = part + (i & 1) * nb;
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0) pb[blockIdx.x] = s;
+    grid.sync();
+    double t = 0.0;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) t += __ldcg(pb + j);
+    __syncthreads();  // red[] reuse
+    const double tot = block_sum(t, red);
+    if (threadIdx.x == 0) {
+      hs = norm ? sqrt(tot) : tot;
+      if (blockIdx.x == 0) h[i] = hs;
+    }
+    __syncthreads();
+    hp = hs;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 4) k_div(const double* __restrict__ w, long long n, double hs,
                       double* __restrict__ out) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -100,7 +153,18 @@ int grid_for(long long n) {
 void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
                 double* h_host) {
   const int nb = grid_for(n);
-  Blk part = C.alloc(1, nb), h = C.alloc(1, k1 + 1);
+  Blk part = C.alloc(1, 2 * nb), h = C.alloc(1, k1 + 1);
+  if (n <= kCoopMaxN) {
+    static int occ = -1;
+    if (occ < 0)
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgs_coop, kThreads, 0));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int g = std::min(nb, std::max(1, occ) * sms);
+    void* args[] = {(void*)&V, (void*)&ldv, (void*)&k1, (void*)&n, (void*)&w, (void*)&h.p,
+                    (void*)&part.p};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_mgs_coop, dim3(g), dim3(kThreads), args, 0, C.st));
+  } else
   for (int i = 0; i <= k1; ++i) {
     k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, i == k1, n, w, h.p, part.p);
     k_mgs_finish<<<1, 1024, 0, C.st>>>(part.p, nb, i, i == k1, h.p);

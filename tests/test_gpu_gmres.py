@@ -17,7 +17,8 @@ def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-@pytest.mark.parametrize("k1,n", [(0, 1), (1, 7), (5, 1000), (40, 65536 + 3), (3, 2_000_000)])
+@pytest.mark.parametrize("k1,n", [(0, 1), (1, 7), (5, 1000), (40, 65536 + 3), (3, 2_000_000),
+                                  (0, 5_000_001), (4, 5_000_001)])
 def test_mgs_step(k1, n):
     """h_i = <V_i, w>; w -= h_i V_i in order (krylov.py:73-75), h[k1] = ||w||
     (krylov.py:76), vs the same loop in numpy."""
