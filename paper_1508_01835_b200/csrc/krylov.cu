@@ -4,11 +4,11 @@
 // final combination u = sum_i y_i V[i].  The Givens rotations and the
 // triangular solve stay on the host, as SURVEY A18 prescribes (O(k) scalars).
 //
-// HBM-bound: step k of MGS reads V[0..k] and w (k+1) times; the fused
-// kernel below does "w -= h[i-1] V[i-1]; partial dot(V[i], w)" in one pass, so
+// HBM-bound: step k of MGS reads V[0..k] and w (k+1) times; each pass of
+// the kernel below does "w -= h[i-1] V[i-1]; partial dot(V[i], w)", so
 // each projection costs 3 reads + 1 write of n doubles (V[i-1] mostly from
-// L2).  Reductions are deterministic (fixed grid, warp shuffles, a one-CTA
-// fixed-order finish), so
+// L2).  Reductions are deterministic (fixed grid, warp shuffles, fixed-order
+// sums of the partials), so
 // repeated runs are bitwise identical.  The elementwise updates use explicit
 // _rn intrinsics (no FMA contraction) to round exactly like the reference's
 // numpy expressions w - h*V[i], w / h and u + y_i*V[i].
@@ -22,9 +22,6 @@ namespace ifmm {
 namespace {
 
 constexpr int kThreads = 512;
-// vectors up to 32 MB (8 MB rows x the handful touched per pass stay in the
-// 126 MB L2): one cooperative launch per MGS call; above, a launch per pass.
-constexpr long long kCoopMaxN = 1LL << 22;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -37,49 +34,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// i-th MGS pass: (if i > 0) w -= h[i-1] * V[i-1]; part[b] = sum over the
-// block's elements of a*c, where (a, c) = (V[i], w), or (w, w) for the norm
-// pass.  4 CTAs x 512 threads per SM (32 registers) make the 4 x SMs grid one
-// wave.  A single-launch variant (last block finishing the sum through a
-// ticket counter) measured 2.5% slower at n = 8.4M, so the finish is its own
-// one-CTA launch.
-__global__ void __launch_bounds__(kThreads, 4) k_mgs_pass(const double* __restrict__ V, long long ldv,
-                                                          int i, int norm, long long n,
-                                                          double* __restrict__ w,
-                                                          const double* __restrict__ h,
-                                                          double* __restrict__ part) {
-  __shared__ double red[kThreads / 32];
-  const double* vp = (i > 0) ? V + (long long)(i - 1) * ldv : nullptr;
-  const double* vi = norm ? nullptr : V + (long long)i * ldv;
-  const double hp = (i > 0) ? h[i - 1] : 0.0;
-  double acc = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    double x = w[e];
-    if (vp) {
-      x = __dsub_rn(x, __dmul_rn(hp, vp[e]));
-      w[e] = x;
-    }
-    acc = __fma_rn(norm ? x : vi[e], x, acc);
-  }
-  const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
-}
-
-// h[slot] = sum(part[0..nb)) in a fixed order (sqrt for the norm slot).
-__global__ void k_mgs_finish(const double* __restrict__ part, int nb, int slot, int norm,
-                             double* __restrict__ h) {
-  __shared__ double red[32];
-  double acc = 0.0;
-  for (int j = threadIdx.x; j < nb; j += blockDim.x) acc += part[j];
-  const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) h[slot] = norm ? sqrt(s) : s;
-}
-
-// All k1+1 passes of one MGS call in one cooperative launch (vectors that fit
-// in L2, where the per-pass launch cost dominates).  Same arithmetic as
-// k_mgs_pass + k_mgs_finish: every CTA adds the partials in the same fixed
-// order after a grid barrier, so all CTAs hold the identical h[i].  The
+// All k1+1 passes of one MGS call in one cooperative launch.  Pass i:
+// (if i > 0) w -= h[i-1] * V[i-1]; block partial of a*c, (a, c) = (V[i], w),
+// or (w, w) for the norm pass; grid barrier; every CTA adds the partials in
+// the same fixed order, so all CTAs hold the identical h[i].  32 registers
+// (launch bounds) keep 4 x 512-thread CTAs resident per SM.  Measured against
+// a launch per pass + a one-CTA finish: n = 8.4M, k1 = 100: 4.47 vs 4.78 ms;
+// n = 1M, k1 = 50: 0.36 vs 0.61 ms (profiles/r01e_gmres_mgs.md).  The
 // partials are double-buffered: pass i+2 overwrites buffer i%2 only after
 // barrier i+1, which every CTA reaches after reading it.
 __global__ void __launch_bounds__(kThreads, 4) k_mgs_coop(const double* __restrict__ V, long long ldv,
@@ -154,21 +115,15 @@ void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, dou
                 double* h_host) {
   const int nb = grid_for(n);
   Blk part = C.alloc(1, 2 * nb), h = C.alloc(1, k1 + 1);
-  if (n <= kCoopMaxN) {
-    static int occ = -1;
-    if (occ < 0)
-      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgs_coop, kThreads, 0));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int g = std::min(nb, std::max(1, occ) * sms);
-    void* args[] = {(void*)&V, (void*)&ldv, (void*)&k1, (void*)&n, (void*)&w, (void*)&h.p,
-                    (void*)&part.p};
-    CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_mgs_coop, dim3(g), dim3(kThreads), args, 0, C.st));
-  } else
-  for (int i = 0; i <= k1; ++i) {
-    k_mgs_pass<<<nb, kThreads, 0, C.st>>>(V, ldv, i, i == k1, n, w, h.p, part.p);
-    k_mgs_finish<<<1, 1024, 0, C.st>>>(part.p, nb, i, i == k1, h.p);
-  }
+  static int occ = -1;
+  if (occ < 0)
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgs_coop, kThreads, 0));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int g = std::min(nb, std::max(1, occ) * sms);
+  void* args[] = {(void*)&V, (void*)&ldv, (void*)&k1, (void*)&n, (void*)&w, (void*)&h.p,
+                  (void*)&part.p};
+  CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_mgs_coop, dim3(g), dim3(kThreads), args, 0, C.st));
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaMemcpyAsync(h_host, h.p, 8 * (size_t)(k1 + 1), cudaMemcpyDeviceToHost, C.st));
   C.sync();

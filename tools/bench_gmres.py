@@ -57,7 +57,7 @@ def main():
                           "alg_bytes": nbytes, "achieved_gbs": round(gbs, 1), "peak_gbs": peak,
                           "frac": round(gbs / peak, 3) if peak else None,
                           "timing": "host clock around the synchronous ABI call (includes "
-                                    "2(k1+1) launches + the h readback)"}))
+                                    "one cooperative launch + the h readback)"}))
 
 
 if __name__ == "__main__":
