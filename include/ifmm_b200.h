@@ -72,10 +72,37 @@ int ifmm_graph_info(void* graph, long long* dim, long long* n_nodes, long long* 
 int ifmm_graph_sigma0(void* graph, const double* omega, int width, int power_iters,
                       double* sigma0_out);
 
+/* Read-only graph view (graph.py:30-216).  nodes: size / kind (0 x, 1 z,
+ * 2 y) / owning cluster per node (n_nodes entries); cluster_nodes: the x, z,
+ * y node of every cluster (-1 if none); edges: the (target, source) keys,
+ * sorted, and the peak edge count; block: one edge block (row-major, r x c;
+ * r = -1 if absent; out NULL queries the shape).                           */
+int ifmm_graph_nodes(void* graph, int* size, int* kind, int* owner);
+int ifmm_graph_cluster_nodes(void* graph, int* nx, int* nz, int* ny);
+int ifmm_graph_edges(void* graph, int* target, int* source, long long* peak_edges);
+int ifmm_graph_block(void* graph, int target, int source, double* out, int* r, int* c);
+/* ExtendedGraph.copy (graph.py:190-216): deep device copy.                */
+void* ifmm_graph_copy(void* graph);
+/* ExtendedGraph.apply / apply_transpose (graph.py:157-170): out = E in or
+ * E^T in over the full node vector (length dim, node order).              */
+int ifmm_graph_apply(void* graph, const double* in, double* out, int transpose, int on_device);
+
 /* ---- factorize:  factor.py:176-230 --------------------------------------
- * Consumes (mutates) the graph like the reference.  flags bit0: exact
- * (non-wave) pair order.                                                   */
+ * Consumes (mutates) the graph like the reference.  flags bit0: strict
+ * (one pair per wave) pair order; bit1: exact SVD for every fill; bit2:
+ * Morton cluster order (one cluster per wave).  Without a normal source the
+ * rSVD sketches come from a counter-based device generator.                */
 void* ifmm_factorize(void* graph, double epsilon, double sigma0, int flags);
+/* The reference's factorize rng, np.random.Generator(PCG64(seed))
+ * (factor.py:188), as a stream of standard normal deviates supplied by the
+ * host: op 0 writes the next n deviates to out; op 1 saves the stream state
+ * in slot n; op 2 restores slot n.  Returns 0 on success.                  */
+typedef int (*ifmm_normal_source)(void* user, int op, long long n, double* out);
+/* factorize drawing every Gaussian the reference draws (rSVD sketches,
+ * lowrank.py:108; _extend_update, factor.py:350) from `src` in the
+ * reference's order; implies Morton cluster order (flags bit2).           */
+void* ifmm_factorize_rng(void* graph, double epsilon, double sigma0, int flags,
+                         ifmm_normal_source src, void* user);
 void ifmm_factor_destroy(void* factor);
 /* Scalar stats: out[0..] = peak_edges, n_clusters, max_basis_rank,
  * max_fill_rank, forced_rank_truncations, n_levels, n_events_elim,
@@ -86,10 +113,23 @@ int ifmm_factor_stats(void* factor, long long* out, int n_out);
 int ifmm_factor_level_stats(void* factor, long long* out, int n_levels);
 /* Ranks list of one level (n_ranks entries). */
 int ifmm_factor_level_ranks(void* factor, int level_index, int* out);
-/* Timings (seconds): lu_and_triangular_solves, matmul_updates,
- * lowrank_approximations, operator_transfer, total, gemm_flops (count),
- * all_flops (count).                                                       */
+/* Timings (seconds; factor.py:71-72 buckets, device time between bucket
+ * switches on the engine stream): lu_and_triangular_solves, matmul_updates,
+ * lowrank_approximations, operator_transfer, then total (host wall),
+ * gemm_flops (count), all_flops (count), rSVD rounds, rSVD re-draws.       */
 int ifmm_factor_timings(void* factor, double* out, int n_out);
+/* Event log (factor.py:80, IFMMFactorization.events) as flat int64 records:
+ *   elim   0, nx, nz, ny, size_x, size_z, n_src, n_tgt, src nodes, tgt nodes
+ *   rebase 1, ny
+ *   merge  2, px, n_parts, (child y node, size) pairs
+ * Returns the record length; writes only when out has room (cap).       */
+long long ifmm_factor_events(void* factor, long long* out, long long cap);
+/* top_nodes / top_sizes / init_sizes / leaf_slices (factor.py:77-92);
+ * sizes[0..2] = n_top, n_init, n_leaves.  Any array may be NULL.         */
+int ifmm_factor_layout(void* factor, int* sizes, int* top_nodes, int* top_sizes, int* init_sizes,
+                       int* leaf_nodes, int* leaf_start, int* leaf_stop);
+/* FillinStats.compress_time per level (device s in lowrank_approximations). */
+int ifmm_factor_level_times(void* factor, double* out, int n_levels);
 /* IFMMFactorization.solve (factor.py:99-157): b, x length N (original
  * order), host or device pointers.                                         */
 int ifmm_solve(void* factor, const double* b, double* x, int on_device);
@@ -138,6 +178,9 @@ int ifmm_dev_svd(void* ctx, int m, int n, const double* A, double thr, double* U
 /* LU with partial pivoting + solve of nrhs right-hand sides (device). */
 int ifmm_dev_lu_solve(void* ctx, int n, double* A, int* piv, double* X, int nrhs);
 /* weighted_basis_union (lowrank.py:166-199) on device pointers. */
+/* Orthonormal basis of a tall row-major n x w device matrix Y into Q
+ * (n x w row-major): np.linalg.qr(Y)[0] (lowrank.py:74-76).               */
+int ifmm_dev_orth(void* ctx, int n, int w, const double* Y, double* Q);
 int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const double* w,
                    const double* F, const double* wf, double thr, int min_rank,
                    double* NB, double* NW, double* OM, double* FM, int* rank);
@@ -163,6 +206,17 @@ int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* c
  * [16..24] the first nine for 256 < m <= 600, [25..33] for m > 600);
  * reset != 0 clears. */
 int ifmm_union_profile(unsigned long long* out, int reset);
+/* Dense kernel matrix out (m x n row-major) = K(|P_i - Q_j|) evaluated on
+ * the device (dense.py:23-32, dense_matrix).  P (m x 3), Q (n x 3).       */
+int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const double* P, int n,
+                       const double* Q, double* out, int on_device);
+/* block_diag_preconditioner (krylov.py:172-196): LU of the diagonal blocks
+ * of A (n x n, ld lda; last block shorter) on the device; apply solves them
+ * blockwise.  A singular block fails with status 2.                       */
+void* ifmm_blockdiag_create(void* ctx, const double* A, int n, int lda, int block_size,
+                            int on_device);
+int ifmm_blockdiag_apply(void* bd, const double* v, double* out, int on_device);
+void ifmm_blockdiag_destroy(void* bd);
 /* Diagnostics: phase times (s) of the last factorize when IFMM_PROFILE=1. */
 int ifmm_profile(double* out, int n);
 

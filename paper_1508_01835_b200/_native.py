@@ -45,8 +45,23 @@ _SIGS = {
     "ifmm_graph_build": (vp, [vp, C.c_int]),
     "ifmm_graph_destroy": (None, [vp]),
     "ifmm_graph_info": (C.c_int, [vp, lp, lp, lp]),
+    "ifmm_graph_nodes": (C.c_int, [vp, ip, ip, ip]),
+    "ifmm_graph_cluster_nodes": (C.c_int, [vp, ip, ip, ip]),
+    "ifmm_graph_edges": (C.c_int, [vp, ip, ip, lp]),
+    "ifmm_graph_block": (C.c_int, [vp, C.c_int, C.c_int, dp, ip, ip]),
+    "ifmm_graph_copy": (vp, [vp]),
+    "ifmm_graph_apply": (C.c_int, [vp, vp, vp, C.c_int, C.c_int]),
     "ifmm_graph_sigma0": (C.c_int, [vp, dp, C.c_int, C.c_int, dp]),
     "ifmm_factorize": (vp, [vp, C.c_double, C.c_double, C.c_int]),
+    "ifmm_factorize_rng": (vp, [vp, C.c_double, C.c_double, C.c_int, vp, vp]),
+    "ifmm_factor_level_times": (C.c_int, [vp, dp, C.c_int]),
+    "ifmm_factor_events": (C.c_longlong, [vp, lp, C.c_longlong]),
+    "ifmm_factor_layout": (C.c_int, [vp, ip, ip, ip, ip, ip, ip, ip]),
+    "ifmm_kernel_matrix": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, vp, C.c_int, vp, vp,
+                                     C.c_int]),
+    "ifmm_blockdiag_create": (vp, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ifmm_blockdiag_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "ifmm_blockdiag_destroy": (None, [vp]),
     "ifmm_factor_destroy": (None, [vp]),
     "ifmm_factor_stats": (C.c_int, [vp, lp, C.c_int]),
     "ifmm_factor_level_stats": (C.c_int, [vp, lp, C.c_int]),
@@ -68,6 +83,7 @@ _SIGS = {
     "ifmm_dev_lu_solve": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),
     "ifmm_dev_union": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_double,
                                  C.c_int, vp, vp, vp, vp, vp]),
+    "ifmm_dev_orth": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "ifmm_dev_sync": (C.c_int, [vp]),
     "ifmm_dev_jacobi_bench": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(C.c_ulonglong)]),
     "ifmm_exact_matvec": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, vp, vp, vp, C.c_int]),

@@ -138,7 +138,7 @@ void ifmm_tree_destroy(void* p) {
   if (!p) return;
   Tree* t = (Tree*)p;
   if (t->ctx) {
-    t->ctx->sync();
+    t->ctx->sync_nothrow();
     t->ctx->free_raw(t->d_points, t->d_points_cls);
     t->ctx->free_raw(t->d_perm, t->d_perm_cls);
     t->ctx->flush();
@@ -195,7 +195,7 @@ void* ifmm_h2_build(void* tree, int kernel_kind, double p0, int n_cheb, double e
 void ifmm_h2_destroy(void* p) {
   if (!p) return;
   H2* h = (H2*)p;
-  h->ctx->sync();
+  h->ctx->sync_nothrow();
   delete h;
 }
 
@@ -318,7 +318,7 @@ void* ifmm_graph_build(void* h2, int consume) {
 void ifmm_graph_destroy(void* p) {
   if (!p) return;
   Graph* g = (Graph*)p;
-  g->ctx->sync();
+  g->ctx->sync_nothrow();
   delete g;
 }
 
@@ -328,6 +328,82 @@ int ifmm_graph_info(void* p, long long* dim, long long* nn, long long* ne) {
   *nn = (long long)g->size.size();
   *ne = (long long)g->E.size();
   return 0;
+}
+
+// ---- read-only graph view (graph.py:30-216 attributes) ------------------------
+int ifmm_graph_nodes(void* p, int* size, int* kind, int* owner) {
+  Graph* g = (Graph*)p;
+  for (size_t i = 0; i < g->size.size(); ++i) {
+    if (size) size[i] = g->size[i];
+    if (kind) kind[i] = g->kind[i];
+    if (owner) owner[i] = g->owner[i];
+  }
+  return 0;
+}
+
+int ifmm_graph_cluster_nodes(void* p, int* nx, int* nz, int* ny) {
+  Graph* g = (Graph*)p;
+  for (size_t c = 0; c < g->nx.size(); ++c) {
+    nx[c] = g->nx[c]; nz[c] = g->nz[c]; ny[c] = g->ny[c];
+  }
+  return 0;
+}
+
+int ifmm_graph_edges(void* p, int* t, int* s, long long* peak_edges) {
+  Graph* g = (Graph*)p;
+  std::vector<uint64_t> keys;
+  keys.reserve(g->E.size());
+  for (auto& kv : g->E) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());
+  for (size_t i = 0; i < keys.size(); ++i) {
+    t[i] = (int)(keys[i] >> 32);
+    s[i] = (int)(keys[i] & 0xffffffffu);
+  }
+  if (peak_edges) *peak_edges = g->peak_edges;
+  return 0;
+}
+
+int ifmm_graph_block(void* p, int t, int s, double* out, int* r, int* c) {
+  ABI_TRY
+  Graph* g = (Graph*)p;
+  if (g->consumed) throw Error(E_VALUE, "graph already factorized");
+  Blk* b = g->get(t, s);
+  if (!b) { *r = -1; *c = -1; return 0; }
+  *r = b->r; *c = b->c;
+  if (out && b->r * b->c > 0) {
+    CUDA_CHECK(cudaMemcpyAsync(out, b->p, 8 * (size_t)b->r * b->c, cudaMemcpyDeviceToHost,
+                               g->ctx->st));
+    g->ctx->sync();
+  }
+  return 0;
+  ABI_CATCH
+}
+
+void* ifmm_graph_copy(void* p) {
+  ABI_TRY
+  Graph* g = (Graph*)p;
+  if (g->consumed) throw Error(E_VALUE, "graph already factorized");
+  return g->clone();
+  ABI_CATCH_NULL
+}
+
+int ifmm_graph_apply(void* p, const double* in, double* out, int transpose, int on_device) {
+  ABI_TRY
+  Graph* g = (Graph*)p;
+  if (g->consumed) throw Error(E_VALUE, "graph already factorized");
+  Ctx& C = *g->ctx;
+  const long long dim = g->dim();
+  Blk I = C.alloc(1, (int)std::max<long long>(dim, 1)), O = C.alloc(1, (int)std::max<long long>(dim, 1));
+  const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CUDA_CHECK(cudaMemcpyAsync(I.p, in, 8 * (size_t)dim, kin, C.st));
+  g->apply(I.p, O.p, transpose != 0);
+  CUDA_CHECK(cudaMemcpyAsync(out, O.p, 8 * (size_t)dim, kout, C.st));
+  C.sync();
+  C.free(I); C.free(O);
+  C.flush();
+  return 0;
+  ABI_CATCH
 }
 
 int ifmm_graph_sigma0(void* p, const double* omega, int width, int power_iters, double* out) {
@@ -346,10 +422,17 @@ void* ifmm_factorize(void* graph, double epsilon, double sigma0, int flags) {
   ABI_CATCH_NULL
 }
 
+void* ifmm_factorize_rng(void* graph, double epsilon, double sigma0, int flags,
+                         ifmm_normal_source src, void* user) {
+  ABI_TRY
+  return factorize((Graph*)graph, epsilon, sigma0, flags, src, user);
+  ABI_CATCH_NULL
+}
+
 void ifmm_factor_destroy(void* p) {
   if (!p) return;
   Factor* f = (Factor*)p;
-  f->ctx->sync();
+  f->ctx->sync_nothrow();
   delete f;
 }
 
@@ -394,8 +477,62 @@ int ifmm_factor_level_ranks(void* p, int li, int* out) {
 
 int ifmm_factor_timings(void* p, double* out, int n) {
   Factor* f = (Factor*)p;
-  double v[7] = {f->t_lu, f->t_mm, f->t_lr, f->t_tr, f->t_total, f->gemm_flops, f->all_flops};
-  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+  double v[9] = {f->t_lu, f->t_mm, f->t_lr, f->t_tr, f->t_total, f->gemm_flops, f->all_flops,
+                 (double)f->rsvd_rounds, (double)f->rsvd_redraws};
+  for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
+  return 0;
+}
+
+// Event log and layout (factor.py:77-92): flat int64 records.  Returns the
+// number of int64 written (or needed when out is NULL / cap too small).
+// elim:   0, nx, nz, ny, size_x, size_z, n_src, n_tgt, src..., tgt...
+// rebase: 1, ny
+// merge:  2, px, n_parts, (child y, size)...
+long long ifmm_factor_events(void* p, long long* out, long long cap) {
+  Factor* f = (Factor*)p;
+  std::vector<long long> v;
+  for (auto& e : f->events) {
+    if (e.type == 0) {
+      const ElimEv& x = f->elims[e.idx];
+      v.insert(v.end(), {0, x.nx, x.nz, x.ny, x.m, x.k, (long long)x.src.size(),
+                         (long long)x.tgt.size()});
+      v.insert(v.end(), x.src.begin(), x.src.end());
+      v.insert(v.end(), x.tgt.begin(), x.tgt.end());
+    } else if (e.type == 1) {
+      v.insert(v.end(), {1, f->rebases[e.idx].ny});
+    } else {
+      const MergeEv& m = f->merges[e.idx];
+      v.insert(v.end(), {2, m.px, (long long)m.parts.size()});
+      for (size_t i = 0; i < m.parts.size(); ++i) v.insert(v.end(), {m.parts[i], m.psize[i]});
+    }
+  }
+  if (out && cap >= (long long)v.size()) std::copy(v.begin(), v.end(), out);
+  return (long long)v.size();
+}
+
+// top_nodes, top_sizes (n_top each), init_sizes (n_init), leaf x nodes /
+// point start / stop (n_leaves each).  sizes: out[0..2] = n_top, n_init,
+// n_leaves when the arrays are NULL.
+int ifmm_factor_layout(void* p, int* sizes, int* top_nodes, int* top_sizes, int* init_sizes,
+                       int* leaf_nodes, int* leaf_start, int* leaf_stop) {
+  Factor* f = (Factor*)p;
+  if (sizes) {
+    sizes[0] = (int)f->top_nodes.size();
+    sizes[1] = (int)f->init_sizes.size();
+    sizes[2] = (int)f->leaf_nodes.size();
+  }
+  if (top_nodes) std::copy(f->top_nodes.begin(), f->top_nodes.end(), top_nodes);
+  if (top_sizes) std::copy(f->top_sizes.begin(), f->top_sizes.end(), top_sizes);
+  if (init_sizes) std::copy(f->init_sizes.begin(), f->init_sizes.end(), init_sizes);
+  if (leaf_nodes) std::copy(f->leaf_nodes.begin(), f->leaf_nodes.end(), leaf_nodes);
+  if (leaf_start) std::copy(f->leaf_start.begin(), f->leaf_start.end(), leaf_start);
+  if (leaf_stop) std::copy(f->leaf_stop.begin(), f->leaf_stop.end(), leaf_stop);
+  return 0;
+}
+
+int ifmm_factor_level_times(void* p, double* out, int n) {
+  Factor* f = (Factor*)p;
+  for (int i = 0; i < n && i < (int)f->levels.size(); ++i) out[i] = f->levels[i].compress_time;
   return 0;
 }
 
@@ -506,6 +643,138 @@ int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double
   ABI_CATCH
 }
 
+// ---- dense kernel matrix (dense.py:23-32) ---------------------------------------
+int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const double* P, int n,
+                       const double* Q, double* out, int on_device) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
+  if (m < 0 || n < 0) throw Error(E_VALUE, "negative matrix size");
+  if ((long long)m * n == 0) return 0;
+  KernelSpec k{kernel_kind, p0};
+  const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  Blk dP = C.alloc(m, 3), dQ = C.alloc(n, 3);
+  CUDA_CHECK(cudaMemcpyAsync(dP.p, P, 24 * (size_t)m, kin, C.st));
+  CUDA_CHECK(cudaMemcpyAsync(dQ.p, Q, 24 * (size_t)n, kin, C.st));
+  // row panels of <= 8 rows: one CTA each, entries in row-major order
+  const int rows = 8;
+  const long long panel = (long long)rows * n;
+  Blk O;
+  double* dst = out;
+  if (!on_device) { O = C.alloc(m, n); dst = O.p; }
+  std::vector<EvalDesc> ed;
+  for (int r0 = 0; r0 < m; r0 += rows) {
+    EvalDesc d;
+    d.P = dP.p + 3 * (size_t)r0; d.Q = dQ.p; d.m = std::min(rows, m - r0); d.n = n;
+    d.out = dst + (size_t)r0 * n; d.ldo = n;
+    ed.push_back(d);
+  }
+  (void)panel;
+  launch_eval(C.stage.push_vec(C, ed), (int)ed.size(), k, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  if (!on_device)
+    CUDA_CHECK(cudaMemcpyAsync(out, O.p, 8 * (size_t)m * n, cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  C.free(dP); C.free(dQ); C.free(O);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
+// ---- block-diagonal preconditioner (krylov.py:172-196) ---------------------------
+struct BlockDiag {
+  Ctx* ctx;
+  int n, bs;
+  Blk lu;                 // the diagonal blocks, factored in place, back to back
+  int* piv = nullptr;
+  int piv_cls = -1;
+  std::vector<LuDesc> lus;
+  std::vector<int> off;   // block row offsets (nb + 1)
+};
+
+void* ifmm_blockdiag_create(void* ctx, const double* A, int n, int lda, int block_size,
+                            int on_device) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  if (block_size < 1 || block_size > n) throw Error(E_VALUE, "block_size must be in [1, n]");
+  BlockDiag* B = new BlockDiag;
+  B->ctx = &C; B->n = n; B->bs = block_size;
+  long long tot = 0;
+  for (int a = 0; a < n; a += block_size) {
+    const int b = std::min(n, a + block_size);
+    B->off.push_back(a);
+    tot += (long long)(b - a) * (b - a);
+  }
+  B->off.push_back(n);
+  B->lu = C.alloc(1, (int)tot);
+  B->piv = C.arena.alloc_int(n, &B->piv_cls);
+  const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  long long o = 0;
+  for (size_t i = 0; i + 1 < B->off.size(); ++i) {
+    const int a = B->off[i], w = B->off[i + 1] - a;
+    CUDA_CHECK(cudaMemcpy2DAsync(B->lu.p + o, 8 * (size_t)w, A + (size_t)a * lda + a, 8 * (size_t)lda,
+                                 8 * (size_t)w, w, kin, C.st));
+    LuDesc d;
+    d.A = B->lu.p + o; d.n = w; d.lda = w; d.piv = B->piv + a; d.tag = a;
+    B->lus.push_back(d);
+    o += (long long)w * w;
+  }
+  std::vector<LuDesc> small, big;
+  for (auto& d : B->lus) (d.n <= 160 ? small : big).push_back(d);
+  if (!small.empty()) launch_lu(C.stage.push_vec(C, small), (int)small.size(), C.d_status, C.st);
+  for (auto& d : big) lu_blocked(C, d.A, d.n, d.n, d.piv, d.tag);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  try {
+    C.check_status("diagonal block at row ");
+  } catch (...) {
+    C.free(B->lu);
+    C.free_raw(B->piv, B->piv_cls);
+    C.flush();
+    delete B;
+    throw;
+  }
+  return B;
+  ABI_CATCH_NULL
+}
+
+int ifmm_blockdiag_apply(void* h, const double* v, double* out, int on_device) {
+  ABI_TRY
+  BlockDiag& B = *(BlockDiag*)h;
+  Ctx& C = *B.ctx;
+  const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  Blk X = C.alloc(1, B.n);
+  CUDA_CHECK(cudaMemcpyAsync(X.p, v, 8 * (size_t)B.n, kin, C.st));
+  std::vector<LuSolveDesc> sd;
+  int maxn = 0;
+  for (size_t i = 0; i < B.lus.size(); ++i) {
+    LuSolveDesc d;
+    d.LU = B.lus[i].A; d.piv = B.lus[i].piv; d.n = B.lus[i].n; d.lda = B.lus[i].n;
+    d.X = X.p + B.off[i]; d.nrhs = 1; d.ldx = 1;
+    sd.push_back(d);
+    maxn = std::max(maxn, d.n);
+  }
+  launch_lusolve(C.stage.push_vec(C, sd), (int)sd.size(), 1, C.st, maxn);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemcpyAsync(out, X.p, 8 * (size_t)B.n, kout, C.st));
+  C.sync();
+  C.free(X);
+  C.flush();
+  return 0;
+  ABI_CATCH
+}
+
+void ifmm_blockdiag_destroy(void* h) {
+  if (!h) return;
+  BlockDiag* B = (BlockDiag*)h;
+  B->ctx->sync_nothrow();
+  B->ctx->free(B->lu);
+  B->ctx->free_raw(B->piv, B->piv_cls);
+  B->ctx->flush();
+  delete B;
+}
+
 // ---- micro-kernel entry points --------------------------------------------------
 int ifmm_dev_gemm(void* ctx, int M, int N, int K, const double* A, int lda, int ta,
                   const double* B, int ldb, int tb, double* Cm, int ldc, double alpha,
@@ -547,6 +816,19 @@ int ifmm_dev_lu_solve(void* ctx, int n, double* A, int* piv, double* X, int nrhs
   CUDA_CHECK(cudaGetLastError());
   C.sync();
   C.check_status("test ");
+  return 0;
+  ABI_CATCH
+}
+
+int ifmm_dev_orth(void* ctx, int n, int w, const double* Y, double* Q) {
+  ABI_TRY
+  Ctx& C = *(Ctx*)ctx;
+  Blk wk = C.alloc(1, 2 * n * w + 2 * w + 64);
+  launch_tall_orth(Y, n, w, Q, wk.p, C.st);
+  CUDA_CHECK(cudaGetLastError());
+  C.sync();
+  C.free(wk);
+  C.flush();
   return 0;
   ABI_CATCH
 }

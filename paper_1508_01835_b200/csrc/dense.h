@@ -93,7 +93,15 @@ void launch_union(const UnionDesc* d_descs, int n, double thr, cudaStream_t s, i
                   int jac_smem_doubles = 0, const UnionDesc* d_giants = nullptr, int n_giants = 0,
                   int max_giant_s = 0, double* d_scratch = nullptr, int max_giant_m = 0,
                   int max_giant_C = 0, int sm_reserved = 0);
-inline int union_giant_scratch_doubles(int n_giants) { return 32 * n_giants + 2 * 160 + 8; }
+// 64 flag words (32 doubles) per giant, the done counter (8 doubles), then 2
+// candidate slots per CTA of the cooperative ACA grid: that grid has at most
+// max(sm_free, n_giants) <= max(148, n_giants) CTAs.
+inline int union_giant_scratch_doubles(int n_giants) {
+  return 32 * n_giants + 8 + 2 * (n_giants > 148 ? n_giants : 148) + 8;
+}
+// giants per launch: beyond this the rest of a wave's large unions take the
+// single-CTA global-workspace path (every cooperative grid stays co-resident)
+constexpr int kMaxGiantsPerLaunch = 96;
 // s_max above which a global-workspace union is "giant" (multi-CTA ACA,
 // CholeskyQR, core SVD and output); IFMM_GIANT overrides (diagnostics)
 int giant_union_threshold();

@@ -118,6 +118,8 @@ struct Graph {
     return d;
   }
   double sigma0(const double* omega, int width, int power_iters);
+  Graph* clone() const;
+  void apply(const double* d_in, double* d_out, bool transpose);
 };
 
 // ---- factorization ---------------------------------------------------------
@@ -125,6 +127,7 @@ struct LevelStats {
   int level = 0;
   long long compressed = 0, added = 0, dropped = 0, forced = 0;
   std::vector<int> ranks;
+  double compress_time = 0.0;  // device s in lowrank_approximations (FillinStats.compress_time)
 };
 
 struct ElimEv {
@@ -173,6 +176,7 @@ struct Factor {
   long long peak_edges = 0, n_clusters = 0, max_basis_rank = 0;
   double t_lu = 0, t_mm = 0, t_lr = 0, t_tr = 0, t_total = 0;
   double gemm_flops = 0, all_flops = 0;
+  unsigned long long rsvd_rounds = 0, rsvd_redraws = 0;
   // solve program (built once after factorization)
   struct Program;
   Program* prog = nullptr;
@@ -181,7 +185,14 @@ struct Factor {
   void solve(const double* d_b_orig, double* d_x_orig);
 };
 
-Factor* factorize(Graph* g, double eps, double sigma0, int flags);
+// Standard-normal source of the reference's factorize rng (see
+// ifmm_normal_source in include/ifmm_b200.h): op 0 draws n deviates into
+// out, op 1 saves the stream state in slot n, op 2 restores slot n.
+typedef int (*NormalSource)(void* user, int op, long long n, double* out);
+// flags bit0: strict pair order (one pair per wave); bit1: exact SVD for every
+// fill; bit2: Morton cluster order (one cluster per wave; implied by src).
+Factor* factorize(Graph* g, double eps, double sigma0, int flags, NormalSource src = nullptr,
+                  void* src_user = nullptr);
 
 // blocked LU for large pivot blocks (host-driven panels)
 void lu_blocked(Ctx& ctx, double* A, int n, int lda, int* piv, int tag);

@@ -47,7 +47,16 @@ struct Phase {
   Ctx& C;
   int id;
   std::chrono::steady_clock::time_point t0;
+  static int bucket_of(int ph) {
+    switch (ph) {
+      case PH_LU: case PH_XSOLVE: case PH_TOP: return 0;   // lu_and_triangular_solves
+      case PH_SCHUR: case PH_ADD: return 1;                // matmul_updates
+      case PH_MERGE: return 3;                             // operator_transfer
+      default: return 2;                                   // lowrank_approximations
+    }
+  }
   Phase(Ctx& c, int i) : C(c), id(i) {
+    C.bucket(bucket_of(i));
     if (prof_on()) { if (prof_mode() == 1) C.sync(); t0 = std::chrono::steady_clock::now(); }
   }
   ~Phase() {
@@ -65,6 +74,7 @@ static FILE* trace_file() {
     init = true;
     const char* p = getenv("IFMM_TRACE");
     if (p && *p) f = fopen(p, "w");
+    if (f) setvbuf(f, nullptr, _IOLBF, 0);  // complete lines even if the process dies
   }
   return f;
 }
@@ -122,6 +132,19 @@ struct Eliminator {
   Blk d_ranks;  // device int scratch
   int d_ranks_cap = 0;
   double flops_gemm = 0, flops_all = 0;
+
+  // the reference's factorize rng (factor.py:188, Generator(PCG64(seed))):
+  // when set, every Gaussian the reference draws -- rSVD sketches
+  // (lowrank.py:108) and _extend_update padding (factor.py:350) -- comes
+  // from this stream in the reference's call order
+  NormalSource src = nullptr;
+  void* src_user = nullptr;
+  void draw(double* out, long long n) {
+    if (src(src_user, 0, n, out) != 0) throw Error(E_VALUE, "normal source callback failed");
+  }
+  void src_op(int op, long long slot) {
+    if (src(src_user, op, slot, nullptr) != 0) throw Error(E_VALUE, "normal source callback failed");
+  }
 
   Eliminator(Ctx& c, Graph& gg, Factor& f, double t, unsigned long long seed)
       : C(c), g(gg), F(f), thr(t), rng(seed) {}
@@ -224,7 +247,7 @@ struct Eliminator {
       const int sm = std::min(u.m, u.k_old + u.k_f);
       u.giant = 0;
       if (union_fits_smem(u.m, u.k_old, u.k_f)) { us.push_back(u); continue; }
-      if (sm > giant_union_threshold()) {
+      if (sm > giant_union_threshold() && (int)giants.size() < kMaxGiantsPerLaunch) {
         u.giant = 1;
         giants.push_back(u);
         max_gs = std::max(max_gs, sm);
@@ -356,8 +379,14 @@ struct Eliminator {
       k.push_back(((unsigned long long)(unsigned)it.first.first << 32) | (unsigned)it.first.second);
     return k;
   }
+  struct RsvdAct { int i, m, n, full, k_try; };
+  std::vector<int> rsvd_round(std::vector<SvdDesc>& sd, std::vector<RsvdAct>& act,
+                              const std::vector<unsigned long long>* keys,
+                              const std::vector<double>* h_omega);
   void rsvd_fills(std::vector<SvdDesc>& sd, const std::vector<int>& big,
                   const std::vector<unsigned long long>& keys, int* dr);
+  void rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>& order);
+  unsigned long long rsvd_redraws = 0;
   void merge(int level);
   void top();
 };
@@ -371,9 +400,17 @@ void Eliminator::extend(BU& b, int kt, const Blk& cur_basis, int basis_is_v, con
   // Materialise the basis as a computed update (col-major m x cap) if needed
   IFMM_ASSERT(!b.identity, "extend of an identity update must be materialised first");
   // host Gaussians (deterministic stream), device orthogonalisation
-  std::normal_distribution<double> nd(0.0, 1.0);
   std::vector<double> G((size_t)m * extra);
-  for (auto& x : G) x = nd(rng);
+  if (src) {
+    // rng.standard_normal((m, extra)) is row-major; launch_extend wants m x extra col-major
+    std::vector<double> R((size_t)m * extra);
+    draw(R.data(), (long long)R.size());
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < extra; ++j) G[(size_t)j * m + i] = R[(size_t)i * extra + j];
+  } else {
+    std::normal_distribution<double> nd(0.0, 1.0);
+    for (auto& x : G) x = nd(rng);
+  }
   Blk Gd = C.alloc(m, extra);
   CUDA_CHECK(cudaMemcpyAsync(Gd.p, G.data(), G.size() * 8, cudaMemcpyHostToDevice, C.st));
   // grow capacity
@@ -1098,7 +1135,21 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     else if (dss) launch_svd(dss, (int)sds.size(), thr, smem_dim, C.st, 0);
     else if (dsg) launch_svd(dsg, (int)sdg.size(), thr, 0, C.st, 0);
     C.kt_end(K_SVD, sflops, ka);
-    if (!big.empty()) rsvd_fills(sd, big, items_key(items), dr);
+    if (!big.empty()) {
+      if (src) {
+        // reference call order: cluster (wave slot), pair (min, max), F_kj (target = max) first
+        std::vector<int> order(big);
+        auto rk = [&](int i) {
+          const auto& k = items[i].first;
+          const int lo = std::min(k.first, k.second), hi = std::max(k.first, k.second);
+          return std::make_tuple(items[i].second.wi, lo, hi, k.first == hi ? 0 : 1);
+        };
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return rk(a) < rk(b); });
+        rsvd_fills_ref(sd, order);
+      } else {
+        rsvd_fills(sd, big, items_key(items), dr);
+      }
+    }
     const int* hr = C.readback_ints(dr, ns);
     for (int i = 0; i < ns; ++i) {
       fac[i].U = sd[i].U; fac[i].S = sd[i].S; fac[i].V = sd[i].V;
@@ -1134,80 +1185,146 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
 // Randomized SVD of the large fills (lowrank.py:79-125, start_rank 16,
 // oversample 10, 2 power iterations, rank doubling), batched across the
 // fills: sketch, GEMMs (grouped DMMA), orthonormalisation and the final
-// small SVD are one launch each per round; the host re-runs the fills whose
-// doubling test has not stopped.  Writes rank into dr[i].
+// small SVD are one launch each per round.  rsvd_round runs one round for
+// every active fill and returns the reference's "stop doubling" flags.
+// h_omega (optional): the sketches, concatenated in `act` order, each
+// n x w row-major exactly as rng.standard_normal((n, w)) (lowrank.py:108);
+// without it a counter-based device generator draws them.
+std::vector<int> Eliminator::rsvd_round(std::vector<SvdDesc>& sd, std::vector<RsvdAct>& act,
+                                        const std::vector<unsigned long long>* keys,
+                                        const std::vector<double>* h_omega) {
+  ++rsvd_calls;
+  const int na = (int)act.size();
+  std::vector<Blk> Om(na), Yt(na), Zt(na), Ow(na), Fw(na);
+  std::vector<RandDesc> rd;
+  std::vector<OrthDesc> od;
+  std::vector<RsvdFinDesc> fd;
+  GemmBatch g0, g1, g2;
+  Blk stopb = C.alloc(1, na / 2 + 2);
+  int* d_stop = reinterpret_cast<int*>(stopb.p);
+  Blk omb;
+  if (h_omega) {
+    omb = C.alloc(1, (int)std::max<size_t>(h_omega->size(), 1));
+    CUDA_CHECK(cudaMemcpyAsync(omb.p, h_omega->data(), h_omega->size() * 8, cudaMemcpyHostToDevice,
+                               C.st));
+  }
+  size_t ooff = 0;
+  for (int t = 0; t < na; ++t) {
+    RsvdAct& a = act[t];
+    const SvdDesc& s = sd[a.i];
+    const int w = std::min(a.k_try + 10, a.full);
+    const double* M = s.src;  // row-major m x n, ld s_r
+    const int ld = s.s_r;
+    double* om;
+    if (h_omega) {
+      om = omb.p + ooff;
+      ooff += (size_t)a.n * w;
+    } else {
+      Om[t] = C.alloc(a.n, w);
+      om = Om[t].p;
+      rd.push_back({om, a.n * w,
+                    ((*keys)[a.i] * 0x9e3779b97f4a7c15ULL) ^ ((unsigned long long)a.k_try << 48) ^ rsvd_calls});
+    }
+    Yt[t] = C.alloc(w, a.m);   // Y col-major m x w
+    Zt[t] = C.alloc(w, a.n);   // Z col-major n x w
+    Ow[t] = C.alloc(1, a.m * w + w + 8);
+    Fw[t] = C.alloc(1, w * w + 2 * w + 8);
+    // Y^T = Om^T M^T ; Z^T = Q^T M ; Y^T = Z^T M^T
+    g0.add(om, w, 1, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
+    g1.add(Yt[t].p, a.m, 0, M, ld, 0, Zt[t].p, a.n, w, a.n, a.m, 1.0, 0.0);
+    g2.add(Zt[t].p, a.n, 0, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
+    od.push_back({Yt[t].p, a.m, w, Ow[t].p});
+    RsvdFinDesc f;
+    f.Bt = Zt[t].p; f.Q = Yt[t].p; f.m = a.m; f.n = a.n; f.w = w; f.k_try = a.k_try;
+    f.full = a.full; f.U = s.U; f.S = s.S; f.V = s.V; f.rank = s.rank; f.stop = d_stop + t;
+    f.work = Fw[t].p;
+    fd.push_back(f);
+  }
+  if (!h_omega) launch_randn(C.stage.push_vec(C, rd), na, C.st);
+  OrthDesc* dod = C.stage.push_vec(C, od);
+  run_gemm(g0);
+  for (int q = 0; q < 2; ++q) {  // power iterations (lowrank.py:99-100)
+    launch_orth(dod, na, C.st);
+    GemmBatch a1 = g1, a2 = g2;
+    run_gemm(a1);
+    run_gemm(a2);
+  }
+  launch_orth(dod, na, C.st);
+  run_gemm(g1);  // B^T = M^T Q  (into Zt)
+  launch_rsvd_fin(C.stage.push_vec(C, fd), na, thr, C.st);
+  C.launches += 8;
+  CUDA_CHECK(cudaGetLastError());
+  const int* hs = C.readback_ints(d_stop, na);
+  std::vector<int> stop(hs, hs + na);
+  for (int t = 0; t < na; ++t) {
+    C.free(Om[t]); C.free(Yt[t]); C.free(Zt[t]); C.free(Ow[t]); C.free(Fw[t]);
+  }
+  C.free(omb);
+  C.free(stopb);
+  C.flush();
+  return stop;
+}
+
+// Device-generator rSVD: every fill doubles independently.
 void Eliminator::rsvd_fills(std::vector<SvdDesc>& sd, const std::vector<int>& big,
                             const std::vector<unsigned long long>& keys, int* dr) {
-  struct A { int i, m, n, full, k_try; };
-  std::vector<A> act;
+  std::vector<RsvdAct> act;
   for (int i : big) {
     const int full = std::min(sd[i].m, sd[i].n);
     act.push_back({i, sd[i].m, sd[i].n, full, std::min(16, full)});
   }
-  Blk stopb = C.alloc(1, (int)big.size() / 2 + 2);
-  int* d_stop = reinterpret_cast<int*>(stopb.p);
-  std::vector<int> final_rank(sd.size(), -1);
   while (!act.empty()) {
-    ++rsvd_calls;
-    const int na = (int)act.size();
-    std::vector<Blk> Om(na), Yt(na), Zt(na), Ow(na), Fw(na);
-    std::vector<RandDesc> rd;
-    std::vector<OrthDesc> od;
-    std::vector<RsvdFinDesc> fd;
-    GemmBatch g0, g1, g2, g3;
-    for (int t = 0; t < na; ++t) {
-      A& a = act[t];
-      const SvdDesc& s = sd[a.i];
-      const int w = std::min(a.k_try + 10, a.full);
-      const double* M = s.src;  // row-major m x n, ld s_r
-      const int ld = s.s_r;
-      Om[t] = C.alloc(a.n, w);
-      Yt[t] = C.alloc(w, a.m);   // Y col-major m x w
-      Zt[t] = C.alloc(w, a.n);   // Z col-major n x w
-      Ow[t] = C.alloc(1, a.m * w + w + 8);
-      Fw[t] = C.alloc(1, w * w + 2 * w + 8);
-      rd.push_back({Om[t].p, a.n * w, (keys[a.i] * 0x9e3779b97f4a7c15ULL) ^ ((unsigned long long)a.k_try << 48) ^ rsvd_calls});
-      // Y^T = Om^T M^T ; Z^T = Q^T M ; Y^T = Z^T M^T
-      g0.add(Om[t].p, w, 1, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
-      g1.add(Yt[t].p, a.m, 0, M, ld, 0, Zt[t].p, a.n, w, a.n, a.m, 1.0, 0.0);
-      g2.add(Zt[t].p, a.n, 0, M, ld, 1, Yt[t].p, a.m, w, a.m, a.n, 1.0, 0.0);
-      od.push_back({Yt[t].p, a.m, w, Ow[t].p});
-      RsvdFinDesc f;
-      f.Bt = Zt[t].p; f.Q = Yt[t].p; f.m = a.m; f.n = a.n; f.w = w; f.k_try = a.k_try;
-      f.full = a.full; f.U = s.U; f.S = s.S; f.V = s.V; f.rank = s.rank; f.stop = d_stop + t;
-      f.work = Fw[t].p;
-      fd.push_back(f);
-    }
-    launch_randn(C.stage.push_vec(C, rd), na, C.st);
-    OrthDesc* dod = C.stage.push_vec(C, od);
-    run_gemm(g0);
-    for (int q = 0; q < 2; ++q) {  // power iterations (lowrank.py:99-100)
-      launch_orth(dod, na, C.st);
-      GemmBatch a1 = g1, a2 = g2;
-      run_gemm(a1);
-      run_gemm(a2);
-    }
-    launch_orth(dod, na, C.st);
-    run_gemm(g1);  // B^T = M^T Q  (into Zt)
-    launch_rsvd_fin(C.stage.push_vec(C, fd), na, thr, C.st);
-    C.launches += 8;
-    CUDA_CHECK(cudaGetLastError());
-    const int* hs = C.readback_ints(d_stop, na);
-    std::vector<int> stop(hs, hs + na);
-    std::vector<A> next;
-    for (int t = 0; t < na; ++t) {
+    std::vector<int> stop = rsvd_round(sd, act, &keys, nullptr);
+    std::vector<RsvdAct> next;
+    for (size_t t = 0; t < act.size(); ++t)
       if (!stop[t]) {
-        A a = act[t];
+        RsvdAct a = act[t];
         a.k_try = std::min(2 * a.k_try, a.full);
         next.push_back(a);
       }
-      C.free(Om[t]); C.free(Yt[t]); C.free(Zt[t]); C.free(Ow[t]); C.free(Fw[t]);
-    }
-    C.flush();
     act.swap(next);
   }
-  C.free(stopb);
   (void)dr;
+}
+
+// rSVD with the reference's Gaussian stream.  `order` lists the large fills
+// in the reference's call order (_compress_fill of F_kj then F_jk per pair,
+// pairs sorted, factor.py:321-332); call i's doubling rounds all precede call
+// i+1's first round in the stream (lowrank.py:104-117).  Batched
+// speculatively: every pending call runs its current round on the stream
+// position it would have if no earlier pending call doubles; the calls up to
+// the first one that must double are final, that one continues from the
+// stream state right after its own draw, and the calls behind it are
+// re-drawn from there (their sketches moved).
+void Eliminator::rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>& order) {
+  std::vector<RsvdAct> act;
+  for (int i : order) {
+    const int full = std::min(sd[i].m, sd[i].n);
+    act.push_back({i, sd[i].m, sd[i].n, full, std::min(16, full)});
+  }
+  while (!act.empty()) {
+    std::vector<double> h;
+    for (size_t t = 0; t < act.size(); ++t) {
+      const RsvdAct& a = act[t];
+      const int w = std::min(a.k_try + 10, a.full);
+      src_op(1, (long long)t);  // stream state before call t's sketch
+      const size_t o = h.size();
+      h.resize(o + (size_t)a.n * w);
+      draw(h.data() + o, (long long)a.n * w);
+    }
+    std::vector<int> stop = rsvd_round(sd, act, nullptr, &h);
+    size_t t0 = 0;
+    while (t0 < act.size() && stop[t0]) ++t0;
+    if (t0 == act.size()) break;  // every call final; the stream sits after the last draw
+    ++rsvd_redraws;
+    if (t0 + 1 < act.size()) src_op(2, (long long)(t0 + 1));  // back to just after call t0
+    std::vector<RsvdAct> next;
+    RsvdAct a = act[t0];
+    a.k_try = std::min(2 * a.k_try, a.full);
+    next.push_back(a);
+    for (size_t t = t0 + 1; t < act.size(); ++t) next.push_back(act[t]);
+    act.swap(next);
+  }
 }
 
 // Waves of clusters of one level: Morton order, a cluster joins the first
@@ -1336,8 +1453,7 @@ void Eliminator::top() {
   flops_all += 2.0 / 3.0 * (double)tot * tot * tot;
 }
 
-Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
-  (void)flags;
+Factor* factorize(Graph* gp, double eps, double sigma0, int flags, NormalSource src, void* src_user) {
   if (!(eps > 0.0 && eps < 1.0)) throw Error(E_VALUE, "epsilon must be in (0, 1)");
   IFMM_ASSERT(!gp->consumed, "graph already consumed by a factorization");
   Graph& g = *gp;
@@ -1360,13 +1476,24 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
   Eliminator el(C, g, *F, eps * sigma0, 0x1f2e3d4c5b6a7988ULL);
   el.exact_order = (flags & 1) != 0;
   el.exact_fill = (flags & 2) != 0 || getenv("IFMM_EXACT_FILL") != nullptr;
+  el.src = src;
+  el.src_user = src_user;
+  // Morton cluster order (one cluster per wave): implied by the reference
+  // stream, whose consumption order is the reference's cluster order
+  const bool morton = el.exact_order || src != nullptr || (flags & 4) != 0;
   for (double& v : g_prof) v = 0.0;
+  C.bucket_start(C.st);
+  C.fail_fast = true;
+  C.fail_prefix = "cluster ";
   try {
     for (int l = T.depth; l >= 2; --l) {
       LevelStats st;
       st.level = l;
-      for (auto& wv : cluster_waves(T, l, el.exact_order)) el.eliminate_wave(wv, st);
+      const double lr0 = C.bc.acc[2];
+      for (auto& wv : cluster_waves(T, l, morton)) el.eliminate_wave(wv, st);
       C.check_status("cluster ");
+      C.bucket_collect();
+      st.compress_time = C.bc.acc[2] - lr0;
       F->levels.push_back(st);
       if (l > 2) el.merge(l);
       if (getenv("IFMM_MEMTRACE")) {
@@ -1388,10 +1515,18 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
     C.sync();
     C.check_status("cluster ");
   } catch (...) {
+    C.fail_fast = false;
+    C.bc.s = nullptr;
     g.consumed = true;
     delete F;
     throw;
   }
+  C.fail_fast = false;
+  C.bucket_stop();
+  F->t_lu = C.bc.acc[0];
+  F->t_mm = C.bc.acc[1];
+  F->t_lr = C.bc.acc[2];
+  F->t_tr = C.bc.acc[3];
   g.consumed = true;
   F->peak_edges = g.peak_edges;
   long long mb = 0;
@@ -1399,6 +1534,8 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags) {
   F->max_basis_rank = mb;
   F->gemm_flops = el.flops_gemm;
   F->all_flops = el.flops_all;
+  F->rsvd_rounds = el.rsvd_calls;
+  F->rsvd_redraws = el.rsvd_redraws;
   C.free(el.d_ranks);
   std::vector<int> final_size = g.size;
   F->build_program(final_size);

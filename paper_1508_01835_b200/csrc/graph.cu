@@ -12,7 +12,7 @@ Graph::~Graph() {
   for (auto& kv : E) ctx->free(kv.second);
   for (auto& b : su) ctx->free(b);
   for (auto& b : sv) ctx->free(b);
-  ctx->sync();
+  if (cudaStreamSynchronize(ctx->st) != cudaSuccess) cudaGetLastError();  // no throw in a destructor
   ctx->flush();
 }
 
@@ -86,6 +86,65 @@ void Graph::build(H2* h, bool consume) {
     h->consumed = true;
     C.flush();
   }
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// Deep copy (graph.py:190-216): same nodes, adjacency and weights, every
+// block duplicated on the device (one batched copy).
+Graph* Graph::clone() const {
+  IFMM_ASSERT(!consumed, "copy of a consumed graph");
+  Ctx& C = *ctx;
+  Graph* g = new Graph;
+  g->ctx = ctx; g->tree = tree; g->ops = ops;
+  g->size = size; g->kind = kind; g->owner = owner;
+  g->nx = nx; g->nz = nz; g->ny = ny;
+  g->rows = rows; g->cols = cols; g->dead = dead;
+  g->peak_edges = peak_edges;
+  CopyBatch cb;
+  auto dup = [&](const Blk& s) {
+    if (!s.p) return Blk();
+    Blk b = C.alloc(s.r, s.c);
+    cb.add(s.p, s.c, 1, b.p, b.c, 1, s.r, s.c, 0);
+    return b;
+  };
+  g->E.reserve(E.size());
+  for (auto& kv : E) g->E.emplace(kv.first, dup(kv.second));
+  g->su.resize(su.size()); g->sv.resize(sv.size());
+  for (size_t i = 0; i < su.size(); ++i) { g->su[i] = dup(su[i]); g->sv[i] = dup(sv[i]); }
+  cb.run(C);
+  CUDA_CHECK(cudaGetLastError());
+  return g;
+}
+
+// out = E in (or E^T in) for one full node vector (graph.py:157-170),
+// deterministic block SpMV in sorted node order.
+void Graph::apply(const double* d_in, double* d_out, bool transpose) {
+  Ctx& C = *ctx;
+  const int nn = (int)size.size();
+  std::vector<long long> off(nn + 1, 0);
+  for (int i = 0; i < nn; ++i) off[i + 1] = off[i] + size[i];
+  std::vector<SpmvRow> rr;
+  std::vector<SpmvTerm> tt;
+  for (int a = 0; a < nn; ++a) {
+    SpmvRow r{d_out + off[a], size[a], (int)tt.size(), 0, 0};
+    if (!transpose) {
+      for (int s : rows[a]) {
+        const Blk& B = E.at(key2(a, s));
+        tt.push_back({B.p, B.r, B.c, B.c, 0, d_in + off[s]});
+        r.nt++;
+      }
+    } else {
+      for (int t : cols[a]) {
+        const Blk& B = E.at(key2(t, a));
+        tt.push_back({B.p, B.r, B.c, B.c, 1, d_in + off[t]});
+        r.nt++;
+      }
+    }
+    rr.push_back(r);
+  }
+  SpmvTerm* dt = C.stage.push_vec(C, tt);
+  SpmvRow* dr = C.stage.push_vec(C, rr);
+  launch_spmv(dr, (int)rr.size(), dt, 1, 1, C.st);
   CUDA_CHECK(cudaGetLastError());
 }
 

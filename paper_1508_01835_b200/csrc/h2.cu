@@ -14,7 +14,7 @@ H2::~H2() {
     for (auto& b : *v) ctx->free(b);
   for (auto& kv : coupling) ctx->free(kv.second);
   for (auto& kv : near) ctx->free(kv.second);
-  ctx->sync();
+  ctx->sync_nothrow();
   ctx->flush();
 }
 

@@ -101,9 +101,8 @@ __global__ void k_combine(const double* __restrict__ V, long long ldv, int k,
   }
 }
 
-int grid_for(long long n) {
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+int grid_for(Ctx& C, long long n) {
+  const int sms = C.sm_count();
   long long want = (n + kThreads - 1) / kThreads;
   long long cap = 4LL * sms;  // 4 resident 512-thread CTAs per SM
   return (int)std::max(1LL, std::min(want, cap));
@@ -113,14 +112,11 @@ int grid_for(long long n) {
 
 void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, double* w,
                 double* h_host) {
-  const int nb = grid_for(n);
+  const int nb = grid_for(C, n);
   Blk part = C.alloc(1, 2 * nb), h = C.alloc(1, k1 + 1);
-  static int occ = -1;
-  if (occ < 0)
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgs_coop, kThreads, 0));
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int g = std::min(nb, std::max(1, occ) * sms);
+  if (C.mgs_occ < 0)  // per context (= per device), not a process-wide static
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&C.mgs_occ, k_mgs_coop, kThreads, 0));
+  const int g = std::min(nb, std::max(1, C.mgs_occ) * C.sm_count());
   void* args[] = {(void*)&V, (void*)&ldv, (void*)&k1, (void*)&n, (void*)&w, (void*)&h.p,
                   (void*)&part.p};
   CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_mgs_coop, dim3(g), dim3(kThreads), args, 0, C.st));
@@ -133,7 +129,7 @@ void krylov_mgs(Ctx& C, const double* V, long long ldv, int k1, long long n, dou
 }
 
 void krylov_div(Ctx& C, const double* w, long long n, double hs, double* out) {
-  k_div<<<grid_for(n), kThreads, 0, C.st>>>(w, n, hs, out);
+  k_div<<<grid_for(C, n), kThreads, 0, C.st>>>(w, n, hs, out);
   CUDA_CHECK(cudaGetLastError());
   C.sync();
 }
@@ -142,7 +138,7 @@ void krylov_combine(Ctx& C, const double* V, long long ldv, int k, const double*
                     long long n, double* u) {
   Blk y = C.alloc(1, std::max(k, 1));
   CUDA_CHECK(cudaMemcpyAsync(y.p, y_host, 8 * (size_t)k, cudaMemcpyHostToDevice, C.st));
-  k_combine<<<grid_for(n), kThreads, 0, C.st>>>(V, ldv, k, y.p, n, u);
+  k_combine<<<grid_for(C, n), kThreads, 0, C.st>>>(V, ldv, k, y.p, n, u);
   CUDA_CHECK(cudaGetLastError());
   C.sync();
   C.free(y);

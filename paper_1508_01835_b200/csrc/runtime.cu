@@ -212,13 +212,21 @@ void* Staging::push(Ctx& ctx, const void* src, size_t bytes) {
 
 // ---------------------------------------------------------------------------
 const int* Ctx::readback_ints(const int* d, size_t n) {
-  if (n > h_pinned_n) {
+  if (n + 1 > h_pinned_n) {
     if (h_pinned_i) cudaFreeHost(h_pinned_i);
-    h_pinned_n = std::max<size_t>(n, 1 << 16);
+    h_pinned_n = std::max<size_t>(n + 1, 1 << 16);
     CUDA_CHECK(cudaMallocHost(&h_pinned_i, h_pinned_n * sizeof(int)));
   }
   if (n) CUDA_CHECK(cudaMemcpyAsync(h_pinned_i, d, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+  // the singular-pivot flag rides along with every readback: a failed LU
+  // stops the factorization at the first sync after it (the reference raises
+  // at the failing cluster, factor.py:166-173) instead of carrying NaNs on
+  if (fail_fast && d != d_status)
+    CUDA_CHECK(cudaMemcpyAsync(h_pinned_i + h_pinned_n - 1, d_status, sizeof(int),
+                               cudaMemcpyDeviceToHost, st));
   sync();
+  if (bc.s) bucket_collect();
+  if (fail_fast && d != d_status && h_pinned_i[h_pinned_n - 1] != 0) check_status(fail_prefix);
   return h_pinned_i;
 }
 

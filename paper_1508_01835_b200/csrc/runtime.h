@@ -102,6 +102,13 @@ class Staging {
 
 struct Ctx {
   int device = 0;
+  int n_sms = 0;       // SM count of `device` (sm_count())
+  int mgs_occ = -1;    // cached occupancy of the cooperative MGS kernel on `device`
+  int sm_count() {
+    if (n_sms <= 0 && cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+      n_sms = 148;
+    return n_sms;
+  }
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;        // forked side stream (concurrent variants)
   cudaStream_t st3 = nullptr;        // side stream for a pair wave's rebases / K rewrite
@@ -160,6 +167,53 @@ struct Ctx {
     krec.clear();
   }
 
+  // Device time of the reference's timing buckets (factor.py:71-72:
+  // lu_and_triangular_solves, matmul_updates, lowrank_approximations,
+  // operator_transfer): one event on the engine stream per bucket switch;
+  // the time between consecutive marks goes to the bucket active in between.
+  struct BucketClock {
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    double acc[4] = {};
+  } bc;
+  void bucket(int b) {
+    if (!bc.s) return;
+    if (!bc.marks.empty() && bc.marks.back().first == b) return;
+    cudaEvent_t e;
+    if (bc.pool.empty()) CUDA_CHECK(cudaEventCreate(&e));
+    else { e = bc.pool.back(); bc.pool.pop_back(); }
+    CUDA_CHECK(cudaEventRecord(e, bc.s));
+    bc.marks.push_back({b, e});
+  }
+  void bucket_collect() {  // reaps every completed interval
+    size_t i = 0;
+    for (; i + 1 < bc.marks.size(); ++i) {
+      if (cudaEventQuery(bc.marks[i + 1].second) != cudaSuccess) { cudaGetLastError(); break; }
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, bc.marks[i].second, bc.marks[i + 1].second) == cudaSuccess &&
+          bc.marks[i].first >= 0 && bc.marks[i].first < 4)
+        bc.acc[bc.marks[i].first] += ms * 1e-3;
+      cudaGetLastError();
+      bc.pool.push_back(bc.marks[i].second);
+    }
+    bc.marks.erase(bc.marks.begin(), bc.marks.begin() + i);
+  }
+  void bucket_start(cudaStream_t s) {
+    for (auto& m : bc.marks) bc.pool.push_back(m.second);
+    bc.marks.clear();
+    for (double& a : bc.acc) a = 0.0;
+    bc.s = s;
+  }
+  void bucket_stop() {  // after a sync of bc.s
+    bucket(-1);
+    CUDA_CHECK(cudaStreamSynchronize(bc.s));
+    bucket_collect();
+    for (auto& m : bc.marks) bc.pool.push_back(m.second);
+    bc.marks.clear();
+    bc.s = nullptr;
+  }
+
   Blk alloc(int r, int c) {
     Blk b;
     b.r = r;
@@ -186,6 +240,11 @@ struct Ctx {
     pending.clear();
   }
   void sync() { CUDA_CHECK(cudaStreamSynchronize(st)); }
+  // destructors / destroy entry points must not throw
+  void sync_nothrow() { if (cudaStreamSynchronize(st) != cudaSuccess) cudaGetLastError(); }
+  // while set, every readback also checks the singular-pivot flag
+  bool fail_fast = false;
+  const char* fail_prefix = "cluster ";
   // read back n ints from device (synchronizes)
   const int* readback_ints(const int* d, size_t n);
   void check_status(const char* what_prefix);

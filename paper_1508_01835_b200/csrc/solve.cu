@@ -68,7 +68,9 @@ Factor::~Factor() {
     ctx->free(prog->perm_d);
     delete prog;
   }
-  ctx->sync();
+  // a destructor must not throw: after a device fault the sync reports the
+  // (sticky) error, which the failing call has already raised
+  if (cudaStreamSynchronize(ctx->st) != cudaSuccess) cudaGetLastError();
   ctx->flush();
 }
 

@@ -91,12 +91,19 @@ class IFMMFactorization:
         self.event_counts = {"elim": int(s[6]), "rebase": int(s[7]), "merge": int(s[8])}
         self.top_nodes_count = int(s[9])
         self.top_dim = int(s[10])
-        t = np.zeros(7)
-        N.check(L.ifmm_factor_timings(handle, N.as_dp(t), 7))
+        t = np.zeros(9)
+        N.check(L.ifmm_factor_timings(handle, N.as_dp(t), 9))
         self.flops = {"gemm_lu_class": float(t[5]), "all": float(t[6])}
-        self.timings = {k: 0.0 for k in _TIMING_KEYS}
+        self.rsvd = {"rounds": int(t[7]), "redraws": int(t[8])}
+        # factor.py:71-72 buckets: device time attributed per bucket (events
+        # on the engine stream at every bucket switch, csrc/runtime.h)
+        self.timings = {k: float(v) for k, v in zip(_TIMING_KEYS, t[:4])}
         self.timings["sigma0_estimation"] = t_sigma0
         self.timings["elimination_total"] = float(t[4])
+        ct = np.zeros(max(nlev, 1))
+        N.check(L.ifmm_factor_level_times(handle, N.as_dp(ct), nlev))
+        for lvl, c in zip(levels, ct):
+            lvl.compress_time = float(c)
 
     def __del__(self):
         try:
@@ -108,11 +115,57 @@ class IFMMFactorization:
     def dim(self):
         return self.n_points * self.block_dim
 
+    def _layout(self):
+        if getattr(self, "_lay", None) is None:
+            L = N.lib()
+            sz = np.zeros(3, dtype=np.int32)
+            N.check(L.ifmm_factor_layout(self._h, N.as_ip(sz), None, None, None, None, None,
+                                         None))
+            nt, ni, nl = (int(v) for v in sz)
+            tn, ts = np.zeros(max(nt, 1), np.int32), np.zeros(max(nt, 1), np.int32)
+            isz = np.zeros(max(ni, 1), np.int32)
+            ln, l0, l1 = (np.zeros(max(nl, 1), np.int32) for _ in range(3))
+            N.check(L.ifmm_factor_layout(self._h, None, N.as_ip(tn), N.as_ip(ts), N.as_ip(isz),
+                                         N.as_ip(ln), N.as_ip(l0), N.as_ip(l1)))
+            self._lay = (tn[:nt].tolist(), ts[:nt].tolist(), isz[:ni].tolist(),
+                         list(zip(ln[:nl].tolist(), l0[:nl].tolist(), l1[:nl].tolist())))
+        return self._lay
+
+    top_nodes = property(lambda self: list(self._layout()[0]))
+    top_sizes = property(lambda self: list(self._layout()[1]))
+    init_sizes = property(lambda self: list(self._layout()[2]))
+    leaf_slices = property(lambda self: list(self._layout()[3]))
+
     @property
     def events(self):
-        """Event tags (counts only; the log itself lives on the device)."""
-        c = self.event_counts
-        return [("elim",)] * c["elim"] + [("rebase",)] * c["rebase"] + [("merge",)] * c["merge"]
+        """The event log (factor.py:80) with the reference's tuple shapes and
+        node ids; the numerical payload (LU factors, edge blocks, rebase maps)
+        stays on the device and reads as None:
+        ("elim", nx, nz, ny, size_x, size_z, None, [(b, None)..], [(a, None)..]),
+        ("rebase", ny, None), ("merge", px, [(child_y, size)..])."""
+        L = N.lib()
+        n = int(L.ifmm_factor_events(self._h, None, 0))
+        buf = np.zeros(max(n, 1), dtype=np.int64)
+        L.ifmm_factor_events(self._h, N.as_lp(buf), n)
+        v, out, i = buf[:n].tolist(), [], 0
+        while i < n:
+            t = v[i]
+            if t == 0:
+                nx, nz, ny, m, k, ns, nt = v[i + 1:i + 8]
+                src = v[i + 8:i + 8 + ns]
+                tgt = v[i + 8 + ns:i + 8 + ns + nt]
+                out.append(("elim", nx, nz, ny, m, k, None, [(b, None) for b in src],
+                            [(a, None) for a in tgt]))
+                i += 8 + ns + nt
+            elif t == 1:
+                out.append(("rebase", v[i + 1], None))
+                i += 2
+            else:
+                px, npart = v[i + 1], v[i + 2]
+                pr = v[i + 3:i + 3 + 2 * npart]
+                out.append(("merge", px, list(zip(pr[0::2], pr[1::2]))))
+                i += 3 + 2 * npart
+        return out
 
     def solve(self, b):
         """A x = b in the original point order (factor.py:99-157)."""
@@ -140,18 +193,72 @@ class IFMMFactorization:
         return x
 
 
+_NORMAL_SOURCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_longlong,
+                             C.POINTER(C.c_double))
+
+
+class _ReferenceStream:
+    """The reference factorize rng -- ``np.random.Generator(PCG64(seed))``
+    (factor.py:188) -- served to the engine as a stream of standard normals
+    (ifmm_normal_source, include/ifmm_b200.h).  ``standard_normal((n, w))``
+    is the next n*w deviates of one sequence, so the engine asks for flat
+    runs of the sizes the reference draws, in the reference's order."""
+
+    def __init__(self, seed):
+        self.g = np.random.Generator(np.random.PCG64(seed))
+        self.slots = {}
+        self.drawn = 0
+        self.error = None
+        self.cb = _NORMAL_SOURCE(self._call)
+
+    def _call(self, user, op, n, out):
+        try:
+            if op == 0:
+                np.ctypeslib.as_array(out, shape=(n,))[:] = self.g.standard_normal(n)
+                self.drawn += n
+            elif op == 1:
+                self.slots[n] = (self.g.bit_generator.state, self.drawn)
+            elif op == 2:
+                st, self.drawn = self.slots[n]
+                self.g.bit_generator.state = st
+            else:
+                return 1
+            return 0
+        except Exception as e:  # surfaces as a ValueError from the engine
+            self.error = e
+            return 1
+
+
+SCHEDULES = ("reference", "wavefront")
+
+
 def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
-              sigma0: float | None = None, exact_order: bool | None = None
-              ) -> IFMMFactorization:
+              sigma0: float | None = None, exact_order: bool | None = None,
+              schedule: str | None = None) -> IFMMFactorization:
     """factor.py:176-230.  Consumes the graph (like the reference's pops).
 
-    ``exact_order`` processes the fill pairs of each elimination strictly in
-    the reference's sorted order (one pair at a time).  The default groups
-    cluster-disjoint pairs into concurrent waves, which commute up to
-    rounding.  IFMM_EXACT_ORDER=1 sets the default."""
+    ``schedule``:
+      * ``"reference"`` -- clusters are eliminated one at a time in the
+        reference's Morton order, and every Gaussian the reference draws
+        (rSVD sketches of fills with min(shape) > 64, lowrank.py:108) comes
+        from the reference's own rng, ``Generator(PCG64(seed))``, in the
+        reference's order.  Rank decisions and x then match the reference up
+        to floating-point rounding.
+      * ``"wavefront"`` -- clusters at Chebyshev distance >= 3 (no shared
+        neighbour) are eliminated together in one batched stage, and the rSVD
+        sketches come from a counter-based device generator.  Same
+        algorithm; results differ from the reference the way the reference's
+        own results differ between rng seeds.
+    The fill pairs of one elimination always run as waves of cluster-disjoint
+    pairs (they commute); ``exact_order=True`` runs them one at a time
+    (diagnostics).  Environment defaults: IFMM_SCHEDULE, IFMM_EXACT_ORDER."""
     import os
     if exact_order is None:
         exact_order = os.environ.get("IFMM_EXACT_ORDER", "0") == "1"
+    if schedule is None:
+        schedule = os.environ.get("IFMM_SCHEDULE", "reference")
+    if schedule not in SCHEDULES:
+        raise ValueError(f"schedule must be one of {SCHEDULES}")
     if not 0.0 < epsilon < 1.0:
         raise ValueError("epsilon must be in (0, 1)")
     if graph.consumed:
@@ -162,7 +269,19 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
         sigma0 = estimate_sigma0(graph, seed=seed)
         t_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    h = N.lib().ifmm_factorize(graph._h, float(epsilon), float(sigma0), 1 if exact_order else 0)
+    flags = 1 if exact_order else 0
+    lib = N.lib()
+    if schedule == "reference":
+        stream = _ReferenceStream(seed)
+        h = lib.ifmm_factorize_rng(graph._h, float(epsilon), float(sigma0), flags | 4,
+                                   C.cast(stream.cb, C.c_void_p), None)
+        if stream.error is not None and not h:
+            graph.consumed = True
+            raise stream.error
+    else:
+        h = lib.ifmm_factorize(graph._h, float(epsilon), float(sigma0), flags)
     graph.consumed = True
     h = N.check_handle(h)
-    return IFMMFactorization(graph, h, epsilon, sigma0, t_s, time.perf_counter() - t0)
+    f = IFMMFactorization(graph, h, epsilon, sigma0, t_s, time.perf_counter() - t0)
+    f.schedule = schedule
+    return f

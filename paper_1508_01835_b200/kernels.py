@@ -126,3 +126,103 @@ def cube_uniform(n: int, seed: int) -> Scene:
     if n < 1:
         raise ValueError("n must be >= 1")
     return Scene(_rng(seed).uniform(-1.0, 1.0, size=(n, 3)), f"cube_uniform(n={n}, seed={seed})")
+
+
+def rpy_kernel(radius: float, viscosity: float = 1.0) -> Kernel:
+    """kernels.py:59-91: Rotne-Prager-Yamakawa 3x3 mobility blocks
+    f(r) I + g(r) r^ r^T with c = 1/(6 pi eta a); far field (r > 2a)
+    f = c(3a/4r + a^3/2r^3), g = c(3a/4r - 3a^3/2r^3); overlap f = c(1 - 9r/32a),
+    g = c(3r/32a); self f = c, g = 0.  The host ``block`` gives the
+    reference's point-major (3m x 3n) layout; the engine has no device
+    implementation of block_dim 3 kernels, so ``device_spec`` raises."""
+    if radius <= 0 or viscosity <= 0:
+        raise ValueError("radius and viscosity must be positive")
+    a = float(radius)
+    c0 = 1.0 / (6.0 * np.pi * viscosity * a)
+
+    def block(P, Q):
+        P = np.atleast_2d(np.asarray(P, dtype=float))
+        Q = np.atleast_2d(np.asarray(Q, dtype=float))
+        dv = P[:, None, :] - Q[None, :, :]
+        r = np.sqrt(np.einsum("ijk,ijk->ij", dv, dv))
+        safe = np.where(r == 0.0, 1.0, r)
+        inv, inv3 = 1.0 / safe, 1.0 / safe ** 3
+        far = r > 2.0 * a
+        f = np.where(far, c0 * (0.75 * a * inv + 0.5 * a ** 3 * inv3), c0 * (1.0 - 9.0 * r / (32.0 * a)))
+        g = np.where(far, c0 * (0.75 * a * inv - 1.5 * a ** 3 * inv3), c0 * (3.0 * r / (32.0 * a)))
+        g = np.where(r == 0.0, 0.0, g)
+        u = dv * inv[..., None]
+        out = g[..., None, None] * (u[..., :, None] * u[..., None, :])
+        out += f[..., None, None] * np.eye(3)
+        m, n = len(P), len(Q)
+        return out.transpose(0, 2, 1, 3).reshape(3 * m, 3 * n)
+
+    return Kernel("rpy", 3, {"radius": a, "viscosity": float(viscosity)}, block)
+
+
+def icosphere(subdivision: int) -> np.ndarray:
+    """kernels.py:133-167: vertices of a unit icosphere (10*4^s + 2).
+
+    Recursive 4-way face split of the regular icosahedron; each new vertex
+    is the normalised edge midpoint, numbered in first-visit order.  Vertex
+    and face orders follow the reference so the point sets are identical."""
+    if subdivision < 0:
+        raise ValueError("subdivision must be >= 0")
+    t = (1.0 + np.sqrt(5.0)) / 2.0
+    base = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t),
+            (0, -1, -t), (0, 1, -t), (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    V = [np.asarray(v, dtype=float) / np.linalg.norm(v) for v in base]
+    F = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
+         (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8),
+         (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(subdivision):
+        seen = {}
+
+        def midpoint(i, j):
+            e = (i, j) if i < j else (j, i)
+            if e not in seen:
+                v = V[i] + V[j]
+                V.append(v / np.linalg.norm(v))
+                seen[e] = len(V) - 1
+            return seen[e]
+
+        nf = []
+        for i, j, k in F:
+            ij, jk, ki = midpoint(i, j), midpoint(j, k), midpoint(k, i)
+            nf.extend([(i, ij, ki), (j, jk, ij), (k, ki, jk), (ij, jk, ki)])
+        F = nf
+    return np.array(V)
+
+
+def sphere_lattice(nx: int, ny: int, nz: int, subdivision: int, spacing: float,
+                   body_radius: float = 1.0) -> Scene:
+    """kernels.py:170-182: an nx x ny x nz lattice of icosphere bodies (x
+    slowest, z fastest)."""
+    body = icosphere(subdivision) * body_radius
+    shifts = [spacing * np.array([i, j, k], dtype=float)
+              for i in range(nx) for j in range(ny) for k in range(nz)]
+    pts = np.vstack([body + s for s in shifts]) if shifts else np.zeros((0, 3))
+    return Scene(pts, f"sphere_lattice({nx}x{ny}x{nz}, subdivision={subdivision}, "
+                      f"spacing={spacing}, body_radius={body_radius})")
+
+
+def concentric_shells(subdivisions, radii) -> Scene:
+    """kernels.py:185-192: one icosphere shell per (subdivision, radius)."""
+    if len(subdivisions) != len(radii):
+        raise ValueError("subdivisions and radii must have equal length")
+    pts = np.vstack([icosphere(s) * r for s, r in zip(subdivisions, radii)])
+    return Scene(pts, f"concentric_shells(subdivisions={list(subdivisions)}, "
+                      f"radii={list(radii)})")
+
+
+def scene_to_text(scene: Scene, path) -> None:
+    """kernels.py:195-196: x y z per line, round-trip precision."""
+    np.savetxt(path, scene.points, fmt="%.17g")
+
+
+def scene_from_text(path, description: str = "imported") -> Scene:
+    """kernels.py:199-203."""
+    pts = np.loadtxt(path, ndmin=2)
+    if pts.shape[1] != 3:
+        raise ValueError("expected three columns (x y z)")
+    return Scene(pts, description)

@@ -6,8 +6,9 @@ non-restarted MGS/Givens loop.  With a CUDA torch ``b`` the Krylov basis V is
 resident in HBM and the Arnoldi step (MGS projections + norm), the basis
 normalisation and the final combination run in the engine's kernels
 (``csrc/krylov.cu``); the Givens rotations and the k x k triangular solve stay
-on the host, as in SURVEY A18.  A numpy ``b`` runs the same loop on the host
-(the reference's own array path, for callers whose apply_A is host-side).
+on the host, as in SURVEY A18.  A numpy ``b`` (the reference harness's call,
+experiments.py:190-233) runs the same device loop: b is copied up once and
+host-only operators are adapted per call (``_DeviceOperator``).
 """
 
 from __future__ import annotations
@@ -64,81 +65,52 @@ def gmres(apply_A, b, tol: float = 1e-10, max_iters: int = 500, precond=None,
     if side not in ("left", "right", "none"):
         raise ValueError("side must be 'left', 'right', or 'none'")
     trace = IterationTrace(side=side)
-    try:
-        import torch
-        is_t = isinstance(b, torch.Tensor)
-    except Exception:
-        is_t = False
-    if is_t and b.is_cuda:
+    import torch
+    if isinstance(b, torch.Tensor) and b.is_cuda:
         return _gmres_device(apply_A, b, tol, max_iters, precond, side, trace)
-    if is_t:
-        def dot(u, v): return float(torch.dot(u, v))
-        def norm(u): return float(torch.linalg.vector_norm(u))
-        zeros = lambda n: torch.zeros(n, dtype=b.dtype, device=b.device)  # noqa: E731
-    else:
-        b = np.asarray(b, dtype=float)
-        def dot(u, v): return float(u @ v)
-        def norm(u): return float(np.linalg.norm(u))
-        zeros = lambda n: np.zeros(n)  # noqa: E731
-    n = len(b)
-    r0 = precond(b) if side == "left" else b
-    beta = norm(r0)
-    if beta == 0.0:
-        trace.converged = True
-        return zeros(n), trace
-    V = [r0 / beta]
-    H = np.zeros((max_iters + 1, max_iters))
-    cs, sn = np.zeros(max_iters), np.zeros(max_iters)
-    g = np.zeros(max_iters + 1)
-    g[0] = beta
-    k_done, breakdown = 0, False
-    for k in range(max_iters):
-        if side == "right":
-            w = apply_A(precond(V[k]))
-        elif side == "left":
-            w = precond(apply_A(V[k]))
-        else:
-            w = apply_A(V[k])
-        for i in range(k + 1):
-            H[i, k] = dot(V[i], w)
-            w = w - H[i, k] * V[i]
-        h_sub = norm(w)
-        H[k + 1, k] = h_sub
-        for i in range(k):
-            h0 = cs[i] * H[i, k] + sn[i] * H[i + 1, k]
-            H[i + 1, k] = -sn[i] * H[i, k] + cs[i] * H[i + 1, k]
-            H[i, k] = h0
-        nu = np.hypot(H[k, k], H[k + 1, k])
-        if nu == 0.0:
-            k_done, breakdown = k, True
-            break
-        cs[k], sn[k] = H[k, k] / nu, H[k + 1, k] / nu
-        H[k, k], H[k + 1, k] = nu, 0.0
-        g[k + 1] = -sn[k] * g[k]
-        g[k] = cs[k] * g[k]
-        rel = abs(g[k + 1]) / beta
-        trace.residual_history.append(float(rel))
-        k_done = k + 1
-        if rel <= tol:
-            trace.converged = True
-            break
-        if h_sub == 0.0:
-            breakdown = True
-            break
-        V.append(w / h_sub)
-    if breakdown and trace.residual_history:
-        trace.converged = trace.residual_history[-1] <= tol
-    k = k_done
-    x = zeros(n)
-    if k > 0:
-        import scipy.linalg as sla
-        y = sla.solve_triangular(H[:k, :k], g[:k])
-        u = zeros(n)
-        for i in range(k):
-            u = u + float(y[i]) * V[i]
-        x = precond(u) if side == "right" else u
-    trace.iterations = k
-    return x, trace
+    # Host operands (numpy b, or a CPU tensor): the Arnoldi loop still runs on
+    # the device -- b is copied up once, the Krylov basis lives in HBM, and
+    # the caller's operators are adapted per call (a device-capable operator
+    # such as h2_matvec or IFMMFactorization.solve receives the CUDA vector
+    # directly; a host-only one, e.g. ``lambda v: A @ v`` on numpy arrays, is
+    # called with a numpy copy).  The result comes back in the caller's kind.
+    if not torch.cuda.is_available():
+        raise RuntimeError("gmres: the Arnoldi loop runs on the CUDA device and none is "
+                           "visible (there is no CPU path)")
+    host_tensor = isinstance(b, torch.Tensor)
+    bh = b.detach().to(torch.float64).numpy() if host_tensor else np.asarray(b, dtype=float)
+    bd = torch.from_numpy(np.ascontiguousarray(bh)).cuda()
+    A_dev = _DeviceOperator(apply_A)
+    P_dev = _DeviceOperator(precond) if precond is not None else None
+    x, trace = _gmres_device(A_dev, bd, tol, max_iters, P_dev, side, trace)
+    x = x.cpu()
+    return (x if host_tensor else x.numpy()), trace
+
+
+class _DeviceOperator:
+    """Adapts a caller's operator to CUDA float64 vectors.  The first call
+    probes whether the operator accepts a CUDA tensor (the package's own
+    operators do); if it does not, every call goes through a host copy."""
+
+    def __init__(self, fn):
+        self.fn, self.mode = fn, None
+
+    def __call__(self, v):
+        import torch
+        if self.mode != "host":
+            try:
+                out = self.fn(v)
+                if isinstance(out, torch.Tensor) and out.is_cuda:
+                    self.mode = "device"
+                    return out
+                if self.mode == "device":
+                    raise TypeError("operator stopped returning CUDA tensors")
+            except (TypeError, RuntimeError, ValueError, AttributeError):
+                if self.mode == "device":
+                    raise
+            self.mode = "host"
+        out = np.asarray(self.fn(v.cpu().numpy()), dtype=float)
+        return torch.from_numpy(np.ascontiguousarray(out)).to(v.device)
 
 
 def _gmres_device(apply_A, b, tol, max_iters, precond, side, trace):
@@ -160,7 +132,9 @@ def _gmres_device(apply_A, b, tol, max_iters, precond, side, trace):
     r0 = (precond(b) if side == "left" else b).contiguous()
     cur_sync()
     hb = np.zeros(1)
-    N.check(lib.ifmm_krylov_mgs(ctx, ptr(r0), n, 0, n, ptr(r0.clone()),
+    # k1 = 0: the kernel only forms ||w|| and never writes w, so r0 itself is
+    # passed (no temporary whose producer runs on another stream)
+    N.check(lib.ifmm_krylov_mgs(ctx, ptr(r0), n, 0, n, ptr(r0),
                                 hb.ctypes.data_as(C.c_void_p)))
     beta = float(hb[0])
     if beta == 0.0:
@@ -236,11 +210,27 @@ def _gmres_device(apply_A, b, tol, max_iters, precond, side, trace):
 def exact_matvec(points, kernel, x):
     """y = A x with A_ij = kernel(|p_i - p_j|) evaluated on the device without
     storing A (replaces dense.dense_matrix(...) @ x of the reference's
-    experiments._matvec_oracle, experiments.py:157-162, at any N)."""
+    experiments._matvec_oracle, experiments.py:157-162, at any N).  numpy or
+    CUDA torch ``x``; the result is of the same kind."""
     pts = np.ascontiguousarray(np.asarray(points, dtype=float))
     if pts.ndim != 2 or pts.shape[1] != 3:
         raise ValueError("points must be an (N, 3) array")
     kind, p0 = kernel.device_spec()
+    try:
+        import torch
+        is_t = isinstance(x, torch.Tensor) and x.is_cuda
+    except Exception:
+        is_t = False
+    if is_t:
+        if x.shape != (len(pts),):
+            raise ValueError("vector length mismatch")
+        xd = x.to(torch.float64).contiguous()
+        dp_ = torch.from_numpy(pts).to(xd.device)
+        y = torch.empty_like(xd)
+        torch.cuda.current_stream().synchronize()
+        N.check(N.lib().ifmm_exact_matvec(N.ctx(), kind, p0, len(pts), C.c_void_p(dp_.data_ptr()),
+                                          C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()), 1))
+        return y
     x = np.ascontiguousarray(np.asarray(x, dtype=float))
     if len(x) != len(pts):
         raise ValueError("vector length mismatch")
@@ -248,3 +238,72 @@ def exact_matvec(points, kernel, x):
     N.check(N.lib().ifmm_exact_matvec(N.ctx(), kind, p0, len(pts), pts.ctypes.data_as(C.c_void_p),
                                       x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 0))
     return y
+
+
+class H2Matvec:
+    """krylov.py:162-169: callable wrapper around h2_matvec."""
+
+    def __init__(self, ops: H2Operators):
+        self.ops = ops
+
+    def __call__(self, x):
+        return h2_matvec(self.ops, x)
+
+
+class _BlockDiag:
+    def __init__(self, handle, n):
+        self._h, self.n = handle, n
+
+    def __del__(self):
+        try:
+            N.lib().ifmm_blockdiag_destroy(self._h)
+        except Exception:
+            pass
+
+    def __call__(self, v):
+        import torch
+        if isinstance(v, torch.Tensor) and v.is_cuda:
+            v = v.to(torch.float64).contiguous()
+            out = torch.empty_like(v)
+            torch.cuda.current_stream().synchronize()
+            N.check(N.lib().ifmm_blockdiag_apply(self._h, C.c_void_p(v.data_ptr()),
+                                                 C.c_void_p(out.data_ptr()), 1))
+            return out
+        v = np.ascontiguousarray(np.asarray(v, dtype=float))
+        if v.shape != (self.n,):
+            raise ValueError("vector length mismatch")
+        out = np.empty_like(v)
+        N.check(N.lib().ifmm_blockdiag_apply(self._h, v.ctypes.data_as(C.c_void_p),
+                                             out.ctypes.data_as(C.c_void_p), 0))
+        return out
+
+
+def block_diag_preconditioner(A, block_size: int):
+    """krylov.py:172-196: factor the diagonal blocks of A once (device LU,
+    partial pivoting), apply the block solves (one batched launch).  The
+    last block is shorter when block_size does not divide the dimension."""
+    try:
+        import torch
+        on_dev = isinstance(A, torch.Tensor) and A.is_cuda
+    except Exception:
+        on_dev = False
+    if on_dev:
+        A = A.to(torch.float64).contiguous()
+        n = A.shape[0]
+        ptr = C.c_void_p(A.data_ptr())
+    else:
+        A = np.ascontiguousarray(np.asarray(A, dtype=float))
+        n = A.shape[0]
+        ptr = A.ctypes.data_as(C.c_void_p)
+    if block_size < 1 or block_size > n:
+        raise ValueError("block_size must be in [1, n]")
+    if on_dev:
+        torch.cuda.current_stream().synchronize()
+    h = N.lib().ifmm_blockdiag_create(N.ctx(), ptr, n, n, int(block_size), 1 if on_dev else 0)
+    if not h:
+        msg = N.last_error()
+        if "diagonal block" in msg:
+            a = int(msg.rsplit(" ", 1)[-1]) if msg.rsplit(" ", 1)[-1].isdigit() else 0
+            raise ValueError(f"singular diagonal block [{a}:{min(n, a + block_size)}]")
+        N.check_handle(h)
+    return _BlockDiag(h, n)

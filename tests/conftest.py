@@ -22,7 +22,7 @@ def load_golden(name):
 
 def golden_names():
     return sorted(f[:-4] for f in os.listdir(GOLDEN)
-                  if f.endswith(".npz") and not f.startswith("kat_"))
+                  if f.endswith(".npz") and not f.startswith(("kat_", "scenes")))
 
 
 def csr_lists(ptr, idx):

@@ -1,0 +1,95 @@
+"""The harness (experiments.py / reports.py / cli.py mirrors) end to end on
+the device, against RunReports of the unmodified reference harness on the
+same configs (tests/golden/reports.json, make_report_golden.py)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(GOLDEN, "reports.json")))
+
+
+def _cfg(kw):
+    from paper_1508_01835_b200.experiments import RunConfig
+    kw = dict(kw)
+    for k in ("lattice_shape", "shell_subdivisions", "shell_radii"):
+        if isinstance(kw.get(k), list):
+            kw[k] = tuple(kw[k])
+    return RunConfig(**kw)
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_report_matches_reference(name):
+    from paper_1508_01835_b200.experiments import run_direct, run_iterative
+    from paper_1508_01835_b200.reports import validate_report
+    g = GOLD[name]
+    cfg = _cfg(g["kwargs"])
+    rep = (run_direct if cfg.mode == "direct" else run_iterative)(cfg).to_dict()
+    validate_report(rep)
+    ref = g["report"]
+    assert rep["config"] == ref["config"]
+    assert rep["edge_stats"] == ref["edge_stats"]
+    strip = lambda rs: {**rs, "per_level": [{k: v for k, v in lv.items() if k != "compress_time"}
+                                            for lv in rs["per_level"]]}  # noqa: E731
+    assert strip(rep["rank_stats"]) == strip(ref["rank_stats"])
+    for k in ("relative_error", "relative_residual"):
+        a, b = rep["errors"][k], ref["errors"][k]
+        assert abs(a - b) <= 1e-6 * b + 1e-14, (k, a, b)
+    if ref["iteration"] is not None:
+        assert rep["iteration"]["iterations"] == ref["iteration"]["iterations"]
+        assert rep["iteration"]["converged"] == ref["iteration"]["converged"]
+        assert rep["iteration"]["side"] == ref["iteration"]["side"]
+        np.testing.assert_allclose(rep["iteration"]["residual_history"],
+                                   ref["iteration"]["residual_history"], rtol=1e-4)
+    t = rep["timings"]
+    assert t["total"] > 0 and all(v >= 0 for v in t.values())
+    assert sum(rep["elimination_breakdown"].values()) <= 1.05 * (t["elimination"] + t["sigma0_estimation"]) + 0.01
+
+
+def test_run_direct_deterministic_and_scaling():
+    from paper_1508_01835_b200.experiments import fit_loglog_slope, run_direct, run_scaling
+    cfg = _cfg(GOLD["direct_small"]["kwargs"])
+    r1, r2 = run_direct(cfg), run_direct(cfg)
+    assert r1.errors == r2.errors and r1.edge_stats == r2.edge_stats
+    reps = run_scaling(cfg, [300, 600])
+    assert [r.config["n_points"] for r in reps] == [300, 600]
+    assert np.isfinite(fit_loglog_slope([300, 600], [r.timings["total"] for r in reps]))
+
+
+def test_cli_end_to_end(tmp_path, capsys):
+    from paper_1508_01835_b200.cli import main
+    from paper_1508_01835_b200.reports import validate_report
+    out = tmp_path / "r.json"
+    assert main(["--n-points", "300", "--cheb-nodes", "2", "--leaf-target", "30", "--d", "1e-2",
+                 "--out", str(out), "--scene-out", str(tmp_path / "s.txt"),
+                 "--dump-pattern", str(tmp_path / "p.json")]) == 0
+    rep = json.load(open(out))
+    validate_report(rep)
+    ref = GOLD["direct_small"]["report"]
+    assert rep["rank_stats"]["max_basis_rank"] == ref["rank_stats"]["max_basis_rank"]
+    pat = json.load(open(tmp_path / "p.json"))
+    assert len(pat["edges"]) > 0 and {"id", "kind", "cluster", "size"} <= set(pat["nodes"][0])
+    assert np.loadtxt(tmp_path / "s.txt").shape == (300, 3)
+    csv = tmp_path / "sw.csv"
+    assert main(["--n-points", "300", "--cheb-nodes", "2", "--leaf-target", "30", "--d", "1e-2",
+                 "--sweep", "200,400", "--out", str(csv), "--format", "csv"]) == 0
+    assert len(csv.read_text().strip().splitlines()) == 3
+    s = capsys.readouterr().out
+    assert "fitted log-log slope" in s
+    g = tmp_path / "g.json"
+    assert main(["--n-points", "300", "--cheb-nodes", "2", "--leaf-target", "30", "--d", "1e-2",
+                 "--mode", "gmres", "--precond", "ifmm", "--out", str(g)]) == 0
+    assert json.load(open(g))["iteration"]["iterations"] == GOLD["gmres_ifmm"]["report"]["iteration"]["iterations"]
+
+
+def test_rpy_refused_without_fallback():
+    from paper_1508_01835_b200.experiments import run_stokes
+    cfg = _cfg(dict(GOLD["gmres_lattice"]["kwargs"]))
+    with pytest.raises(ValueError, match="block_dim"):
+        run_stokes(cfg)
