@@ -412,11 +412,12 @@ __device__ __forceinline__ void cta_sv_order(const double* W, int rows, int cols
     if (lane == 0) sig[j] = sqrt(a);
   }
   __syncthreads();
+  // rank by value (NaN sorts last): a permutation even for non-finite input
   for (int j = threadIdx.x; j < cols; j += blockDim.x) {
-    const double sj = sig[j];
+    const double sj = isnan(sig[j]) ? -1.0 : sig[j];
     int pos = 0;
     for (int l = 0; l < cols; ++l) {
-      const double sl = sig[l];
+      const double sl = isnan(sig[l]) ? -1.0 : sig[l];
       pos += (sl > sj) || (sl == sj && l < j);
     }
     order[pos] = j;
@@ -521,7 +522,8 @@ __device__ int cta_qrcp(double* A, int m, int nn, int kmax, double* nrm, int* pe
     }
     t = block_sum(t, red);
     block_argmax(bv, bi, red, redi);
-    if (threadIdx.x == 0) { s_stop = t <= stop2; s_p = (int)bi; }
+    // non-finite norms (a failed pivot upstream): stop instead of indexing garbage
+    if (threadIdx.x == 0) { s_stop = !(t > stop2) || bi < j || bi >= nn; s_p = (int)bi; }
     __syncthreads();
     if (s_stop) break;
     const int p = s_p;
@@ -625,7 +627,7 @@ fill_svd_kernel(const SvdDesc* __restrict__ descs, int n, double thr, int smem_d
     double fro = 0.0;
     for (int j = threadIdx.x; j < nn; j += blockDim.x) fro += nrm[j];
     fro = block_sum(fro, red);
-    if (sqrt(fro) <= thr * (1.0 - 1e-12)) {  // sigma_1 <= ||F||_F <= thr
+    if (!(sqrt(fro) > thr * (1.0 - 1e-12))) {  // sigma_1 <= ||F||_F <= thr (or non-finite F)
       if (threadIdx.x == 0) *d.rank = 0;
       __syncthreads();
       continue;
@@ -1359,7 +1361,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
       cta_trmul2(GA, RA1s, TA, GB, RB1s, TB, s, sp);
       __syncthreads();
       unsigned long long c4 = clock64();
-      if (threadIdx.x == 0 && m > 400) {  // CholeskyQR sub-phases of large unions
+      if (threadIdx.x == 0 && m > 200) {  // CholeskyQR sub-phases of larger unions
         atomicAdd(&g_uprof[34], c1 - c0);
         atomicAdd(&g_uprof[35], c2 - c1);
         atomicAdd(&g_uprof[36], c3 - c2);

@@ -183,6 +183,7 @@ struct Factor {
   ~Factor();
   void build_program(const std::vector<int>& final_size);
   void solve(const double* d_b_orig, double* d_x_orig);
+  void enqueue_program(cudaStream_t s);
 };
 
 // Standard-normal source of the reference's factorize rng (see

@@ -1302,22 +1302,29 @@ void Eliminator::rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>
     const int full = std::min(sd[i].m, sd[i].n);
     act.push_back({i, sd[i].m, sd[i].n, full, std::min(16, full)});
   }
+  std::vector<double> h, skip;
   while (!act.empty()) {
-    std::vector<double> h;
+    // one save + one draw per round: the sketches of every pending call,
+    // back to back in call order (call t's run starts at off[t])
+    std::vector<size_t> off(act.size() + 1, 0);
     for (size_t t = 0; t < act.size(); ++t) {
       const RsvdAct& a = act[t];
-      const int w = std::min(a.k_try + 10, a.full);
-      src_op(1, (long long)t);  // stream state before call t's sketch
-      const size_t o = h.size();
-      h.resize(o + (size_t)a.n * w);
-      draw(h.data() + o, (long long)a.n * w);
+      off[t + 1] = off[t] + (size_t)a.n * std::min(a.k_try + 10, a.full);
     }
+    src_op(1, 0);  // stream state at the start of the round
+    h.resize(off.back());
+    draw(h.data(), (long long)h.size());
     std::vector<int> stop = rsvd_round(sd, act, nullptr, &h);
     size_t t0 = 0;
     while (t0 < act.size() && stop[t0]) ++t0;
     if (t0 == act.size()) break;  // every call final; the stream sits after the last draw
     ++rsvd_redraws;
-    if (t0 + 1 < act.size()) src_op(2, (long long)(t0 + 1));  // back to just after call t0
+    if (t0 + 1 < act.size()) {
+      // back to just after call t0's sketch: replay the round's stream up to there
+      src_op(2, 0);
+      skip.resize(off[t0 + 1]);
+      draw(skip.data(), (long long)skip.size());
+    }
     std::vector<RsvdAct> next;
     RsvdAct a = act[t0];
     a.k_try = std::min(2 * a.k_try, a.full);

@@ -9,10 +9,17 @@
 //     final level-2 y versions inside the top-level rhs;
 //   * the backward solution slots alias the same way (factor.py:147-152).
 // Ops are levelled into dependency waves (read-after-write, write-after-
-// write, write-after-read on slots); each wave is one launch with one CTA
-// per op.  Updates to one slot stay in event order, so solves are bitwise
-// reproducible (reference test_factor.py:95-106).
+// write, write-after-read on slots).  A wave runs as two launches whose
+// row tasks spread every op over many CTAs (forward: g = P^{-1}[:, :m] rhs_x,
+// then the target rows rhs_a -= T_a g; backward: v = [rhs_x - S sol_src;
+// sol_y], then [sol_x; sol_z] = P^{-1} v), so a wave streams its factor
+// bytes at HBM rate instead of one SM per op.  Every output row is one warp's
+// fixed-order dot product and ops of one wave write disjoint slots, so solves
+// are bitwise reproducible (reference test_factor.py:95-106).  The whole
+// program (waves + blocked top-level triangular solves) is captured once into
+// a CUDA graph and replayed per right-hand side.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 
 #include "common.cuh"
@@ -37,14 +44,28 @@ struct SolveOp {
   long long e;      // bwd: gather scratch
   int rows;         // rebase: k_new ; fwd: total target rows
   int cols;         // rebase: k_old ; bwd: Csrc
+  long long g;      // scratch: g (fwd) / v (bwd), n doubles
 };
 struct ListEnt {
   long long slot;
   int off, len;  // fwd: row offset in Tstk, height | bwd: col offset in Scat, width
 };
 
+struct SolveTask {
+  int op;       // index into the op array
+  int list;     // forward target phase: list entry; -1 otherwise
+  int r0, r1;   // output rows [r0, r1) of the phase
+};
+
 struct Factor::Program {
   Blk ops_d, list_d, work, perm_d;
+  Blk task_d;
+  std::vector<int> task_start;   // per launch: [task_start[i], task_start[i+1])
+  std::vector<int> launch_kind;  // 0 fwd-g, 1 fwd-t, 2 bwd-v, 3 bwd-x
+  long long scratch0 = 0;        // per-op scratch (g / v) region in the workspace
+  Blk bin, bout;                 // graph-resident rhs / solution buffers
+  cudaGraphExec_t graph = nullptr;
+  double bytes = 0;              // algorithmic bytes of one solve
   std::vector<int> fwd_wave_start, bwd_wave_start;  // op index ranges per wave
   int n_fwd = 0, n_bwd = 0;
   long long top_rhs = 0, top_sol = 0;
@@ -53,6 +74,9 @@ struct Factor::Program {
   int max_n = 0;
   int fwd_waves = 0, bwd_waves = 0;
   int smem = 0;  // doubles of dynamic shared memory per op
+  int n_fwd_launch = 0;
+  int max_csrc = 1;
+  long long nsolves = 0;
 };
 
 Factor::~Factor() {
@@ -66,6 +90,8 @@ Factor::~Factor() {
   if (prog) {
     ctx->free(prog->ops_d); ctx->free(prog->list_d); ctx->free(prog->work);
     ctx->free(prog->perm_d);
+    ctx->free(prog->task_d); ctx->free(prog->bin); ctx->free(prog->bout);
+    if (prog->graph) cudaGraphExecDestroy(prog->graph);
     delete prog;
   }
   // a destructor must not throw: after a device fault the sync reports the
@@ -79,73 +105,113 @@ Factor::~Factor() {
 // ---------------------------------------------------------------------------
 namespace {
 
-// One CTA per elimination op.  Forward (factor.py:111-119):
-//   g = P^{-1}[:, :m] rhs_x ;  rhs[a] -= T_a g[:m] ;  rhs[y] += g[m:]
-// Backward (factor.py:139-146):
-//   v = [rhs_x - S gather(sol_b) ; sol_y] ;  [sol_x ; sol_z] = P^{-1} v
-// Every product is a warp-per-row GEMV (lanes split the dot product, fixed
-// shuffle tree) -> deterministic, no serial triangular solves.
+// ---- row-task kernels (one launch per wave and phase) ----------------------
+// Each CTA takes one task; its 8 warps take the task's rows round robin, one
+// warp per row (lanes split the dot product, fixed shuffle tree).
+constexpr int kGatherCap = 24576;  // doubles of gathered sources staged in shared memory
+constexpr int kSolveRowsPerTask = 8;  // one row per warp: a wave's rows spread over the most CTAs
+
 __global__ void __launch_bounds__(256)
-solve_wave_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists, int first,
-                  int count, double* __restrict__ W) {
-  extern __shared__ double v[];  // n (+ Csrc gather for backward)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int oi = blockIdx.x; oi < count; oi += gridDim.x) {
-    const SolveOp op = ops[first + oi];
-    const int n = op.n, m = op.m;
-    if (op.type == OP_FWD_ELIM) {
-      double* rx = v + n;  // rhs_x staged in smem
-      for (int i = threadIdx.x; i < m; i += blockDim.x) rx[i] = W[op.a + i];
-      __syncthreads();
-      for (int i = warp; i < n; i += nw) {
-        const double* row = op.LU + (size_t)i * n;  // P^{-1} row i, first m columns
-        double s = 0.0;
-        for (int j = lane; j < m; j += 32) s = fma(row[j], rx[j], s);
-        s = warp_sum(s);
-        if (lane == 0) v[i] = s;
-      }
-      __syncthreads();
-      for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
-        const ListEnt t = lists[l];
-        for (int i = warp; i < t.len; i += nw) {
-          const double* row = op.M + (size_t)(t.off + i) * op.ldm;
-          double s = 0.0;
-          for (int j = lane; j < m; j += 32) s = fma(row[j], v[j], s);
-          s = warp_sum(s);
-          if (lane == 0) W[t.slot + i] = W[t.slot + i] - s;
-        }
-      }
-      for (int i = threadIdx.x; i < op.k; i += blockDim.x) W[op.b + i] = W[op.b + i] + v[m + i];
-      __syncthreads();
-      continue;
+solve_fwd_g_kernel(const SolveOp* __restrict__ ops, const SolveTask* __restrict__ tasks,
+                   double* __restrict__ W) {
+  const SolveTask t = tasks[blockIdx.x];
+  const SolveOp& op = ops[t.op];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = op.m, n = op.n;
+  const double* rx = W + op.a;
+  for (int i = t.r0 + warp; i < t.r1; i += 8) {
+    const double* row = op.LU + (size_t)i * n;  // P^{-1} row i, first m columns
+    double s = 0.0;
+    for (int j = lane; j < m; j += 32) s = fma(row[j], rx[j], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      W[op.g + i] = s;
+      if (i >= m) W[op.b + i - m] += s;  // rhs_y += g[m:]
     }
-    // OP_BWD_ELIM
-    double* gsol = v + n;
-    for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
-      const ListEnt s = lists[l];
-      for (int j = threadIdx.x; j < s.len; j += blockDim.x) gsol[s.off + j] = W[s.slot + j];
-    }
-    __syncthreads();
-    for (int i = warp; i < m; i += nw) {
+  }
+}
+
+__global__ void __launch_bounds__(256)
+solve_fwd_t_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists,
+                   const SolveTask* __restrict__ tasks, double* __restrict__ W) {
+  const SolveTask t = tasks[blockIdx.x];
+  const SolveOp& op = ops[t.op];
+  const ListEnt e = lists[t.list];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = op.m;
+  const double* g = W + op.g;
+  for (int i = t.r0 + warp; i < t.r1; i += 8) {
+    const double* row = op.M + (size_t)(e.off + i) * op.ldm;
+    double s = 0.0;
+    for (int j = lane; j < m; j += 32) s = fma(row[j], g[j], s);
+    s = warp_sum(s);
+    if (lane == 0) W[e.slot + i] = W[e.slot + i] - s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+solve_bwd_v_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ lists,
+                   const SolveTask* __restrict__ tasks, double* __restrict__ W, int cap) {
+  extern __shared__ double gsol[];  // the op's source solutions, gathered (Csrc <= cap)
+  const SolveTask t = tasks[blockIdx.x];
+  const SolveOp& op = ops[t.op];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = op.m;
+  if (op.cols > cap) {  // sources too wide for shared memory: read them in place
+    for (int i = t.r0 + warp; i < t.r1; i += 8) {
+      if (i >= m) {
+        if (lane == 0) W[op.g + i] = W[op.b + i - m];
+        continue;
+      }
       const double* row = op.M + (size_t)i * op.ldm;
       double s = 0.0;
-      for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
-      s = warp_sum(s);
-      if (lane == 0) v[i] = W[op.a + i] - s;
-    }
-    for (int i = threadIdx.x; i < op.k; i += blockDim.x) v[m + i] = W[op.b + i];
-    __syncthreads();
-    for (int i = warp; i < n; i += nw) {
-      const double* row = op.LU + (size_t)i * n;
-      double s = 0.0;
-      for (int j = lane; j < n; j += 32) s = fma(row[j], v[j], s);
-      s = warp_sum(s);
-      if (lane == 0) {
-        if (i < m) W[op.c + i] = s;
-        else W[op.d + i - m] = s;
+      for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+        const ListEnt e = lists[l];
+        for (int j = lane; j < e.len; j += 32) s = fma(row[e.off + j], W[e.slot + j], s);
       }
+      s = warp_sum(s);
+      if (lane == 0) W[op.g + i] = W[op.a + i] - s;
+    }
+    return;
+  }
+  if (t.r0 < m) {
+    for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
+      const ListEnt e = lists[l];
+      for (int j = threadIdx.x; j < e.len; j += blockDim.x) gsol[e.off + j] = W[e.slot + j];
     }
     __syncthreads();
+  }
+  for (int i = t.r0 + warp; i < t.r1; i += 8) {
+    if (i >= m) {  // v[m:] = sol_y
+      if (lane == 0) W[op.g + i] = W[op.b + i - m];
+      continue;
+    }
+    const double* row = op.M + (size_t)i * op.ldm;
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
+    s = warp_sum(s);
+    if (lane == 0) W[op.g + i] = W[op.a + i] - s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+solve_bwd_x_kernel(const SolveOp* __restrict__ ops, const SolveTask* __restrict__ tasks,
+                   double* __restrict__ W) {
+  const SolveTask t = tasks[blockIdx.x];
+  const SolveOp& op = ops[t.op];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = op.m, n = op.n;
+  const double* v = W + op.g;
+  for (int i = t.r0 + warp; i < t.r1; i += 8) {
+    const double* row = op.LU + (size_t)i * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(row[j], v[j], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (i < m) W[op.c + i] = s;
+      else W[op.d + i - m] = s;
+    }
   }
 }
 
@@ -198,27 +264,33 @@ __global__ void top_perm_kernel(const int* piv, int n, double* v) {
       if (p != j) { const double t = v[j]; v[j] = v[p]; v[p] = t; }
     }
 }
-__global__ void top_diag_kernel(const double* LU, int n, int b0, int bs, double* v, int upper) {
-  const int lane = threadIdx.x;
-  if (!upper) {
-    for (int i = b0 + 1; i < b0 + bs; ++i) {
-      const double* L = LU + (size_t)i * n;
-      double s = 0.0;
-      for (int j = b0 + lane; j < i; j += 32) s = fma(L[j], v[j], s);
-      s = warp_sum(s);
-      if (lane == 0) v[i] -= s;
-      __syncwarp();
+// Triangular solve of one bs x bs diagonal block (bs <= 128), column
+// oriented: the block sits in shared memory, x_j is final after step j and
+// every later row subtracts L[i][j] x_j in parallel (one barrier per column).
+__global__ void __launch_bounds__(128)
+top_diag_kernel(const double* LU, int n, int b0, int bs, double* v, int upper) {
+  extern __shared__ double blk[];  // bs x bs, then bs
+  double* x = blk + bs * bs;
+  for (int e = threadIdx.x; e < bs * bs; e += blockDim.x)
+    blk[e] = LU[(size_t)(b0 + e / bs) * n + b0 + e % bs];
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) x[i] = v[b0 + i];
+  __syncthreads();
+  if (!upper) {  // unit lower
+    for (int j = 0; j < bs - 1; ++j) {
+      const double xj = x[j];
+      for (int i = j + 1 + threadIdx.x; i < bs; i += blockDim.x) x[i] = fma(-blk[i * bs + j], xj, x[i]);
+      __syncthreads();
     }
   } else {
-    for (int i = b0 + bs - 1; i >= b0; --i) {
-      const double* U = LU + (size_t)i * n;
-      double s = 0.0;
-      for (int j = i + 1 + lane; j < b0 + bs; j += 32) s = fma(U[j], v[j], s);
-      s = warp_sum(s);
-      if (lane == 0) v[i] = (v[i] - s) / U[i];
-      __syncwarp();
+    for (int j = bs - 1; j >= 0; --j) {
+      if (threadIdx.x == 0) x[j] = x[j] / blk[j * bs + j];
+      __syncthreads();
+      const double xj = x[j];
+      for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] = fma(-blk[i * bs + j], xj, x[i]);
+      __syncthreads();
     }
   }
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) v[b0 + i] = x[i];
 }
 // rows [r0, r1): v[i] -= sum_{j in [c0, c0+bs)} A[i][j] v[j]
 __global__ void top_update_kernel(const double* LU, int n, int r0, int r1, int c0, int bs,
@@ -383,6 +455,7 @@ void Factor::build_program(const std::vector<int>& final_size) {
     int csrc = 0;
     for (int w : E.src_w) csrc += w;
     o.cols = csrc;
+    P.max_csrc = std::max(P.max_csrc, csrc);
     o.list0 = (int)lists.size(); o.nlist = (int)E.src.size();
     std::vector<long long> rd, wr;
     rd.push_back(o.b);
@@ -397,7 +470,11 @@ void Factor::build_program(const std::vector<int>& final_size) {
     bops.push_back(o);
     bwave.push_back(wave_for(rd, wr));
   }
-  const long long wtot = top;
+  // per-op scratch (g forward, v backward): one n-vector per elimination
+  long long scr = top;
+  for (auto& o : fops) { o.g = scr; scr += o.n; }
+  for (size_t i = 0; i < bops.size(); ++i) bops[i].g = fops[fops.size() - 1 - i].g;  // same event
+  const long long wtot = scr;
   auto order_by = [](const std::vector<int>& wv, std::vector<int>& starts) {
     std::vector<int> idx(wv.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
@@ -419,72 +496,161 @@ void Factor::build_program(const std::vector<int>& final_size) {
   P.fwd_waves = (int)P.fwd_wave_start.size() - 1;
   P.bwd_waves = (int)P.bwd_wave_start.size() - 1;
   P.smem = max_smem;
+  // row tasks: two launches per wave (kinds 0/1 forward, 2/3 backward)
+  std::vector<SolveTask> tasks;
+  P.task_start.clear();
+  P.launch_kind.clear();
+  auto rows = [&](int op, int list, int nrows) {
+    for (int r0 = 0; r0 < nrows; r0 += kSolveRowsPerTask)
+      tasks.push_back({op, list, r0, std::min(nrows, r0 + kSolveRowsPerTask)});
+  };
+  auto launch = [&](int kind) { P.task_start.push_back((int)tasks.size()); P.launch_kind.push_back(kind); };
+  P.bytes = 0;
+  for (int w = 0; w < P.fwd_waves; ++w) {
+    launch(0);
+    for (int o = P.fwd_wave_start[w]; o < P.fwd_wave_start[w + 1]; ++o) {
+      rows(o, -1, all[o].n);
+      P.bytes += 8.0 * all[o].n * all[o].m;
+    }
+    launch(1);
+    for (int o = P.fwd_wave_start[w]; o < P.fwd_wave_start[w + 1]; ++o)
+      for (int l = all[o].list0; l < all[o].list0 + all[o].nlist; ++l) {
+        rows(o, l, lists[l].len);
+        P.bytes += 8.0 * lists[l].len * all[o].m;
+      }
+  }
+  const int n_fwd_launch = (int)P.launch_kind.size();
+  for (int w = 0; w < P.bwd_waves; ++w) {
+    launch(2);
+    for (int o = P.n_fwd + P.bwd_wave_start[w]; o < P.n_fwd + P.bwd_wave_start[w + 1]; ++o) {
+      rows(o, -1, all[o].n);
+      P.bytes += 8.0 * all[o].m * all[o].cols;
+    }
+    launch(3);
+    for (int o = P.n_fwd + P.bwd_wave_start[w]; o < P.n_fwd + P.bwd_wave_start[w + 1]; ++o) {
+      rows(o, -1, all[o].n);
+      P.bytes += 8.0 * all[o].n * all[o].n;
+    }
+  }
+  P.task_start.push_back((int)tasks.size());
+  P.n_fwd_launch = n_fwd_launch;
+  P.bytes += 8.0 * (double)P.top_n * P.top_n;  // both triangles of the top LU, once
   const size_t ob = all.size() * sizeof(SolveOp), lb = lists.size() * sizeof(ListEnt);
+  const size_t tb = tasks.size() * sizeof(SolveTask);
   P.ops_d = C.alloc(1, (int)(ob / 8 + 1));
   P.list_d = C.alloc(1, (int)(lb / 8 + 1));
+  P.task_d = C.alloc(1, (int)(tb / 8 + 1));
   if (ob) CUDA_CHECK(cudaMemcpyAsync(P.ops_d.p, all.data(), ob, cudaMemcpyHostToDevice, C.st));
   if (lb) CUDA_CHECK(cudaMemcpyAsync(P.list_d.p, lists.data(), lb, cudaMemcpyHostToDevice, C.st));
+  if (tb) CUDA_CHECK(cudaMemcpyAsync(P.task_d.p, tasks.data(), tb, cudaMemcpyHostToDevice, C.st));
   P.work = C.alloc(1, (int)std::max<long long>(wtot, 1));
+  P.bin = C.alloc(1, std::max(n_points, 1));
+  P.bout = C.alloc(1, std::max(n_points, 1));
   C.sync();  // host vectors die here
+}
+
+// The solve program on stream s: permute b (P.bin) into the workspace, the
+// forward waves, the top-level LU solve, the backward waves, un-permute into
+// P.bout.  Captured once into a CUDA graph (Factor::solve).
+void Factor::enqueue_program(cudaStream_t s) {
+  Program& P = *prog;
+  const int N = n_points;
+  double* W = P.work.p;
+  const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
+  CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, s));
+  gather_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(P.bin.p, d_perm, N, W);
+  const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
+  const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
+  const SolveTask* tasks = reinterpret_cast<const SolveTask*>(P.task_d.p);
+  auto run = [&](int li) {
+    const int a = P.task_start[li], b = P.task_start[li + 1];
+    if (b <= a) return;
+    switch (P.launch_kind[li]) {
+      case 0: solve_fwd_g_kernel<<<b - a, 256, 0, s>>>(ops, tasks + a, W); break;
+      case 1: solve_fwd_t_kernel<<<b - a, 256, 0, s>>>(ops, lists, tasks + a, W); break;
+      case 2:
+        solve_bwd_v_kernel<<<b - a, 256, sizeof(double) * std::min(P.max_csrc, kGatherCap), s>>>(
+            ops, lists, tasks + a, W, kGatherCap);
+        break;
+      default: solve_bwd_x_kernel<<<b - a, 256, 0, s>>>(ops, tasks + a, W); break;
+    }
+  };
+  static const int parts = getenv("IFMM_SOLVE_PARTS") ? atoi(getenv("IFMM_SOLVE_PARTS")) : 7;
+  if (parts & 1)
+    for (int li = 0; li < P.n_fwd_launch; ++li) run(li);
+  if (!(parts & 2)) {
+  } else if (P.top_n > 0 && P.top_n <= 1024) {
+    top_solve_kernel<<<1, 1024, (size_t)P.top_n * sizeof(double), s>>>(
+        top_lu.p, top_piv, P.top_n, W + P.top_rhs, W + P.top_sol);
+  } else if (P.top_n > 0) {
+    // blocked getrs: a one-warp triangular solve per 128-row diagonal block,
+    // then a many-CTA GEMV update of the rows below (above) it
+    const int n = P.top_n, bs = 128;
+    double* v = W + P.top_sol;
+    CUDA_CHECK(cudaMemcpyAsync(v, W + P.top_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    top_perm_kernel<<<1, 32, 0, s>>>(top_piv, n, v);
+    for (int b0 = 0; b0 < n; b0 += bs) {  // L (unit) forward
+      const int b = std::min(bs, n - b0);
+      top_diag_kernel<<<1, 128, sizeof(double) * (b * b + b), s>>>(top_lu.p, n, b0, b, v, 0);
+      if (b0 + b < n)
+        top_update_kernel<<<(n - b0 - b + 7) / 8, 256, 0, s>>>(top_lu.p, n, b0 + b, n, b0, b, v);
+    }
+    for (int b0 = ((n - 1) / bs) * bs; b0 >= 0; b0 -= bs) {  // U backward
+      const int b = std::min(bs, n - b0);
+      top_diag_kernel<<<1, 128, sizeof(double) * (b * b + b), s>>>(top_lu.p, n, b0, b, v, 1);
+      if (b0 > 0) top_update_kernel<<<(b0 + 7) / 8, 256, 0, s>>>(top_lu.p, n, 0, b0, b0, b, v);
+    }
+  }
+  if (parts & 4)
+    for (int li = P.n_fwd_launch; li + 1 < (int)P.task_start.size(); ++li) run(li);
+  scatter_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(W + P.sol0, d_perm, N, P.bout.p);
+  CUDA_CHECK(cudaGetLastError());
 }
 
 void Factor::solve(const double* d_b, double* d_x) {
   Ctx& C = *ctx;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(solve_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(top_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(top_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(solve_bwd_v_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  IFMM_ASSERT(prog->smem <= 25000, "solve vector exceeds shared memory");
   Program& P = *prog;
   const int N = n_points;
-  double* W = P.work.p;
-  // algorithmic bytes: P^{-1}[:, :m] + T (forward), S + P^{-1} (backward)
-  double solve_bytes = 0;
-  for (auto& e : elims) {
-    const double n = e.m + e.k;
-    solve_bytes += 8.0 * (n * e.m + n * n + (double)e.Tstk.r * e.m + (double)e.m * e.Scat.c);
-  }
-  const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
-  CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, C.st));
-  gather_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(d_b, d_perm, N, W);
-  const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
-  const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
-  const size_t smem = (size_t)std::max(P.smem, 1) * sizeof(double);
+  CUDA_CHECK(cudaMemcpyAsync(P.bin.p, d_b, sizeof(double) * N, cudaMemcpyDeviceToDevice, C.st));
   cudaEvent_t ka = nullptr;
-  C.kt_begin(K_SOLVE, 0, &ka);
-  for (int w = 0; w < P.fwd_waves; ++w) {
-    const int a = P.fwd_wave_start[w], b = P.fwd_wave_start[w + 1];
-    solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
+  if (P.nsolves++ == 0) {
+    // first right-hand side: launch the program directly (a one-off solve
+    // does not pay for graph instantiation)
+    C.kt_begin(K_SOLVE, P.bytes, &ka);
+    enqueue_program(C.st);
+    C.kt_end(K_SOLVE, P.bytes, ka);
+    CUDA_CHECK(cudaMemcpyAsync(d_x, P.bout.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, C.st));
+    C.launches += (long long)P.launch_kind.size() + 3;
+    return;
   }
-  if (P.top_n > 0 && P.top_n <= 20000) {
-    top_solve_kernel<<<1, 1024, (size_t)P.top_n * sizeof(double), C.st>>>(
-        top_lu.p, top_piv, P.top_n, W + P.top_rhs, W + P.top_sol);
-  } else if (P.top_n > 0) {
-    const int n = P.top_n, bs = 256;
-    double* v = W + P.top_sol;
-    CUDA_CHECK(cudaMemcpyAsync(v, W + P.top_rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, C.st));
-    top_perm_kernel<<<1, 32, 0, C.st>>>(top_piv, n, v);
-    for (int b0 = 0; b0 < n; b0 += bs) {  // L (unit) forward
-      const int b = std::min(bs, n - b0);
-      top_diag_kernel<<<1, 32, 0, C.st>>>(top_lu.p, n, b0, b, v, 0);
-      if (b0 + b < n)
-        top_update_kernel<<<(n - b0 - b + 7) / 8, 256, 0, C.st>>>(top_lu.p, n, b0 + b, n, b0, b, v);
+  if (!P.graph) {
+    // repeated solves (GMRES preconditioning, many rhs): capture the fixed
+    // program once; replays differ only in P.bin's content
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(C.st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_program(C.st);
+    } catch (...) {
+      cudaStreamEndCapture(C.st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
     }
-    for (int b0 = ((n - 1) / bs) * bs; b0 >= 0; b0 -= bs) {  // U backward
-      const int b = std::min(bs, n - b0);
-      top_diag_kernel<<<1, 32, 0, C.st>>>(top_lu.p, n, b0, b, v, 1);
-      if (b0 > 0) top_update_kernel<<<(b0 + 7) / 8, 256, 0, C.st>>>(top_lu.p, n, 0, b0, b0, b, v);
-    }
+    CUDA_CHECK(cudaStreamEndCapture(C.st, &g));
+    CUDA_CHECK(cudaGraphInstantiate(&P.graph, g, 0));
+    cudaGraphDestroy(g);
   }
-  for (int w = 0; w < P.bwd_waves; ++w) {
-    const int a = P.n_fwd + P.bwd_wave_start[w], b = P.n_fwd + P.bwd_wave_start[w + 1];
-    solve_wave_kernel<<<std::min(b - a, 65535), 256, smem, C.st>>>(ops, lists, a, b - a, W);
-  }
-  scatter_perm_kernel<<<(N + 255) / 256, 256, 0, C.st>>>(W + P.sol0, d_perm, N, d_x);
-  C.kt_end(K_SOLVE, solve_bytes, ka);
-  C.launches += 3 + P.fwd_waves + P.bwd_waves;
+  C.kt_begin(K_SOLVE, P.bytes, &ka);
+  CUDA_CHECK(cudaGraphLaunch(P.graph, C.st));
+  C.kt_end(K_SOLVE, P.bytes, ka);
+  CUDA_CHECK(cudaMemcpyAsync(d_x, P.bout.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, C.st));
+  C.launches += (long long)P.launch_kind.size() + 3;
   CUDA_CHECK(cudaGetLastError());
 }
 

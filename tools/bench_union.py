@@ -60,3 +60,6 @@ for m, ko, kf in sizes:
     print(f"m={m:5d} C={ko + kf:4d} s={s:4d} rank={int(dr.item()):4d} wall {dt * 1e3:8.2f} ms | Mcycles "
           f"aca {u[0] / 1e6:7.2f} cholqr {u[1] / 1e6:7.2f} jacobi {u[3] / 1e6:7.2f} (sweeps {u[11]}) "
           f"out {u[4] / 1e6:6.2f}", flush=True)
+    if u[39]:
+        print(f"   cholqr parts (m>400): scale+gram1+chol1 {u[38] / 1e6:.3f} trsm1 {u[34] / 1e6:.3f} "
+              f"gram2 {u[35] / 1e6:.3f} chol2 {u[36] / 1e6:.3f} trsm2+trmul {u[37] / 1e6:.3f}", flush=True)
