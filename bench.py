@@ -12,7 +12,14 @@ assembly (factorize consumes its graph) -- is outside the timed region.
   e2e    : same, but every step's solve goes through the public API with a
            HOST numpy rhs (h2d of b and d2h of x inside the timed region)
   roofline : dominant device kernel category of one extra instrumented step
-  cpu_baseline : the numpy oracle port on a bounded same-recipe sample
+  cpu_baseline : the numpy oracle port on a bounded same-recipe sample, plus
+           the unmodified reference timed on the FULL config once in the build
+           container (full_size_reference, from tests/golden/mid/)
+  parity : |x - x_reference| and the exact-matvec residuals of ours and of
+           the reference's committed solution of the same config
+--schedule: "wavefront" (default: the fastest; clusters at Chebyshev
+distance >= 3 batched) or "reference" (Morton order + the reference's PCG64
+sketch stream); see paper_1508_01835_b200.factor.factorize.
 
 `--impl reference` times the CPU reference path (the oracle port of the
 reference; the unmodified reference is Python and not installable on the
@@ -42,7 +49,7 @@ CONFIGS = {
     "c3": (262144, 3, 2, "imq", 64, 4, 1e-6),
     "c4": (1048576, 3, 3, "imq", 64, 4, 1e-6),
 }
-DEFAULT_CONFIG = "c3"  # the headline recipe (3D IMQ, eps=1e-6) at the largest N a default run finishes in minutes
+DEFAULT_CONFIG = "c3"  # the headline recipe (3D IMQ, eps=1e-6) at the largest N whose 5+20-step driver run fits its time cap
 METRIC = "IFMM factorize+solve unknowns/s"
 # CPU sample sizes for the oracle leg (about 10-30 s of single-core work)
 CPU_SAMPLE_N = {"c1": 4096, "c2": 8192, "c3": 4096, "c4": 4096}
@@ -60,6 +67,17 @@ def inputs(cfg, n=None):
     b = gb.uniform(-1.0, 1.0, N) if dim == 2 else gb.standard_normal(N)
     h = N ** (-1.0 / 3.0)
     return dict(N=N, pts=pts, b=b, kern=kern, h=h, leaf=leaf, nc=nc, eps=eps, dim=dim)
+
+
+def reference_golden(cfg):
+    """The unmodified reference's solution of the full config, if committed."""
+    name = {"c2": "c2_exp2d_n65536", "c3": "c3_imq3d_n262144"}.get(cfg)
+    path = os.path.join(ROOT, "tests", "golden", "mid", f"{name}.npz") if name else None
+    if not path or not os.path.exists(path):
+        return None
+    g = np.load(path)
+    return {"x": g["x"], "sigma0": float(g["sigma0"]), "t": float(g["t_factorize"]) + float(g["t_solve"]),
+            "levels": g["lv_compressed"].tolist()}
 
 
 def workload_desc(cfg, inp):
@@ -86,8 +104,10 @@ def cpu_oracle_rate(cfg, threads):
         x = f.solve(inp["b"])
         dt = time.perf_counter() - t0
     del x
-    sample = (f"oracle numpy port of the reference path, {cfg} recipe at N={n} "
-              f"(sigma0+factorize+solve {dt:.2f} s)")
+    sample = (f"oracle numpy port of the reference path (pinned bitwise to the reference on "
+              f"c2 / mid goldens), {cfg} recipe at a bounded N={n} (depth {tree.depth}; "
+              f"sigma0+factorize+solve {dt:.2f} s on {threads} thread(s)); the per-unknown "
+              f"rate falls with N (see full_size_reference)")
     return n / dt, dt, sample
 
 
@@ -95,7 +115,9 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = args.config
-    threads = os.cpu_count() or 1
+    # single BLAS thread: faster than all cores for this small-block numpy
+    # code (12-13 s with 1 thread vs ~19 s with 8)
+    threads = 1
     times = []
     n = CPU_SAMPLE_N[cfg]
     for i in range(args.warmup + args.steps):
@@ -111,10 +133,22 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_desc(cfg, inp),
             "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample,
+                             "full_size_reference": full_size_reference(cfg)},
             "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def full_size_reference(cfg):
+    """The unmodified reference on the full config, measured once in the build
+    container (1 thread): unknowns/s, or None when not measured."""
+    g = reference_golden(cfg)
+    if g is None:
+        return None
+    N = CONFIGS[cfg][0]
+    return {"N": N, "seconds": round(g["t"], 1), "unknowns_per_s": N / g["t"], "cores": 1,
+            "source": "tests/golden/mid (make_golden_mid.py), unmodified reference package"}
 
 
 # ---------------------------------------------------------------------------
@@ -202,6 +236,7 @@ def run_ours(args, rank, world):
         # leave ~22 GB outside the arena for the dedicated >= 256 MB blocks
         os.environ["IFMM_ARENA_GB"] = f"{max(0.5 * free, free - 22 * 2**30) / 2**30:.1f}"
     cfg = args.config
+    sched = args.schedule
     inp = inputs(cfg, args.n)
     N = inp["N"]
     K = P.exp_kernel() if inp["kern"] == "exp" else P.imq_kernel(inp["h"])
@@ -231,7 +266,7 @@ def run_ours(args, rank, world):
         NN.lib().ifmm_dev_sync(NN.ctx())
         NN.event(0)
         s0 = P.estimate_sigma0(graph, seed=0)
-        fct = P.factorize(graph, inp["eps"], seed=0, sigma0=s0)
+        fct = P.factorize(graph, inp["eps"], seed=0, sigma0=s0, schedule=sched)
         NN.event(1)
         x = fct.solve(b_host if host_rhs else b_dev)
         NN.event(2)
@@ -271,8 +306,18 @@ def run_ours(args, rank, world):
     kt = NN.ktime(0)
     if state["ops"] is None:
         state["ops"] = make_ops()
-    res = float(np.linalg.norm(P.h2_matvec(state["ops"], x.cpu().numpy()) - b_host) /
-                np.linalg.norm(b_host))
+    xh = x.cpu().numpy()
+    res = float(np.linalg.norm(P.h2_matvec(state["ops"], xh) - b_host) / np.linalg.norm(b_host))
+    parity = {"schedule": sched, "factorize_levels_compressed": [s.compressed_pairs for s in fct.stats.levels]}
+    gold = reference_golden(cfg) if args.n is None else None
+    if gold is not None:
+        Kx = P.exact_matvec(inp["pts"], K, xh)
+        parity.update({
+            "rel_diff_x_vs_reference": float(np.linalg.norm(xh - gold["x"]) / np.linalg.norm(gold["x"])),
+            "exact_residual": float(np.linalg.norm(Kx - b_host) / np.linalg.norm(b_host)),
+            "reference_exact_residual": float(np.linalg.norm(P.exact_matvec(inp["pts"], K, gold["x"]) - b_host)
+                                              / np.linalg.norm(b_host)),
+            "reference_levels_compressed": gold["levels"]})
     del fct, x
     dom = max(kt.items(), key=lambda kv: kv[1][0])
     cat, (ksec, kwork, kcnt) = dom
@@ -300,13 +345,15 @@ def run_ours(args, rank, world):
             "ms_per_step": 1e3 * tot_dev / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md 8d seeded recipe)",
-            "config": dict(workload_desc(cfg, inp), parallelism=f"replicas{world}"),
+            "config": dict(workload_desc(cfg, inp), parallelism=f"replicas{world}", schedule=sched),
             "e2e": {"value": e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": {"value": cpu_rate, "unit": "unknowns/s", "cores": 1,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample,
+                             "full_size_reference": full_size_reference(cfg)},
+            "parity": parity,
             "clocks": clk,
             "detail": {"t_factorize_s": statistics.mean(tf), "t_solve_dev_s": statistics.mean(ts),
                        "t_solve_host_s": statistics.mean(tsh), "t_setup_s": t_setup,
@@ -323,6 +370,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None, help="override N (diagnostics)")
+    ap.add_argument("--schedule", default=os.environ.get("IFMM_SCHEDULE", "wavefront"),
+                    choices=["wavefront", "reference"],
+                    help="factorize schedule (paper_1508_01835_b200.factor.factorize)")
     ap.add_argument("--consume-from", type=int, default=500000,
                     help="N at/above which graphs consume (move) the operator blocks")
     args = ap.parse_args()

@@ -103,6 +103,14 @@ typedef int (*ifmm_normal_source)(void* user, int op, long long n, double* out);
  * reference's order; implies Morton cluster order (flags bit2).           */
 void* ifmm_factorize_rng(void* graph, double epsilon, double sigma0, int flags,
                          ifmm_normal_source src, void* user);
+/* The same with the stream generated natively: numpy's PCG64 state as
+ * {state_hi, state_lo, inc_hi, inc_lo} (np.random.PCG64(seed).state), its
+ * standard normals from numpy's own ziggurat (libnpyrandom) -- bitwise
+ * Generator(PCG64(seed)).standard_normal.                                 */
+void* ifmm_factorize_pcg64(void* graph, double epsilon, double sigma0, int flags,
+                           const unsigned long long* pcg_state);
+/* n standard normals of that stream from a given state (host; tests).     */
+int ifmm_pcg64_normals(const unsigned long long* pcg_state, long long n, double* out);
 void ifmm_factor_destroy(void* factor);
 /* Scalar stats: out[0..] = peak_edges, n_clusters, max_basis_rank,
  * max_fill_rank, forced_rank_truncations, n_levels, n_events_elim,

@@ -54,6 +54,8 @@ _SIGS = {
     "ifmm_graph_sigma0": (C.c_int, [vp, dp, C.c_int, C.c_int, dp]),
     "ifmm_factorize": (vp, [vp, C.c_double, C.c_double, C.c_int]),
     "ifmm_factorize_rng": (vp, [vp, C.c_double, C.c_double, C.c_int, vp, vp]),
+    "ifmm_factorize_pcg64": (vp, [vp, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_ulonglong)]),
+    "ifmm_pcg64_normals": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_longlong, dp]),
     "ifmm_factor_level_times": (C.c_int, [vp, dp, C.c_int]),
     "ifmm_factor_events": (C.c_longlong, [vp, lp, C.c_longlong]),
     "ifmm_factor_layout": (C.c_int, [vp, ip, ip, ip, ip, ip, ip, ip]),
@@ -201,7 +203,7 @@ def as_lp(a: np.ndarray):
 
 
 PROFILE_PHASES = ("lu", "xsolve", "schur", "add", "fillsvd", "union", "rebase", "newk", "merge",
-                  "top", "host")
+                  "top", "host", "rsvd")
 
 
 def profile():

@@ -422,6 +422,21 @@ void* ifmm_factorize(void* graph, double epsilon, double sigma0, int flags) {
   ABI_CATCH_NULL
 }
 
+void* ifmm_factorize_pcg64(void* graph, double epsilon, double sigma0, int flags,
+                           const unsigned long long* pcg_state) {
+  ABI_TRY
+  uint64_t st[4] = {pcg_state[0], pcg_state[1], pcg_state[2], pcg_state[3]};
+  return factorize_pcg64((Graph*)graph, epsilon, sigma0, flags, st);
+  ABI_CATCH_NULL
+}
+
+int ifmm_pcg64_normals(const unsigned long long* pcg_state, long long n, double* out) {
+  ABI_TRY
+  uint64_t st[4] = {pcg_state[0], pcg_state[1], pcg_state[2], pcg_state[3]};
+  return pcg64_normals(st, n, out);
+  ABI_CATCH
+}
+
 void* ifmm_factorize_rng(void* graph, double epsilon, double sigma0, int flags,
                          ifmm_normal_source src, void* user) {
   ABI_TRY
@@ -595,7 +610,7 @@ int ifmm_union_profile(unsigned long long* out, int reset) {
 }
 
 int ifmm_profile(double* out, int n) {
-  for (int i = 0; i < n && i < 11; ++i) out[i] = ifmm::g_prof[i];
+  for (int i = 0; i < n && i < 12; ++i) out[i] = ifmm::g_prof[i];
   return 0;
 }
 

@@ -194,6 +194,10 @@ typedef int (*NormalSource)(void* user, int op, long long n, double* out);
 // fill; bit2: Morton cluster order (one cluster per wave; implied by src).
 Factor* factorize(Graph* g, double eps, double sigma0, int flags, NormalSource src = nullptr,
                   void* src_user = nullptr);
+// factorize with the reference stream generated natively: PCG64 state / inc
+// as (hi, lo) 64-bit halves, st = {state_hi, state_lo, inc_hi, inc_lo}
+Factor* factorize_pcg64(Graph* g, double eps, double sigma0, int flags, const uint64_t st[4]);
+int pcg64_normals(const uint64_t st[4], long long n, double* out);
 
 // blocked LU for large pivot blocks (host-driven panels)
 void lu_blocked(Ctx& ctx, double* A, int n, int lda, int* piv, int tag);

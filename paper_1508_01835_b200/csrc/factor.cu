@@ -20,12 +20,139 @@
 #include <cmath>
 #include <map>
 #include <random>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 
 #include "engine.h"
 
+// numpy's own standard-normal sampler (the ziggurat of
+// numpy/random/src/distributions, linked from numpy's static libnpyrandom)
+// driven by a native PCG64 below: together, bit for bit the stream of
+// np.random.Generator(np.random.PCG64(seed)).standard_normal.
+extern "C" {
+struct npy_bitgen {
+  void* state;
+  uint64_t (*next_uint64)(void* st);
+  uint32_t (*next_uint32)(void* st);
+  double (*next_double)(void* st);
+  uint64_t (*next_raw)(void* st);
+};
+void random_standard_normal_fill(npy_bitgen* bitgen_state, long cnt, double* out);
+}
+
 namespace ifmm {
+
+// PCG64 (O'Neill's pcg_setseq_128 with the XSL-RR 128/64 output), numpy's
+// default bit generator: step, then output from the new state.
+struct Pcg64 {
+  unsigned __int128 state = 0, inc = 0;
+  static uint64_t next64(void* p) {
+    Pcg64& g = *static_cast<Pcg64*>(p);
+    const unsigned __int128 mul =
+        ((unsigned __int128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+    g.state = g.state * mul + g.inc;
+    const uint64_t x = (uint64_t)(g.state >> 64) ^ (uint64_t)g.state;
+    const unsigned rot = (unsigned)(g.state >> 122);
+    return (x >> rot) | (x << ((-rot) & 63));
+  }
+  static uint32_t next32(void* p) { return (uint32_t)(next64(p) >> 32); }  // unused by normals
+  static double next_double(void* p) { return (double)(next64(p) >> 11) * (1.0 / 9007199254740992.0); }
+  void fill(double* out, long long n) {
+    npy_bitgen bg{this, &Pcg64::next64, &Pcg64::next32, &Pcg64::next_double, &Pcg64::next64};
+    random_standard_normal_fill(&bg, (long)n, out);
+  }
+};
+
+// Native reference stream: the NormalSource protocol over the PCG64 normal
+// sequence.  The sequence is fixed, so a saved state is just a position:
+// a producer thread runs ahead of the consumer filling 1 M-normal chunks
+// (hidden behind the device work), draws copy [pos, pos + n) out of the
+// chunks, save / restore record / reset pos.  Chunks far behind pos are freed.
+struct PcgSource {
+  static constexpr long long kChunk = 1 << 20, kAhead = 24 * kChunk, kKeep = 32 * kChunk;
+  Pcg64 g;                                   // producer-owned
+  std::map<long long, std::vector<double>> chunks;  // chunk index -> normals
+  long long produced = 0, pos = 0;           // normals generated / consumer position
+  std::vector<long long> slots;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool stop = false;
+  std::thread th;
+  void start() { th = std::thread([this] { run(); }); }
+  ~PcgSource() {
+    { std::lock_guard<std::mutex> l(mu); stop = true; }
+    cv.notify_all();
+    if (th.joinable()) th.join();
+  }
+  void run() {
+    std::vector<double> buf(kChunk);
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(mu);
+        cv.wait(l, [&] { return stop || produced < pos + kAhead; });
+        if (stop) return;
+      }
+      g.fill(buf.data(), kChunk);  // outside the lock
+      std::lock_guard<std::mutex> l(mu);
+      chunks[produced / kChunk] = buf;
+      produced += kChunk;
+      const long long lo = (pos - kKeep) / kChunk;  // free what no restore can reach
+      while (!chunks.empty() && chunks.begin()->first < lo) chunks.erase(chunks.begin());
+      cv.notify_all();
+    }
+  }
+  void copy_out(long long p, long long n, double* out) {
+    std::unique_lock<std::mutex> l(mu);
+    cv.notify_all();
+    cv.wait(l, [&] { return produced >= p + n; });
+    while (n > 0) {
+      const long long ci = p / kChunk, o = p % kChunk;
+      const long long take = std::min(n, kChunk - o);
+      const std::vector<double>& c = chunks.at(ci);
+      std::memcpy(out, c.data() + o, sizeof(double) * take);
+      out += take; p += take; n -= take;
+    }
+  }
+  static int call(void* user, int op, long long n, double* out) {
+    PcgSource& s = *static_cast<PcgSource*>(user);
+    if (op == 0) {
+      s.copy_out(s.pos, n, out);
+      std::lock_guard<std::mutex> l(s.mu);
+      s.pos += n;
+      s.cv.notify_all();
+      return 0;
+    }
+    if (n < 0) return 1;
+    if (op == 1) { if ((long long)s.slots.size() <= n) s.slots.resize(n + 1); s.slots[n] = s.pos; return 0; }
+    if (op == 2) {
+      if (n >= (long long)s.slots.size() || s.slots[n] < s.pos - kKeep) return 1;
+      std::lock_guard<std::mutex> l(s.mu);
+      s.pos = s.slots[n];
+      return 0;
+    }
+    return 1;
+  }
+};
+
+int pcg64_normals(const uint64_t st[4], long long n, double* out) {
+  Pcg64 g;
+  g.state = ((unsigned __int128)st[0] << 64) | st[1];
+  g.inc = ((unsigned __int128)st[2] << 64) | st[3];
+  g.fill(out, n);
+  return 0;
+}
+
+Factor* factorize_pcg64(Graph* g, double eps, double sigma0, int flags, const uint64_t st[4]) {
+  PcgSource src;
+  src.g.state = ((unsigned __int128)st[0] << 64) | st[1];
+  src.g.inc = ((unsigned __int128)st[2] << 64) | st[3];
+  src.start();
+  return factorize(g, eps, sigma0, flags, &PcgSource::call, &src);
+}
 
 static constexpr int TOP_TAG = 0x7fffffff - 1;
 
@@ -33,7 +160,7 @@ static constexpr int TOP_TAG = 0x7fffffff - 1;
 // IFMM_PROFILE=1: stream-synchronised phase timers (diagnostics; perturbs
 // overlap, never used for reported numbers)
 enum { PH_LU = 0, PH_XSOLVE, PH_SCHUR, PH_ADD, PH_FILLSVD, PH_UNION, PH_REBASE, PH_NEWK, PH_MERGE,
-       PH_TOP, PH_HOST, PH_N };
+       PH_TOP, PH_HOST, PH_RSVD, PH_N };
 double g_prof[PH_N];
 // IFMM_PROFILE=2: host-only phase timers (no synchronisation): host
 // enqueue/bookkeeping cost per phase.
@@ -382,11 +509,12 @@ struct Eliminator {
   struct RsvdAct { int i, m, n, full, k_try; };
   std::vector<int> rsvd_round(std::vector<SvdDesc>& sd, std::vector<RsvdAct>& act,
                               const std::vector<unsigned long long>* keys,
-                              const std::vector<double>* h_omega);
+                              const std::vector<double, PinnedAlloc<double>>* h_omega);
   void rsvd_fills(std::vector<SvdDesc>& sd, const std::vector<int>& big,
                   const std::vector<unsigned long long>& keys, int* dr);
   void rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>& order);
   unsigned long long rsvd_redraws = 0;
+  std::vector<double, PinnedAlloc<double>> rs_h;
   void merge(int level);
   void top();
 };
@@ -1070,6 +1198,30 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     adds.run(C);
   }
   delete ph;
+  // IFMM_DUMP=E,cj,ck,file: raw fills (ck, cj) and (cj, ck) of one pair when
+  // cluster E is eliminated (parity triage; row-major doubles after a
+  // "rows cols" text line per block)
+  if (const char* dp = getenv("IFMM_DUMP")) {
+    int E = -1, dj = -1, dk = -1;
+    char path[512] = {0};
+    if (sscanf(dp, "%d,%d,%d,%511s", &E, &dj, &dk, path) == 4)
+      for (size_t wi = 0; wi < ws.size(); ++wi) {
+        if (ws[wi].c != E) continue;
+        FILE* f = fopen(path, "wb");
+        for (auto key : {std::make_pair(dk, dj), std::make_pair(dj, dk)}) {
+          auto it = stash[wi].find(key);
+          if (it == stash[wi].end()) { fprintf(f, "0 0\n"); continue; }
+          const Stash& st = it->second;
+          std::vector<double> hb((size_t)st.h * st.w);
+          CUDA_CHECK(cudaMemcpy2DAsync(hb.data(), 8 * (size_t)st.w, ws[wi].Fm.p + (size_t)st.ro * ws[wi].NC + st.co,
+                                       8 * (size_t)ws[wi].NC, 8 * (size_t)st.w, st.h, cudaMemcpyDeviceToHost, C.st));
+          C.sync();
+          fprintf(f, "%d %d\n", st.h, st.w);
+          fwrite(hb.data(), 8, hb.size(), f);
+        }
+        fclose(f);
+      }
+  }
   // ---- fill compression of every stashed block of the wave, one launch ----
   std::vector<std::pair<std::pair<int, int>, Stash>> items;
   std::vector<size_t> first(ws.size() + 1, 0);
@@ -1136,6 +1288,7 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     else if (dsg) launch_svd(dsg, (int)sdg.size(), thr, 0, C.st, 0);
     C.kt_end(K_SVD, sflops, ka);
     if (!big.empty()) {
+      Phase pr(C, PH_RSVD);
       if (src) {
         // reference call order: cluster (wave slot), pair (min, max), F_kj (target = max) first
         std::vector<int> order(big);
@@ -1192,7 +1345,7 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
 // without it a counter-based device generator draws them.
 std::vector<int> Eliminator::rsvd_round(std::vector<SvdDesc>& sd, std::vector<RsvdAct>& act,
                                         const std::vector<unsigned long long>* keys,
-                                        const std::vector<double>* h_omega) {
+                                        const std::vector<double, PinnedAlloc<double>>* h_omega) {
   ++rsvd_calls;
   const int na = (int)act.size();
   std::vector<Blk> Om(na), Yt(na), Zt(na), Ow(na), Fw(na);
@@ -1206,7 +1359,7 @@ std::vector<int> Eliminator::rsvd_round(std::vector<SvdDesc>& sd, std::vector<Rs
   if (h_omega) {
     omb = C.alloc(1, (int)std::max<size_t>(h_omega->size(), 1));
     CUDA_CHECK(cudaMemcpyAsync(omb.p, h_omega->data(), h_omega->size() * 8, cudaMemcpyHostToDevice,
-                               C.st));
+                               C.st));  // pinned (host_buf): asynchronous
   }
   size_t ooff = 0;
   for (int t = 0; t < na; ++t) {
@@ -1302,7 +1455,8 @@ void Eliminator::rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>
     const int full = std::min(sd[i].m, sd[i].n);
     act.push_back({i, sd[i].m, sd[i].n, full, std::min(16, full)});
   }
-  std::vector<double> h, skip;
+  auto& h = rs_h;  // pinned, kept across clusters (grows, never shrinks)
+  std::vector<double> skip;
   while (!act.empty()) {
     // one save + one draw per round: the sketches of every pending call,
     // back to back in call order (call t's run starts at off[t])
@@ -1312,6 +1466,7 @@ void Eliminator::rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>
       off[t + 1] = off[t] + (size_t)a.n * std::min(a.k_try + 10, a.full);
     }
     src_op(1, 0);  // stream state at the start of the round
+    if (h.capacity() < off.back()) h.reserve(std::max(off.back(), 2 * h.capacity()));
     h.resize(off.back());
     draw(h.data(), (long long)h.size());
     std::vector<int> stop = rsvd_round(sd, act, nullptr, &h);

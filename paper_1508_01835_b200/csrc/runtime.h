@@ -72,6 +72,23 @@ class Arena {
   std::set<std::pair<size_t, size_t>> by_size_;   // (length, offset)
 };
 
+// Page-locked host allocator: host staging whose cudaMemcpyAsync is truly
+// asynchronous (the buffer must outlive the copy: callers sync before reuse).
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U> PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U> bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U> bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+
 // ---- dense block handle (row-major r x c, ld = c) ------------------------
 struct Blk {
   double* p = nullptr;

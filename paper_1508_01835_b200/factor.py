@@ -232,6 +232,13 @@ class _ReferenceStream:
 SCHEDULES = ("reference", "wavefront")
 
 
+def pcg64_state(seed):
+    """np.random.PCG64(seed)'s state as {state_hi, state_lo, inc_hi, inc_lo}."""
+    st = np.random.PCG64(seed).state["state"]
+    m = (1 << 64) - 1
+    return (C.c_ulonglong * 4)(st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m)
+
+
 def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
               sigma0: float | None = None, exact_order: bool | None = None,
               schedule: str | None = None) -> IFMMFactorization:
@@ -272,12 +279,10 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
     flags = 1 if exact_order else 0
     lib = N.lib()
     if schedule == "reference":
-        stream = _ReferenceStream(seed)
-        h = lib.ifmm_factorize_rng(graph._h, float(epsilon), float(sigma0), flags | 4,
-                                   C.cast(stream.cb, C.c_void_p), None)
-        if stream.error is not None and not h:
-            graph.consumed = True
-            raise stream.error
+        # the reference's Generator(PCG64(seed)) (factor.py:188), run natively
+        # in the engine (PCG64 + numpy's own ziggurat): bitwise the same draws
+        h = lib.ifmm_factorize_pcg64(graph._h, float(epsilon), float(sigma0), flags | 4,
+                                     pcg64_state(seed))
     else:
         h = lib.ifmm_factorize(graph._h, float(epsilon), float(sigma0), flags)
     graph.consumed = True

@@ -37,15 +37,22 @@ CASES = {
     "c2_exp2d_n65536": (65536, 2, 1, "exp", 64, 6, 1e-10),
     # c3 itself (BASELINE configs[2]); about an hour of CPU
     "c3_imq3d_n262144": (262144, 3, 2, "imq", 64, 4, 1e-6),
+    # the c3 recipe on a slab [0,1]^2 x [0,1/4]: depth 4 with 64-point leaves
+    # (compression at the leaf level AND at merged levels, as in c3) at 1/4 of
+    # c3's size
+    "imq_slab_n65536": (65536, 3, 2, "imq", 64, 4, 1e-6),
 }
+SLAB = {"imq_slab_n65536": 0.25}
 
 
-def inputs(N, dim, seed, kern):
+def inputs(N, dim, seed, kern, zscale=1.0):
     g = np.random.Generator(np.random.PCG64(seed))
     if dim == 2:
         pts = np.column_stack([g.uniform(0.0, 1.0, size=(N, 2)), np.zeros(N)])
     else:
         pts = g.uniform(0.0, 1.0, size=(N, 3))
+        if zscale != 1.0:
+            pts[:, 2] *= zscale
     gb = np.random.Generator(np.random.PCG64(seed + 1))
     b = gb.uniform(-1.0, 1.0, N) if dim == 2 else gb.standard_normal(N)
     return pts, b
@@ -56,7 +63,8 @@ def run(name, N, dim, seed, kern, leaf, n, eps):
     import ifmm.factor as F
     import ifmm.lowrank as L
     from scipy.spatial.distance import cdist
-    pts, b = inputs(N, dim, seed, kern)
+    zs = SLAB.get(name, 1.0)
+    pts, b = inputs(N, dim, seed, kern, zs)
     if kern == "exp":
         h = 0.0
         block = lambda P, Q: np.exp(-cdist(P, Q))  # noqa: E731
@@ -114,7 +122,7 @@ def run(name, N, dim, seed, kern, leaf, n, eps):
     lv = fct.stats.levels
     ranks = np.array([ops.rank.get(c, -1) for c in range(len(cl))], dtype=np.int32)
     out = dict(
-        N=N, dim=dim, seed=seed, kernel=kern, h=h, leaf=leaf, n=n, eps=eps,
+        N=N, dim=dim, seed=seed, kernel=kern, h=h, leaf=leaf, n=n, eps=eps, zscale=zs,
         depth=tree.depth, n_clusters=len(cl),
         perm_checksum=np.int64((perm.astype(np.int64) * np.arange(1, N + 1)).sum()),
         cl_start=np.array([c.start for c in cl], dtype=np.int32),

@@ -21,7 +21,11 @@ def mid_points(g):
     r = np.random.Generator(np.random.PCG64(seed))
     if dim == 2:
         return np.column_stack([r.uniform(0.0, 1.0, size=(N, 2)), np.zeros(N)])
-    return r.uniform(0.0, 1.0, size=(N, 3))
+    pts = r.uniform(0.0, 1.0, size=(N, 3))
+    zs = float(g["zscale"]) if "zscale" in g else 1.0
+    if zs != 1.0:
+        pts[:, 2] *= zs
+    return pts
 
 
 def mid_inputs(P, g):

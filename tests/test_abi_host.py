@@ -126,3 +126,19 @@ def test_kernel_plugin_contract():
     assert P.imq_kernel(0.1).device_spec() == (2, 0.1)
     with pytest.raises(ValueError):
         P.Kernel("custom", 1, {}, lambda P_, Q: None).device_spec()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 123456789])
+def test_native_pcg64_stream_is_numpys(seed):
+    """The engine's reference stream (native PCG64 + numpy's ziggurat from
+    libnpyrandom, factor.cu) is bitwise np.random.Generator(PCG64(seed))
+    .standard_normal -- the draws of the reference's factorize rng
+    (factor.py:188, lowrank.py:108)."""
+    import ctypes as C
+    from paper_1508_01835_b200 import _native as N
+    from paper_1508_01835_b200.factor import pcg64_state
+    n = 2_000_003
+    out = np.empty(n)
+    N.check(N.lib().ifmm_pcg64_normals(pcg64_state(seed), n, N.as_dp(out)))
+    ref = np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
+    assert np.array_equal(out, ref)

@@ -64,6 +64,12 @@ def main():
     x = fct.solve(b)
     rel = np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"])
     print(f"|x - x_ref|/|x_ref| = {rel:.3e} (10 eps = {10 * eps:.1e})")
+    nb = np.linalg.norm(b)
+    r_ours = np.linalg.norm(P.exact_matvec(pts, K, x) - b) / nb
+    r_ref = np.linalg.norm(P.exact_matvec(pts, K, g["x"]) - b) / nb
+    r_h2 = np.linalg.norm(P.h2_matvec(ops, x) - b) / nb if not getattr(ops, "consumed", False) else float("nan")
+    print(f"exact-matvec residual: ours {r_ours:.4e} reference {r_ref:.4e}")
+    np.save(os.path.join(ROOT, "gpurun_out", f"x_{name}_{schedule}.npy"), x)
     tr = os.environ.get("IFMM_TRACE")
     if not tr:
         return
