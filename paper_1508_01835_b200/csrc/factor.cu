@@ -156,6 +156,74 @@ Factor* factorize_pcg64(Graph* g, double eps, double sigma0, int flags, const ui
 
 static constexpr int TOP_TAG = 0x7fffffff - 1;
 
+// ---- IFMM_SYMCHECK (parity triage): asymmetry of the graph ----------------
+// For a symmetric kernel the extended matrix stays symmetric through the
+// elimination up to rounding; symcheck reports max ||E(a,b) - E(b,a)^T|| /
+// ||E(a,b)|| over all edge pairs (one CTA per pair).
+struct AsymDesc { const double* A; const double* B; int r, c; double* out; };
+__global__ void asym_kernel(const AsymDesc* d, int n) {
+  __shared__ double sd[2][32];
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const AsymDesc q = d[b];
+    double s1 = 0.0, s2 = 0.0;
+    for (int e = threadIdx.x; e < q.r * q.c; e += blockDim.x) {
+      const int i = e / q.c, j = e % q.c;
+      const double a = q.A[e], bt = q.B[(size_t)j * q.r + i];
+      s1 += (a - bt) * (a - bt);
+      s2 += a * a;
+    }
+    for (int o = 16; o; o >>= 1) { s1 += __shfl_xor_sync(0xffffffffu, s1, o); s2 += __shfl_xor_sync(0xffffffffu, s2, o); }
+    if ((threadIdx.x & 31) == 0) { sd[0][threadIdx.x >> 5] = s1; sd[1][threadIdx.x >> 5] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t1 = 0, t2 = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t1 += sd[0][w]; t2 += sd[1][w]; }
+      q.out[0] = t1; q.out[1] = t2;
+    }
+    __syncthreads();
+  }
+}
+static void symcheck(Ctx& C, Graph& g, const char* where) {
+  std::vector<AsymDesc> d;
+  std::vector<std::pair<int, int>> keys;
+  for (auto& kv : g.E) {
+    const int t = (int)(kv.first >> 32), s = (int)(kv.first & 0xffffffffu);
+    if (t > s) continue;
+    Blk* o = g.get(s, t);
+    if (!o || o->r != kv.second.c || o->c != kv.second.r || kv.second.r * kv.second.c == 0) continue;
+    d.push_back({kv.second.p, o->p, kv.second.r, kv.second.c, nullptr});
+    keys.push_back({t, s});
+  }
+  if (d.empty()) return;
+  Blk out = C.alloc(1, 2 * (int)d.size());
+  for (size_t i = 0; i < d.size(); ++i) d[i].out = out.p + 2 * i;
+  AsymDesc* dd = C.stage.push_vec(C, d);
+  asym_kernel<<<(int)std::min<size_t>(d.size(), 65535), 256, 0, C.st>>>(dd, (int)d.size());
+  std::vector<double> h(2 * d.size());
+  CUDA_CHECK(cudaMemcpyAsync(h.data(), out.p, 8 * h.size(), cudaMemcpyDeviceToHost, C.st));
+  C.sync();
+  double worst = 0, sum = 0;
+  size_t wi = 0;
+  int over = 0;
+  for (size_t i = 0; i < d.size(); ++i) {
+    const double r = h[2 * i + 1] > 0 ? std::sqrt(h[2 * i] / h[2 * i + 1]) : 0.0;
+    sum += r;
+    if (r > 1e-8) ++over;
+    if (r > worst) { worst = r; wi = i; }
+  }
+  const int t = keys[wi].first, s = keys[wi].second;
+  fprintf(stderr, "[symcheck] %s: %zu pairs, mean %.2e, max %.2e (>1e-8: %d) at (%d[%c c%d], %d[%c c%d]) %dx%d\n",
+          where, d.size(), sum / d.size(), worst, over, t, "xzy"[g.kind[t]], g.owner[t], s,
+          "xzy"[g.kind[s]], g.owner[s], d[wi].r, d[wi].c);
+  C.free(out);
+  C.flush();
+}
+static int symcheck_every() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("IFMM_SYMCHECK"); v = e ? atoi(e) : 0; }
+  return v;
+}
+
 // IFMM_TRACE=<file>: per-pair decision trace (debug / parity triage)
 // IFMM_PROFILE=1: stream-synchronised phase timers (diagnostics; perturbs
 // overlap, never used for reported numbers)
@@ -1242,14 +1310,31 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     size_t tot = 0;
     std::vector<size_t> uo(ns), so(ns), vo(ns), wo(ns);
     double sflops = 0;
+    // Transposition-consistent exact SVDs.  For a symmetric kernel the fill
+    // pair is F(b, a) = F(a, b)^T up to rounding, and the reference's LAPACK
+    // SVD treats M and M^T through the same factorisation, so the singular
+    // vectors of both fills agree and the U- and V-side basis unions get the
+    // same input (the graph stays symmetric).  A QRCP + Jacobi SVD of M and
+    // of M^T is not transposition-consistent (vectors of close singular
+    // values rotate), and the full-pivot ACA of the unions is not rotation
+    // invariant: so the fill whose cluster pair is (hi, lo) is factorised as
+    // its transpose and U / V are swapped back.  rSVD fills keep their
+    // orientation (their sketch is drawn for the fill as given, lowrank.py:108).
+    std::vector<char> tr(ns, 0);
+    for (int i = 0; i < ns; ++i) {
+      const Stash& s = items[i].second;
+      const bool rs = std::min(s.h, s.w) > 64 && !exact_fill;
+      tr[i] = (!rs && items[i].first.first > items[i].first.second) ? 1 : 0;
+    }
     for (int i = 0; i < ns; ++i) {
       const Stash& s = items[i].second;
       const int mn = std::min(s.h, s.w);
-      uo[i] = tot; tot += (size_t)s.h * mn;
+      uo[i] = tot; tot += (size_t)(tr[i] ? s.w : s.h) * mn;
       so[i] = tot; tot += mn;
-      vo[i] = tot; tot += (size_t)s.w * mn;
+      vo[i] = tot; tot += (size_t)(tr[i] ? s.h : s.w) * mn;
       wo[i] = tot;
-      if (svd_work_doubles(s.h, s.w) > smem_d) tot += svd_work_doubles(s.h, s.w);
+      const int dm = tr[i] ? s.w : s.h, dn = tr[i] ? s.h : s.w;  // the descriptor's orientation
+      if (svd_work_doubles(dm, dn) > smem_d) tot += svd_work_doubles(dm, dn);
       const double mm = std::max(s.h, s.w), nn = mn;
       sflops += 4 * mm * nn * nn + 22 * nn * nn * nn;
     }
@@ -1261,7 +1346,8 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
       const Stash& s = items[i].second;
       const W& w = ws[s.wi];
       sd[i].src = w.Fm.p + (size_t)s.ro * w.NC + s.co;
-      sd[i].m = s.h; sd[i].n = s.w; sd[i].s_r = w.NC; sd[i].s_c = 1;
+      if (tr[i]) { sd[i].m = s.w; sd[i].n = s.h; sd[i].s_r = 1; sd[i].s_c = w.NC; }
+      else { sd[i].m = s.h; sd[i].n = s.w; sd[i].s_r = w.NC; sd[i].s_c = 1; }
       sd[i].U = wsb.p + uo[i]; sd[i].S = wsb.p + so[i]; sd[i].V = wsb.p + vo[i];
       sd[i].rank = dr + i;
       sd[i].work = wsb.p + wo[i];
@@ -1305,8 +1391,14 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
     }
     const int* hr = C.readback_ints(dr, ns);
     for (int i = 0; i < ns; ++i) {
-      fac[i].U = sd[i].U; fac[i].S = sd[i].S; fac[i].V = sd[i].V;
-      fac[i].m = sd[i].m; fac[i].n = sd[i].n; fac[i].rank = hr[i];
+      if (tr[i]) {  // factors of F^T: F = (U S V^T)^T = V S U^T
+        fac[i].U = sd[i].V; fac[i].S = sd[i].S; fac[i].V = sd[i].U;
+        fac[i].m = sd[i].n; fac[i].n = sd[i].m;
+      } else {
+        fac[i].U = sd[i].U; fac[i].S = sd[i].S; fac[i].V = sd[i].V;
+        fac[i].m = sd[i].m; fac[i].n = sd[i].n;
+      }
+      fac[i].rank = hr[i];
     }
   }
   // ---- pairs of every cluster (cluster-disjoint across the wave) ----
@@ -1652,12 +1744,22 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags, NormalSource 
       LevelStats st;
       st.level = l;
       const double lr0 = C.bc.acc[2];
-      for (auto& wv : cluster_waves(T, l, morton)) el.eliminate_wave(wv, st);
+      int nwave = 0;
+      for (auto& wv : cluster_waves(T, l, morton)) {
+        el.eliminate_wave(wv, st);
+        if (symcheck_every() > 0 && ++nwave % symcheck_every() == 0) {
+          char w[64];
+          snprintf(w, sizeof w, "level %d after %d waves (cluster %d)", l, nwave, wv.back());
+          symcheck(C, g, w);
+        }
+      }
       C.check_status("cluster ");
       C.bucket_collect();
       st.compress_time = C.bc.acc[2] - lr0;
       F->levels.push_back(st);
+      if (symcheck_every() > 0) symcheck(C, g, "level end");
       if (l > 2) el.merge(l);
+      if (symcheck_every() > 0 && l > 2) symcheck(C, g, "after merge");
       if (getenv("IFMM_MEMTRACE")) {
         fprintf(stderr, "[ifmm] level %d done: arena in use %.2f GB, peak %.2f GB, %.1f s\n", l,
                 C.arena.in_use() / 1073741824.0, C.arena.peak() / 1073741824.0,

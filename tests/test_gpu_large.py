@@ -1,15 +1,14 @@
-"""BASELINE-size parity (c3: 3D N=262,144 IMQ, eps=1e-6) against the oracle
-run with reference semantics (tests/golden/large/, written by
-tests/golden/make_large_stats.py -- 53 min on one CPU core).
+"""BASELINE-size parity: c3 (3D N=262,144 IMQ, eps=1e-6) against the
+UNMODIFIED reference run on the same seeded inputs (tests/golden/mid/
+c3_imq3d_n262144.npz, make_golden_mid.py: 42 min of CPU).
 
-Gates: tree, H2 ranks (sum), leaf-level fill statistics and peak edges
-exact; relative residual against the EXACT matvec within 2x the
-reference's (north star); x within the reference's own variability.
-
-Why not "x within 10 eps" at this size: the reference's x itself moves by
-9.4e-3 between factorize rng seeds 0 and 1 (rSVD sketches of fills with
-min(shape) > 64, factor.py:329-332), see tests/golden/large/c3_seed1_*.
-Upper-level fill statistics are reported, not gated, for the same reason."""
+Gates: tree (perm checksum, neighbour / interaction counts), H2 ranks and
+the leaf-level fill statistics exact; levels 3 and 2 within 3x the
+reference's own variability (its compressed-pair count moves by 43 at level
+3 between factorize rng seeds, tests/golden/large/c3_seed1_stats.json);
+|x - x_ref| within 2x the reference's seed-to-seed |x| variability (9.4e-3,
+tests/golden/large/c3_seed1_x.npy); relative residual against the EXACT
+matvec within 2x the reference's (north star)."""
 
 import json
 import os
@@ -18,41 +17,49 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN
+from golden_mid import load_mid, mid_inputs
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def test_c3_parity_against_reference_semantics():
+@pytest.mark.parametrize("schedule", ["reference"])
+def test_c3_parity_against_reference(schedule):
     import paper_1508_01835_b200 as P
-    from oracle.ifmm_np import config_inputs  # seeded inputs only
-    st = json.load(open(os.path.join(GOLDEN, "large", "c3_stats.json")))
-    x_ref = np.load(os.path.join(GOLDEN, "large", "c3_x.npy"))
-    inp = config_inputs("c3")
-    tree, _ = P.build_octree(inp["points"], inp["leaf"])
-    assert tree.depth == st["depth"]
+    g = load_mid("c3_imq3d_n262144")
+    pts, b, K = mid_inputs(P, g)
+    eps = float(g["eps"])
+    tree, perm = P.build_octree(pts, int(g["leaf"]))
+    assert tree.depth == int(g["depth"])
+    assert int((np.asarray(perm, dtype=np.int64) * np.arange(1, len(perm) + 1)).sum()) == int(g["perm_checksum"])
     topo = P.compute_topology(tree)
-    ops = P.chebyshev_operators(tree, topo, P.imq_kernel(inp["kernel"][1]["h"]), inp["n"],
-                                epsilon=inp["eps"])
-    assert sum(ops.rank.values()) == st["ranks_sum"]
+    np.testing.assert_array_equal([len(x) for x in topo.neighbors], g["n_neighbors"])
+    np.testing.assert_array_equal([len(x) for x in topo.interactions], g["n_interactions"])
+    ops = P.chebyshev_operators(tree, topo, K, int(g["n"]), epsilon=eps)
+    np.testing.assert_array_equal([ops.rank.get(c, -1) for c in range(tree.n_clusters)], g["ranks"])
     P.initialize_weights(ops, topo)
     graph = P.assemble_extended_graph(ops, consume=True)
-    fct = P.factorize(graph, inp["eps"], seed=0, sigma0=st["sigma0"])
+    fct = P.factorize(graph, eps, seed=0, sigma0=float(g["sigma0"]), schedule=schedule)
     lv = fct.stats.levels
-    leaf = st["levels"][0]
-    assert [lv[0].level, lv[0].compressed_pairs, lv[0].dropped_pairs, lv[0].added,
-            sum(lv[0].ranks)] == leaf[:5]
-    assert fct.stats.peak_edges == st["peak_edges"]
-    x = fct.solve(inp["b"])
-    b = inp["b"]
-    K = P.imq_kernel(inp["kernel"][1]["h"])
-    res = float(np.linalg.norm(P.exact_matvec(inp["points"], K, x) - b) / np.linalg.norm(b))
-    res_ref = float(np.linalg.norm(P.exact_matvec(inp["points"], K, x_ref) - b) / np.linalg.norm(b))
+    assert (lv[0].level, lv[0].compressed_pairs, lv[0].dropped_pairs, lv[0].added, sum(lv[0].ranks)) == \
+        (int(g["lv_level"][0]), int(g["lv_compressed"][0]), int(g["lv_dropped"][0]),
+         int(g["lv_added"][0]), int(g["lv_ranksum"][0]))
+    assert fct.stats.peak_edges == int(g["peak_edges"])
+    seed1 = json.load(open(os.path.join(GOLDEN, "large", "c3_seed1_stats.json")))
+    s0 = json.load(open(os.path.join(GOLDEN, "large", "c3_stats.json")))
+    for i in (1, 2):
+        spread = abs(seed1["levels"][i][1] - s0["levels"][i][1])
+        assert abs(lv[i].compressed_pairs - int(g["lv_compressed"][i])) <= 3 * max(spread, 10), \
+            (lv[i].level, lv[i].compressed_pairs, int(g["lv_compressed"][i]), spread)
+    x = fct.solve(b)
     x_s1 = np.load(os.path.join(GOLDEN, "large", "c3_seed1_x.npy"))
-    var_ref = float(np.linalg.norm(x_s1 - x_ref) / np.linalg.norm(x_ref))
-    rel = float(np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref))
-    print(f"c3 |x - x_ref|/|x_ref| = {rel:.3e} (reference seed0 vs seed1: {var_ref:.3e}); "
+    var_ref = float(np.linalg.norm(x_s1 - g["x"]) / np.linalg.norm(g["x"]))
+    rel = float(np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]))
+    nb = np.linalg.norm(b)
+    res = float(np.linalg.norm(P.exact_matvec(pts, K, x) - b) / nb)
+    res_ref = float(np.linalg.norm(P.exact_matvec(pts, K, g["x"]) - b) / nb)
+    print(f"c3 {schedule}: |x - x_ref|/|x_ref| = {rel:.3e} (reference seed0 vs seed1: {var_ref:.3e}); "
           f"exact residual ours {res:.4e} ref {res_ref:.4e}; levels ours "
           f"{[(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in lv]} "
-          f"ref {[tuple(v[:3]) + (v[4],) for v in st['levels']]}")
+          f"ref {g['lv_compressed'].tolist()} / {g['lv_ranksum'].tolist()}")
     assert res <= 2.0 * res_ref, (res, res_ref)
-    assert rel <= 5.0 * var_ref, (rel, var_ref)
+    assert rel <= 2.0 * var_ref, (rel, var_ref)

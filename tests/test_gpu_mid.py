@@ -2,13 +2,16 @@
 make_golden_mid.py): fill compression at merged (non-leaf) 3D levels and the
 full c2 configuration.
 
-schedule="reference" (Morton cluster order, the reference's PCG64 sketch
-stream): on the 3D cases every per-level statistic is exact and
-|x - x_ref| <= 10 eps.  c2 (eps = 1e-10) has decisions that the reference
-itself flips between rng seeds (tests/golden/mid_seed1/: 192 of 16,314 pair
-decisions and |x_seed0 - x_seed1| = 1.8e-5); there the gate is the
-reference's own variability: statistics within its seed spread and
-|x - x_ref| <= 2 x |x_seed0 - x_seed1|."""
+Both schedules: on the 3D cases every per-level statistic is exact and
+|x - x_ref| <= 10 eps.  c2 (eps = 1e-10): every statistic exact; x is
+within 2e-6 of the reference's (10 eps = 1e-9 is below the rounding
+amplification of this problem -- the reference's own x moves by 1.8e-5
+between factorize rng seeds, tests/golden/mid_seed1/).  The slab (the c3
+recipe on [0,1]^2 x [0,1/4]: leaf-level AND merged-level compression at 1/4
+of c3's size) is exact at the leaf level; above it the reference itself is
+chaotic -- rerun with 4 BLAS threads it changes 428 decisions and its x by
+188 % (tests/golden/mid_seed1/imq_slab_n65536_blas4.npz) -- so only the leaf
+level and the structure are gated there."""
 
 import os
 
@@ -62,20 +65,28 @@ def test_mid_3d_exact(name, schedule):
 
 
 @pytest.mark.parametrize("schedule", ["reference", "wavefront"])
-def test_c2_full_within_reference_variability(schedule):
+def test_c2_full_exact_statistics(schedule):
     g, fct, x = _run("c2_exp2d_n65536", schedule)
+    st = fct.stats
+    np.testing.assert_array_equal([s.compressed_pairs for s in st.levels], g["lv_compressed"])
+    np.testing.assert_array_equal([s.dropped_pairs for s in st.levels], g["lv_dropped"])
+    np.testing.assert_array_equal([sum(s.ranks) for s in st.levels], g["lv_ranksum"])
+    assert st.peak_edges == int(g["peak_edges"])
     s1 = dict(np.load(os.path.join(os.path.dirname(MID), "mid_seed1", "c2_exp2d_n65536.npz")))
     var = np.linalg.norm(s1["x"] - g["x"]) / np.linalg.norm(g["x"])
     rel = np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"])
     print(f"c2 {schedule}: |x - x_ref| = {rel:.3e}; reference seed0 vs seed1 {var:.3e}")
-    assert rel <= 2.0 * var, (rel, var)
+    assert rel <= 2e-6, (rel, var)
+
+
+@pytest.mark.parametrize("schedule", ["reference", "wavefront"])
+def test_slab_leaf_level_exact(schedule):
+    g, fct, x = _run("imq_slab_n65536", schedule)
     st = fct.stats
-    # leaf level: exact; merged levels: within the reference's seed spread
-    assert st.levels[0].compressed_pairs == int(g["lv_compressed"][0])
-    assert sum(st.levels[0].ranks) == int(g["lv_ranksum"][0])
-    for i in range(1, len(st.levels)):
-        spread = abs(int(s1["lv_compressed"][i]) - int(g["lv_compressed"][i]))
-        assert abs(st.levels[i].compressed_pairs - int(g["lv_compressed"][i])) <= 4 * max(spread, 1)
-        rspread = abs(int(s1["lv_ranksum"][i]) - int(g["lv_ranksum"][i]))
-        assert abs(sum(st.levels[i].ranks) - int(g["lv_ranksum"][i])) <= 4 * max(rspread, 1)
+    lv = st.levels[0]
+    assert lv.level == int(g["lv_level"][0])
+    assert (lv.compressed_pairs, lv.dropped_pairs, lv.added, sum(lv.ranks)) == \
+        (int(g["lv_compressed"][0]), int(g["lv_dropped"][0]), int(g["lv_added"][0]),
+         int(g["lv_ranksum"][0]))
+    assert [s.added for s in st.levels] == g["lv_added"].tolist()
     assert st.peak_edges == int(g["peak_edges"])
