@@ -864,9 +864,14 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
   const int smax = std::min(m, k_old + k_f);
   const bool fits = union_fits_smem(m, k_old, k_f);
   d[0].giant = (!fits && smax > giant_union_threshold()) ? 1 : 0;
+  int rg = 0, rer = 0, rec = 0;
+  const char* ar = getenv("IFMM_ACA_REG");
+  const bool reg = !d[0].giant && (!ar || atoi(ar)) && union_aca_reg_class(m, k_old + k_f, &rg, &rer, &rec);
+  if (reg) d[0].giant = 2;
   UnionDesc* dd = C.stage.push_vec(C, d);
   Blk fl = C.alloc(1, union_giant_scratch_doubles(1));
-  launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant ? dd : nullptr, d[0].giant,
+  if (reg) launch_union_aca_reg(dd, 1, thr, rg, rer, rec, C.st);
+  launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant == 1 ? dd : nullptr, d[0].giant == 1,
                smax, fl.p, m, k_old + k_f);
   C.free(fl);
   CUDA_CHECK(cudaGetLastError());

@@ -1144,13 +1144,26 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     int steps = 0;
     unsigned long long t0 = clock64();
     bool giant_hh = false;
-    if (d.giant) {
+    if (d.giant == 1) {
       // the ACA (union_aca_coop) and CholeskyQR (union_cholqr_coop) ran on
       // several CTAs; only a Householder fallback (hdr[1]) or s = 0 is left here
       const int* hg = (const int*)(Dp + 4 * (size_t)smax);
       steps = hg[0];
       if (steps > 0 && hg[1] == 0) continue;  // uniform per CTA
       giant_hh = steps > 0;
+    } else if (d.giant == 2) {
+      // the register-resident ACA (union_aca_reg, union_aca.cu) ran: X, Y and
+      // the pivots sit in the global workspace (same offsets as Acol / Bt / Dp
+      // of the global variant); the shared-memory variant copies them in
+      double* gA = d.work + mreg;
+      double* gB = gA + (size_t)m * smax;
+      double* gD = gB + 2 * (size_t)C * smax + 2 * (size_t)smax * smax;
+      steps = *(const int*)(gD + 4 * (size_t)smax);
+      if (SM) {
+        for (int e = threadIdx.x; e < m * steps; e += blockDim.x) Acol[e] = gA[e];
+        for (int e = threadIdx.x; e < C * steps; e += blockDim.x) Bt[e] = gB[e];
+        for (int e = threadIdx.x; e < steps; e += blockDim.x) Dp[e] = gD[e];
+      }
     } else {
       // concat [B*diag(w) | F*diag(wf)] (col-major m x C) + first local argmax.
       // Thread layout: R threads cover the rows (coalesced), G = nthreads / R
@@ -1309,7 +1322,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
     // ---- scale X columns by 1/pivot: L~ = X D^{-1} ----
     // thread per row, 8 columns per batch with all loads before the stores
     // (giant unions: already scaled by union_cholqr_coop)
-    if (!d.giant)
+    if (d.giant != 1)
     for (int i = threadIdx.x; i < m; i += blockDim.x)
       for (int t0 = 0; t0 < s; t0 += 8) {
         double v[8];
@@ -1523,14 +1536,14 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     int* order = (int*)(gW + 2 * (size_t)smax * smax + 2 * (size_t)smax);  // tauB slot
     if (s == 0) continue;  // rank 0 already written by the first half
     unsigned long long t3 = clock64();
-    double* Wc = (!d.giant && (size_t)s * s <= (size_t)smem_doubles) ? smem : gW;
-    double* Vc = (!d.giant && 2 * (size_t)s * s <= (size_t)smem_doubles) ? smem + (size_t)s * s
+    double* Wc = (d.giant != 1 && (size_t)s * s <= (size_t)smem_doubles) ? smem : gW;
+    double* Vc = (d.giant != 1 && 2 * (size_t)s * s <= (size_t)smem_doubles) ? smem + (size_t)s * s
                                                                           : gW + (size_t)s * s;
     if (Wc != gW)
       for (int e = threadIdx.x; e < s * s; e += blockDim.x) Wc[e] = gW[e];
     __syncthreads();
     // giant unions: the multi-CTA Jacobi (union_jacobi_coop) already ran
-    const int nsw = d.giant ? 0 : cta_jacobi_wv(Wc, Vc, s);
+    const int nsw = d.giant == 1 ? 0 : cta_jacobi_wv(Wc, Vc, s);
     unsigned long long t35 = clock64();
     cta_sv_order(Wc, s, s, s, sig, order);
     unsigned long long t4 = clock64();
@@ -1539,7 +1552,7 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
     const int mr = d.min_rank < s ? d.min_rank : s;
     const int k = kk > mr ? kk : mr;
     // output products (giant unions: union_output_kernel on several CTAs)
-    if (!d.giant) union_output(d, s, k, gQA, gQB, Wc, Vc, order, 0, blockDim.x);
+    if (d.giant != 1) union_output(d, s, k, gQA, gQB, Wc, Vc, order, 0, blockDim.x);
     for (int a = threadIdx.x; a < k; a += blockDim.x) d.NW[a] = sig[order[a]];
     if (threadIdx.x == 0) *d.rank = k;
     __syncthreads();

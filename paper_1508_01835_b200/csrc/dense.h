@@ -68,7 +68,7 @@ struct UnionDesc {
   double* FM;
   int* rank;
   double* work;
-  int giant;  // set by the launcher: core SVD by the multi-CTA Jacobi
+  int giant;  // set by the launcher: 1 = multi-CTA giant path, 2 = register ACA ran
 };
 
 __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f);
@@ -105,6 +105,13 @@ constexpr int kMaxGiantsPerLaunch = 96;
 // s_max above which a global-workspace union is "giant" (multi-CTA ACA,
 // CholeskyQR, core SVD and output); IFMM_GIANT overrides (diagnostics)
 int giant_union_threshold();
+// Register-resident ACA (union_aca.cu) for the unions whose desc has giant ==
+// 2 (union_kernel then starts at the CholeskyQR).  union_aca_reg_class picks
+// the register tile (G CTAs per cluster, ER rows per warp slot, EC column
+// slots per lane) for the batch's largest m / C; false: keep the legacy ACA.
+bool union_aca_reg_class(int max_m, int max_C, int* G, int* ER, int* EC);
+void launch_union_aca_reg(const UnionDesc* d_descs, int n, double thr, int G, int ER, int EC,
+                          cudaStream_t s);
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to

@@ -450,6 +450,29 @@ struct Eliminator {
       ug.push_back(u);
       if (2 * sm * sm <= 28500) jsd = std::max(jsd, 2 * sm * sm);
     }
+    // register-resident ACA (union_aca.cu) for every non-giant union whose
+    // residual fits a register tile; IFMM_ACA_REG=0 keeps the legacy ACA
+    static int aca_reg = -1;
+    if (aca_reg < 0) {
+      const char* e = getenv("IFMM_ACA_REG");
+      aca_reg = e ? atoi(e) : 1;
+    }
+    int rs_g = 0, rs_er = 0, rs_ec = 0, rg_g = 0, rg_er = 0, rg_ec = 0;
+    bool reg_s = false, reg_g = false;
+    if (aca_reg) {
+      int mm = 0, mc = 0;
+      for (auto& u : us) { mm = std::max(mm, u.m); mc = std::max(mc, u.k_old + u.k_f); }
+      reg_s = !us.empty() && union_aca_reg_class(mm, mc, &rs_g, &rs_er, &rs_ec);
+      if (reg_s)
+        for (auto& u : us) u.giant = 2;
+      mm = 0; mc = 0;
+      for (auto& u : ug)
+        if (!u.giant) { mm = std::max(mm, u.m); mc = std::max(mc, u.k_old + u.k_f); }
+      reg_g = mm > 0 && union_aca_reg_class(mm, mc, &rg_g, &rg_er, &rg_ec);
+      if (reg_g)
+        for (auto& u : ug)
+          if (!u.giant) u.giant = 2;
+    }
     UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
     UnionDesc* dgi = giants.empty() ? nullptr : C.stage.push_vec(C, giants);
@@ -465,14 +488,18 @@ struct Eliminator {
     if (ulog) CUDA_CHECK(cudaStreamSynchronize(C.st));
     auto tl1 = std::chrono::steady_clock::now();
     C.kt_begin(K_UNION, uflops, &ka);
+    auto run_s = [&](cudaStream_t s) {
+      if (reg_s) launch_union_aca_reg(dus, (int)us.size(), thr, rs_g, rs_er, rs_ec, s);
+      launch_union(dus, (int)us.size(), thr, s, 1);
+    };
+    auto run_g = [&](cudaStream_t s, int reserved) {
+      if (reg_g) launch_union_aca_reg(dug, (int)ug.size(), thr, rg_g, rg_er, rg_ec, s);
+      launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc, reserved);
+    };
     if (dus && dug)
-      C.fork2([&](cudaStream_t s) { launch_union(dus, (int)us.size(), thr, s, 1); },
-              [&](cudaStream_t s) {
-                launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc,
-                             (int)us.size());
-              });
-    else if (dus) launch_union(dus, (int)us.size(), thr, C.st, 1);
-    else launch_union(dug, (int)ug.size(), thr, C.st, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc);
+      C.fork2([&](cudaStream_t s) { run_s(s); }, [&](cudaStream_t s) { run_g(s, (int)us.size()); });
+    else if (dus) run_s(C.st);
+    else run_g(C.st, 0);
     C.kt_end(K_UNION, uflops, ka);
     C.launches += (!us.empty()) + (!ug.empty());
     CUDA_CHECK(cudaGetLastError());
