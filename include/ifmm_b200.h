@@ -214,6 +214,8 @@ int ifmm_ktime(void* ctx, int enable, double* time_s, double* work, long long* c
  * [16..24] the first nine for 256 < m <= 600, [25..33] for m > 600);
  * reset != 0 clears. */
 int ifmm_union_profile(unsigned long long* out, int reset);
+/* diagnostics: 16 phase counters of union_post_kernel (union_post.cu) */
+int ifmm_union_post_profile(unsigned long long* out, int reset);
 /* Dense kernel matrix out (m x n row-major) = K(|P_i - Q_j|) evaluated on
  * the device (dense.py:23-32, dense_matrix).  P (m x 3), Q (n x 3).       */
 int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const double* P, int n,

@@ -76,6 +76,7 @@ _SIGS = {
     "ifmm_ctx_launches": (C.c_longlong, [vp]),
     "ifmm_ktime": (C.c_int, [vp, C.c_int, dp, dp, lp, C.c_int]),
     "ifmm_union_profile": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
+    "ifmm_union_post_profile": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     "ifmm_krylov_mgs": (C.c_int, [vp, vp, C.c_longlong, C.c_int, C.c_longlong, vp, vp]),
     "ifmm_krylov_div": (C.c_int, [vp, vp, C.c_longlong, C.c_double, vp]),
     "ifmm_krylov_combine": (C.c_int, [vp, vp, C.c_longlong, C.c_int, vp, C.c_longlong, vp]),

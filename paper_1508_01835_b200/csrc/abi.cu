@@ -609,6 +609,11 @@ int ifmm_union_profile(unsigned long long* out, int reset) {
   return 0;
 }
 
+int ifmm_union_post_profile(unsigned long long* out, int reset) {
+  ifmm::union_post_profile(out, reset);
+  return 0;
+}
+
 int ifmm_profile(double* out, int n) {
   for (int i = 0; i < n && i < 12; ++i) out[i] = ifmm::g_prof[i];
   return 0;
@@ -867,15 +872,31 @@ int ifmm_dev_union(void* ctx, int m, int k_old, int k_f, const double* B, const 
   int rg = 0, rer = 0, rec = 0;
   const char* ar = getenv("IFMM_ACA_REG");
   const bool reg = !d[0].giant && (!ar || atoi(ar)) && union_aca_reg_class(m, k_old + k_f, &rg, &rer, &rec);
-  if (reg) d[0].giant = 2;
+  const char* up = getenv("IFMM_UNION_POST");
+  const bool post = reg && (!up || atoi(up)) && union_post_eligible(m, k_old, k_f);
+  if (reg) d[0].giant = post ? 3 : 2;
   UnionDesc* dd = C.stage.push_vec(C, d);
   Blk fl = C.alloc(1, union_giant_scratch_doubles(1));
   if (reg) launch_union_aca_reg(dd, 1, thr, rg, rer, rec, C.st);
-  launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant == 1 ? dd : nullptr, d[0].giant == 1,
-               smax, fl.p, m, k_old + k_f);
-  C.free(fl);
+  if (post) launch_union_post(dd, 1, thr, C.st);
+  else
+    launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant == 1 ? dd : nullptr, d[0].giant == 1,
+                 smax, fl.p, m, k_old + k_f);
   CUDA_CHECK(cudaGetLastError());
   C.sync();
+  if (post) {  // declined (rank -1): the legacy path, as the engine does
+    int hr = 0;
+    CUDA_CHECK(cudaMemcpy(&hr, rank, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hr < 0) {
+      d[0].giant = (!fits && smax > giant_union_threshold()) ? 1 : 0;
+      dd = C.stage.push_vec(C, d);
+      launch_union(dd, 1, thr, C.st, fits ? 1 : 0, 0, d[0].giant == 1 ? dd : nullptr, d[0].giant == 1,
+                   smax, fl.p, m, k_old + k_f);
+      CUDA_CHECK(cudaGetLastError());
+      C.sync();
+    }
+  }
+  C.free(fl);
   C.free(wk);
   C.flush();
   return 0;

@@ -1106,6 +1106,7 @@ union_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int smem_do
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const UnionDesc d = descs[bb];
+    if (d.giant == 3) continue;  // union_post_kernel's (uniform per CTA)
     const int m = d.m, ko = d.k_old, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
     const int spx = smax + (smax & 1);
@@ -1524,6 +1525,7 @@ union_svd_kernel(const UnionDesc* __restrict__ descs, int n, double thr, int sme
   extern __shared__ double smem[];
   for (int bb = blockIdx.x; bb < n; bb += gridDim.x) {
     const UnionDesc d = descs[bb];
+    if (d.giant == 3) continue;  // union_post_kernel's
     const int m = d.m, C = d.k_old + d.k_f;
     const int smax = m < C ? m : C;
     const int spx = smax + (smax & 1);

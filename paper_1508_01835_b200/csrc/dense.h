@@ -68,7 +68,7 @@ struct UnionDesc {
   double* FM;
   int* rank;
   double* work;
-  int giant;  // set by the launcher: 1 = multi-CTA giant path, 2 = register ACA ran
+  int giant;  // set by the launcher: 1 = multi-CTA giant path, 2 = register ACA ran, 3 = register ACA + union_post
 };
 
 __host__ __device__ size_t union_work_doubles(int m, int k_old, int k_f);
@@ -112,6 +112,13 @@ int giant_union_threshold();
 bool union_aca_reg_class(int max_m, int max_C, int* G, int* ER, int* EC);
 void launch_union_aca_reg(const UnionDesc* d_descs, int n, double thr, int G, int ER, int EC,
                           cudaStream_t s);
+// Fused second half (union_post.cu) for the register-ACA unions with
+// min(m, C) <= 96 (desc.giant == 3): CholeskyQR2 + core Jacobi + outputs, one
+// CTA per union, everything on chip.  A union it cannot take gets rank -1
+// (the host reruns it on the legacy path with giant = 0).
+bool union_post_eligible(int m, int k_old, int k_f);
+void launch_union_post(const UnionDesc* d_descs, int n, double thr, cudaStream_t s);
+void union_post_profile(unsigned long long* out, int reset);
 
 // LU with partial pivoting (getrf semantics) of row-major n x n matrices,
 // in place; piv is 0-based (row j swapped with piv[j]).  status[0] is set to

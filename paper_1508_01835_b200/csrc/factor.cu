@@ -457,21 +457,38 @@ struct Eliminator {
       const char* e = getenv("IFMM_ACA_REG");
       aca_reg = e ? atoi(e) : 1;
     }
+    // fused second half (union_post.cu) for the register-ACA unions it can
+    // take (giant = 3); IFMM_UNION_POST=0 keeps union_kernel / union_svd_kernel
+    static int use_post = -1;
+    if (use_post < 0) {
+      const char* e = getenv("IFMM_UNION_POST");
+      use_post = e ? atoi(e) : 1;
+    }
     int rs_g = 0, rs_er = 0, rs_ec = 0, rg_g = 0, rg_er = 0, rg_ec = 0;
     bool reg_s = false, reg_g = false;
-    if (aca_reg) {
+    bool post_s = false, post_g = false, legacy_s = !us.empty(), legacy_g = !ug.empty();
+    if (aca_reg && !legacy_only) {
       int mm = 0, mc = 0;
       for (auto& u : us) { mm = std::max(mm, u.m); mc = std::max(mc, u.k_old + u.k_f); }
       reg_s = !us.empty() && union_aca_reg_class(mm, mc, &rs_g, &rs_er, &rs_ec);
-      if (reg_s)
-        for (auto& u : us) u.giant = 2;
+      if (reg_s) {
+        legacy_s = false;
+        for (auto& u : us) {
+          u.giant = (use_post && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
+          (u.giant == 3 ? post_s : legacy_s) = true;
+        }
+      }
       mm = 0; mc = 0;
       for (auto& u : ug)
         if (!u.giant) { mm = std::max(mm, u.m); mc = std::max(mc, u.k_old + u.k_f); }
       reg_g = mm > 0 && union_aca_reg_class(mm, mc, &rg_g, &rg_er, &rg_ec);
-      if (reg_g)
-        for (auto& u : ug)
-          if (!u.giant) u.giant = 2;
+      if (reg_g) {
+        legacy_g = false;
+        for (auto& u : ug) {
+          if (!u.giant) u.giant = (use_post && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
+          (u.giant == 3 ? post_g : legacy_g) = true;
+        }
+      }
     }
     UnionDesc* dus = us.empty() ? nullptr : C.stage.push_vec(C, us);
     UnionDesc* dug = ug.empty() ? nullptr : C.stage.push_vec(C, ug);
@@ -490,11 +507,14 @@ struct Eliminator {
     C.kt_begin(K_UNION, uflops, &ka);
     auto run_s = [&](cudaStream_t s) {
       if (reg_s) launch_union_aca_reg(dus, (int)us.size(), thr, rs_g, rs_er, rs_ec, s);
-      launch_union(dus, (int)us.size(), thr, s, 1);
+      if (post_s) launch_union_post(dus, (int)us.size(), thr, s);
+      if (legacy_s) launch_union(dus, (int)us.size(), thr, s, 1);
     };
     auto run_g = [&](cudaStream_t s, int reserved) {
       if (reg_g) launch_union_aca_reg(dug, (int)ug.size(), thr, rg_g, rg_er, rg_ec, s);
-      launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc, reserved);
+      if (post_g) launch_union_post(dug, (int)ug.size(), thr, s);
+      if (legacy_g)
+        launch_union(dug, (int)ug.size(), thr, s, 0, jsd, dgi, ngi, max_gs, dfl, max_gm, max_gc, reserved);
     };
     if (dus && dug)
       C.fork2([&](cudaStream_t s) { run_s(s); }, [&](cudaStream_t s) { run_g(s, (int)us.size()); });
@@ -517,7 +537,9 @@ struct Eliminator {
     FILE* ulog = union_log();
     const auto tl0 = fl.tl0, tl1 = fl.tl1;
     const size_t nus = fl.ns, nug = fl.ng;
-    const int* hr = C.readback_ints(fl.dr, reqs.size());
+    const int* hr0 = C.readback_ints(fl.dr, reqs.size());
+    std::vector<int> hrv(hr0, hr0 + reqs.size());
+    const int* hr = hrv.data();
     if (ulog) {
       auto tl2 = std::chrono::steady_clock::now();
       int mm = 0, mc = 0, mk = 0;
@@ -533,12 +555,23 @@ struct Eliminator {
               std::chrono::duration<double, std::milli>(tl0 - prev).count());
       prev = tl2;
     }
+    std::vector<UReq> redo;
     for (size_t i = 0; i < reqs.size(); ++i) {
       reqs[i].bu->rank = hr[i];
       C.free(reqs[i].bu->W);
+      if (hr[i] < 0) redo.push_back(reqs[i]);  // union_post_kernel declined it
     }
     if (fl.giants) C.free(fl.gflags);
+    if (!redo.empty()) {
+      post_fallbacks += redo.size();
+      const bool was = legacy_only;
+      legacy_only = true;
+      launch_unions(redo);
+      legacy_only = was;
+    }
   }
+  bool legacy_only = false;  // reruns of unions the fused second half declined
+  unsigned long long post_fallbacks = 0;
 
   void make_identity(BU& b, int m, int k, const Blk& w) {
     b.identity = true;

@@ -86,7 +86,7 @@ union_aca_reg(const UnionDesc* __restrict__ descs, int n, double thr) {
   if (u >= n) return;  // whole clusters only (grid = n G)
   const int g = G > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const UnionDesc d = descs[u];
-  if (d.giant != 2) return;  // uniform per cluster: giants / legacy-ACA unions
+  if (d.giant < 2) return;  // uniform per cluster: giants / legacy-ACA unions
   const int m = d.m, ko = d.k_old, C = ko + d.k_f;
   const int smax = m < C ? m : C;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -190,3 +190,46 @@ def test_union_giant_matches_oracle(N):
     fm = FM.cpu().numpy()[:r * kf].reshape(r, kf)
     np.testing.assert_allclose(nb @ om, ref.basis @ ref.old_map, atol=1e-9)
     np.testing.assert_allclose(nb @ fm, ref.basis @ ref.fill_map, atol=1e-9)
+
+
+@pytest.mark.parametrize("m,ko,kf,decay", [(12, 5, 3, 3), (64, 20, 6, 6), (97, 41, 9, 7),
+                                           (120, 30, 8, 9), (230, 45, 10, 9), (255, 64, 17, 8),
+                                           (530, 80, 12, 9), (700, 70, 26, 5), (60, 70, 20, 6),
+                                           (400, 88, 8, 2), (1000, 60, 30, 12)])
+def test_union_fused_second_half_matches_oracle(N, m, ko, kf, decay):
+    """Register ACA + union_post_kernel (CholeskyQR2 with a first-order second
+    pass, shared-memory Jacobi, DMMA outputs) against the oracle union: same
+    rank, weights to 1e-10, the same represented operators, orthonormal basis."""
+    import ctypes as C
+    from oracle import ifmm_np as O
+    rng = np.random.default_rng(m + 7 * ko)
+    B, _ = np.linalg.qr(rng.standard_normal((m, min(ko, m))))
+    ko = B.shape[1]
+    F, _ = np.linalg.qr(rng.standard_normal((m, min(kf, m))))
+    kf = F.shape[1]
+    w = np.sort(10.0 ** (-decay * rng.random(ko)))[::-1]
+    wf = np.sort(10.0 ** (-decay * rng.random(kf)))[::-1] * 0.5
+    thr = 1e-6 * w[0]
+    ref = O.basis_union(B, w, F, wf, thr)
+    cap = min(m, ko + kf)
+    dB, dw, dF, dwf = _dev(B), _dev(w), _dev(F), _dev(wf)
+    NB = torch.zeros(m * cap, dtype=torch.float64, device="cuda")
+    NW = torch.zeros(cap, dtype=torch.float64, device="cuda")
+    OM = torch.zeros(cap * ko, dtype=torch.float64, device="cuda")
+    FM = torch.zeros(cap * kf, dtype=torch.float64, device="cuda")
+    dr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    up = (C.c_ulonglong * 16)()
+    N.lib().ifmm_union_post_profile(up, 1)
+    N.check(N.lib().ifmm_dev_union(N.ctx(), m, ko, kf, _p(dB), _p(dw), _p(dF), _p(dwf), thr, 0,
+                                   _p(NB), _p(NW), _p(OM), _p(FM), _p(dr)))
+    N.lib().ifmm_union_post_profile(up, 0)
+    assert up[6] == 1, "the fused second half did not take this union"
+    r = int(dr.item())
+    assert r == ref.rank
+    nb = NB.cpu().numpy()[:m * r].reshape(r, m).T
+    np.testing.assert_allclose(NW.cpu().numpy()[:r], ref.weights, rtol=1e-10, atol=1e-13 * w[0])
+    np.testing.assert_allclose(nb.T @ nb, np.eye(r), atol=1e-12)
+    om = OM.cpu().numpy()[:r * ko].reshape(r, ko)
+    fm = FM.cpu().numpy()[:r * kf].reshape(r, kf)
+    np.testing.assert_allclose(nb @ om, ref.basis @ ref.old_map, atol=1e-9)
+    np.testing.assert_allclose(nb @ fm, ref.basis @ ref.fill_map, atol=1e-9)

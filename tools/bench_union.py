@@ -48,6 +48,7 @@ for m, ko, kf in sizes:
     up = (C.c_ulonglong * 48)()
     for rep in range(2):
         N.lib().ifmm_union_profile(up, 1)
+        N.lib().ifmm_union_post_profile((C.c_ulonglong * 16)(), 1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         N.check(N.lib().ifmm_dev_union(N.ctx(), m, ko, kf, ptr(dB), ptr(dw), ptr(dF), ptr(dwf), thr, 0,
@@ -60,6 +61,13 @@ for m, ko, kf in sizes:
     print(f"m={m:5d} C={ko + kf:4d} s={s:4d} rank={int(dr.item()):4d} wall {dt * 1e3:8.2f} ms | Mcycles "
           f"aca {u[0] / 1e6:7.2f} cholqr {u[1] / 1e6:7.2f} jacobi {u[3] / 1e6:7.2f} (sweeps {u[11]}) "
           f"out {u[4] / 1e6:6.2f}", flush=True)
+    vp = (C.c_ulonglong * 16)()
+    N.lib().ifmm_union_post_profile(vp, 1)
+    v = list(vp)
+    if v[6]:
+        print(f"   fused second half: s={v[7]} k={v[10]} sweeps {v[9]} pass2 {v[11]} | kcycles gram1 {v[0] / 1e3:.1f} chol+M {v[1] / 1e3:.1f} "
+              f"trsm+gram2+corr {v[2] / 1e3:.1f} jacobi {v[3] / 1e3:.1f} order+Z {v[4] / 1e3:.1f} out {v[5] / 1e3:.1f}"
+              f" | gram1: fetch+store {v[12] / 1e3:.1f} accum {v[13] / 1e3:.1f} reduce {v[14] / 1e3:.1f}; chol only {v[15] / 1e3:.1f}", flush=True)
     if u[39]:
         print(f"   cholqr parts (m>400): scale+gram1+chol1 {u[38] / 1e6:.3f} trsm1 {u[34] / 1e6:.3f} "
               f"gram2 {u[35] / 1e6:.3f} chol2 {u[36] / 1e6:.3f} trsm2+trmul {u[37] / 1e6:.3f}", flush=True)

@@ -42,3 +42,4 @@ print(f"factorize {tf:.1f}s solve {ts:.2f}s unknowns/s {inp['N'] / (tf + ts):.1f
 print({k: (round(v[0], 2), v[2]) for k, v in kt.items() if v[2]})
 print("levels", [(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in f.stats.levels])
 print("flops", f.flops)
+print("phases", {k: round(v, 2) for k, v in NN.profile().items()})

@@ -58,6 +58,24 @@ __global__ void thr(double* out, long long* cyc, int n) {
   double s = 0; for (int k = 0; k < 8; ++k) s += a[k];
   out[threadIdx.x] = s;
 }
+__global__ void dmma_k(double* out, long long* cyc, int n, int chains) {
+  double c[8][2];
+  for (int k = 0; k < 8; ++k) { c[k][0] = threadIdx.x; c[k][1] = k; }
+  double a = 1.0 + threadIdx.x * 1e-6, b = 0.5;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < chains)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  double s = 0; for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+  out[threadIdx.x] = s;
+}
 int main() {
   double* d; long long* c; cudaMalloc(&d, 1 << 20); cudaMalloc(&c, 1024);
   const int n = 1000;
@@ -72,6 +90,14 @@ int main() {
     cudaMemcpy(h, c, 8, cudaMemcpyDeviceToHost);
     printf("throughput threads=%4d: %.2f DFMA/clk/SM\n", t, 8.0 * n * t / h[0]);
   }
+  for (int ch : {1, 2, 4, 8})
+    for (int t : {32, 128, 512}) {
+      dmma_k<<<1, t>>>(d, c, n, ch); cudaDeviceSynchronize();
+      dmma_k<<<1, t>>>(d, c, n, ch);
+      cudaMemcpy(h, c, 8, cudaMemcpyDeviceToHost);
+      printf("dmma chains=%d threads=%4d: %.1f cyc per step (%d dmma/warp/step), %.2f dmma/clk/SM\n", ch, t,
+             (double)h[0] / n, ch, (double)ch * n * (t / 32) / h[0]);
+    }
   lat<<<1, 512>>>(d, c, n, 0.5); cudaDeviceSynchronize();
   cudaMemcpy(h, c, sizeof h, cudaMemcpyDeviceToHost);
   printf("bar latency with 16 warps: %.1f cyc\n", (double)h[7] / n);
