@@ -371,7 +371,7 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None, help="override N (diagnostics)")
     ap.add_argument("--schedule", default=os.environ.get("IFMM_SCHEDULE", "wavefront"),
-                    choices=["wavefront", "reference"],
+                    choices=["wavefront", "reference", "colored"],
                     help="factorize schedule (paper_1508_01835_b200.factor.factorize)")
     ap.add_argument("--consume-from", type=int, default=500000,
                     help="N at/above which graphs consume (move) the operator blocks")

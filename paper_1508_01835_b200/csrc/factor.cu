@@ -316,7 +316,7 @@ struct BU {  // BasisUpdate (lowrank.py:22-51)
 };
 
 struct PairCtx;
-std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact);
+std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact, bool colored = false);
 
 struct Eliminator {
   Ctx& C;
@@ -569,6 +569,32 @@ struct Eliminator {
       launch_unions(redo);
       legacy_only = was;
     }
+  }
+  // A wave's clusters in chunks whose Schur fill matrices (the largest
+  // per-cluster temporaries: NR x NC, plus X) stay within IFMM_WAVE_GB
+  // (default 6) GB, so the big colour waves of the upper levels fit the arena.
+  std::vector<std::vector<int>> split_wave(const std::vector<int>& wave) {
+    static double budget = -1.0;
+    if (budget < 0) {
+      const char* e = getenv("IFMM_WAVE_GB");
+      budget = (e ? atof(e) : 6.0) * 1073741824.0;
+    }
+    std::vector<std::vector<int>> out(1);
+    double acc = 0.0;
+    for (int c : wave) {
+      const int nx = g.nx[c];
+      double R = g.size[g.nz[c]], Cc = R;
+      for (int a : g.cols[nx]) R += g.size[a];
+      for (int b : g.rows[nx]) Cc += g.size[b];
+      const double need = 8.0 * (R * Cc + 2.0 * (g.size[nx] + g.size[g.nz[c]]) * (Cc + g.size[nx]));
+      if (!out.back().empty() && acc + need > budget) {
+        out.emplace_back();
+        acc = 0.0;
+      }
+      out.back().push_back(c);
+      acc += need;
+    }
+    return out;
   }
   bool legacy_only = false;  // reruns of unions the fused second half declined
   unsigned long long post_fallbacks = 0;
@@ -1643,11 +1669,27 @@ void Eliminator::rsvd_fills_ref(std::vector<SvdDesc>& sd, const std::vector<int>
 
 // Waves of clusters of one level: Morton order, a cluster joins the first
 // wave after every earlier cluster within Chebyshev distance 2.
-std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact) {
+//
+// colored: the relaxed order of SURVEY 8e instead -- one wave per colour
+// (x mod 3, y mod 3, z mod 3), colours in lexicographic order, Morton order
+// inside a colour.  Same-colour clusters are at Chebyshev distance >= 3 (no
+// shared neighbour), so a wave is still one batched stage, but the
+// elimination order is no longer the reference's.
+std::vector<std::vector<int>> cluster_waves(const Tree& T, int level, bool exact, bool colored) {
   const auto& ids = T.levels[level];
   std::vector<std::vector<int>> out;
   if (exact) {
     for (int c : ids) out.push_back({c});
+    return out;
+  }
+  if (colored) {
+    std::vector<std::vector<int>> by(27);
+    for (int c : ids) {
+      const long long x = T.cell[3 * c], y = T.cell[3 * c + 1], z = T.cell[3 * c + 2];
+      by[(x % 3) * 9 + (y % 3) * 3 + (z % 3)].push_back(c);
+    }
+    for (auto& v : by)
+      if (!v.empty()) out.push_back(std::move(v));
     return out;
   }
   std::unordered_map<uint64_t, int> wave_at;
@@ -1805,7 +1847,8 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags, NormalSource 
       st.level = l;
       const double lr0 = C.bc.acc[2];
       int nwave = 0;
-      for (auto& wv : cluster_waves(T, l, morton)) {
+      for (auto& wave : cluster_waves(T, l, morton, !morton && (flags & 8) != 0))
+      for (auto& wv : el.split_wave(wave)) {
         el.eliminate_wave(wv, st);
         if (symcheck_every() > 0 && ++nwave % symcheck_every() == 0) {
           char w[64];

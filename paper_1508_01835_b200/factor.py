@@ -229,7 +229,7 @@ class _ReferenceStream:
             return 1
 
 
-SCHEDULES = ("reference", "wavefront")
+SCHEDULES = ("reference", "wavefront", "colored")
 
 
 def pcg64_state(seed):
@@ -256,6 +256,13 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
         sketches come from a counter-based device generator.  Same
         algorithm; results differ from the reference the way the reference's
         own results differ between rng seeds.
+      * ``"colored"`` -- the relaxed order of SURVEY.md 8e: 27 waves per
+        level (9 in 2D), one per colour (x mod 3, y mod 3, z mod 3) of the
+        cluster grid, every cluster of a colour eliminated in one batched
+        stage.  The elimination ORDER differs from the reference's Morton
+        order, so per-level fill statistics and x are not comparable with the
+        reference's; this mode is validated by the residual criterion only
+        (exact-matvec residual <= 2x the reference's, tests/test_gpu_large.py).
     The fill pairs of one elimination always run as waves of cluster-disjoint
     pairs (they commute); ``exact_order=True`` runs them one at a time
     (diagnostics).  Environment defaults: IFMM_SCHEDULE, IFMM_EXACT_ORDER."""
@@ -276,7 +283,7 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
         sigma0 = estimate_sigma0(graph, seed=seed)
         t_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    flags = 1 if exact_order else 0
+    flags = (1 if exact_order else 0) | (8 if schedule == "colored" else 0)
     lib = N.lib()
     if schedule == "reference":
         # the reference's Generator(PCG64(seed)) (factor.py:188), run natively

@@ -24,7 +24,7 @@ def _setup(P, n_points=400, seed=5, d=1e-2, n=2, leaf_target=12, depth=None, eps
     return pts, kern, tree, topo, ops
 
 
-@pytest.mark.parametrize("schedule", ["reference", "wavefront"])
+@pytest.mark.parametrize("schedule", ["reference", "wavefront", "colored"])
 @pytest.mark.parametrize("n_points,leaf_target", [(400, 12), (500, 3)])
 def test_lossless_equals_h2_dense_solve(n_points, leaf_target, schedule):
     """test_factor.py:37-46."""
@@ -64,7 +64,7 @@ def test_zero_rhs_and_linearity():
     assert np.linalg.norm(lhs - rhs) / np.linalg.norm(lhs) < 1e-10
 
 
-@pytest.mark.parametrize("schedule", ["reference", "wavefront"])
+@pytest.mark.parametrize("schedule", ["reference", "wavefront", "colored"])
 def test_refactorization_bitwise_deterministic(schedule):
     """test_factor.py:95-106: an independent factorize with the same seed is
     bitwise identical (here: of a device copy of the graph, and of a freshly

@@ -43,3 +43,8 @@ print({k: (round(v[0], 2), v[2]) for k, v in kt.items() if v[2]})
 print("levels", [(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in f.stats.levels])
 print("flops", f.flops)
 print("phases", {k: round(v, 2) for k, v in NN.profile().items()})
+if os.environ.get("IFMM_DIAG_RESIDUAL"):
+    b = inp["b"]
+    t0 = time.perf_counter()
+    res = np.linalg.norm(P.exact_matvec(inp["pts"], K, x) - b) / np.linalg.norm(b)
+    print(f"schedule {f.schedule} exact-matvec residual {res:.4e} ({time.perf_counter() - t0:.1f}s)")
