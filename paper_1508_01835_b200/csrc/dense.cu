@@ -29,132 +29,6 @@ __device__ __forceinline__ void cta_orgqr(const double* A, int rows, int cols, i
                           double* Q, int ldq);
 
 // ============================================================================
-// Grouped GEMM (DMMA)
-// ============================================================================
-
-namespace {
-constexpr int GT_M = 64, GT_N = 64, GT_K = 16, G_LD = GT_M + 4;
-
-__global__ void __launch_bounds__(128)
-gemm_grouped_kernel(const GemmDesc* __restrict__ descs, const int* __restrict__ tstart,
-                    int nprob, int total) {
-  __shared__ double As[2][GT_K][G_LD];
-  __shared__ double Bs[2][GT_K][G_LD];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
-
-  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    // locate problem: largest p with tstart[p] <= tile
-    int lo = 0, hi = nprob - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (tstart[mid] <= tile) lo = mid; else hi = mid - 1;
-    }
-    const GemmDesc d = descs[lo];
-    const int local = tile - tstart[lo];
-    const int tiles_n = (d.N + GT_N - 1) / GT_N;
-    const int m0 = (local / tiles_n) * GT_M, n0 = (local % tiles_n) * GT_N;
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    double ra[8], rb[8];
-    auto load_tile = [&](int k0) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        int mm, kk;
-        if (d.ta == 0) { kk = tid & 15; mm = (tid >> 4) + 8 * r; }
-        else { mm = tid & 63; kk = (tid >> 6) + 2 * r; }
-        int gm = m0 + mm, gk = k0 + kk;
-        double v = 0.0;
-        if (gm < d.M && gk < d.K) {
-          v = d.ta == 0 ? d.A[(size_t)gm * d.lda + gk] : d.A[(size_t)gk * d.lda + gm];
-          if (d.dscale) v *= d.dscale[gk];
-        }
-        ra[r] = v;
-        int nn, kb;
-        if (d.tb == 0) { nn = tid & 63; kb = (tid >> 6) + 2 * r; }
-        else { kb = tid & 15; nn = (tid >> 4) + 8 * r; }
-        int gn = n0 + nn, gkb = k0 + kb;
-        double w = 0.0;
-        if (gn < d.N && gkb < d.K)
-          w = d.tb == 0 ? d.B[(size_t)gkb * d.ldb + gn] : d.B[(size_t)gn * d.ldb + gkb];
-        rb[r] = w;
-      }
-    };
-    auto store_tile = [&](int buf) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        int mm, kk;
-        if (d.ta == 0) { kk = tid & 15; mm = (tid >> 4) + 8 * r; }
-        else { mm = tid & 63; kk = (tid >> 6) + 2 * r; }
-        As[buf][kk][mm] = ra[r];
-        int nn, kb;
-        if (d.tb == 0) { nn = tid & 63; kb = (tid >> 6) + 2 * r; }
-        else { kb = tid & 15; nn = (tid >> 4) + 8 * r; }
-        Bs[buf][kb][nn] = rb[r];
-      }
-    };
-
-    const int nk = (d.K + GT_K - 1) / GT_K;
-    if (nk > 0) {
-      load_tile(0);
-      store_tile(0);
-    }
-    __syncthreads();
-    for (int kt = 0; kt < nk; ++kt) {
-      const int buf = kt & 1;
-      if (kt + 1 < nk) load_tile((kt + 1) * GT_K);
-#pragma unroll
-      for (int k4 = 0; k4 < GT_K; k4 += 4) {
-        double af[4], bf[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][k4 + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      }
-      if (kt + 1 < nk) store_tile(buf ^ 1);
-      __syncthreads();
-    }
-    // epilogue
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
-      if (gm >= d.M) continue;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int gn = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + e;
-          if (gn >= d.N) continue;
-          double* c = d.C + (size_t)gm * d.ldc + gn;
-          double v = d.alpha * acc[i][j][e];
-          if (d.beta != 0.0) v += d.beta * (*c);
-          *c = v;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-}  // namespace
-
-void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob, int total_tiles,
-                 cudaStream_t s) {
-  DbgSync dbg_sync_{s, "launch_gemm"};
-  if (total_tiles <= 0) return;
-  int grid = total_tiles < 148 * 8 ? total_tiles : 148 * 8;
-  gemm_grouped_kernel<<<grid, 128, 0, s>>>(d_descs, d_tile_start, nprob, total_tiles);
-}
-
-// ============================================================================
 // Strided copy / accumulate
 // ============================================================================
 

@@ -77,8 +77,11 @@ __host__ __device__ size_t svd_work_doubles(int m, int n);
 size_t svd_smem_doubles(int max_smem_dim);
 
 // Host launchers.  `descs` / side arrays must already be device-resident.
+// (gemm.cu) d_tile_start: prefix sums of the problems' output-tile counts for
+// the tile shape gemm_tile_dims(big) reports (128 x 128 or 64 x 64).
+void gemm_tile_dims(int big, int* bm, int* bn);
 void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob,
-                 int total_tiles, cudaStream_t s);
+                 int total_tiles, cudaStream_t s, int big);
 void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s);
 // rel_mode: thr is relative to sigma_max and rank >= 1 (h2.py:124-127).
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim,

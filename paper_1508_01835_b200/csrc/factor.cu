@@ -464,6 +464,12 @@ struct Eliminator {
       const char* e = getenv("IFMM_UNION_POST");
       use_post = e ? atoi(e) : 1;
     }
+    // The fused path resolves the core's singular values to ~1e-13 of its
+    // scale (first-order second CholeskyQR pass); rank decisions at
+    // eps < 1e-8 need more (at c2, eps = 1e-10, it moved 4 of ~20,000
+    // decisions against the reference), so those configurations keep the
+    // two-pass kernels.
+    const bool post_ok = use_post && F.eps >= 1e-8;
     int rs_g = 0, rs_er = 0, rs_ec = 0, rg_g = 0, rg_er = 0, rg_ec = 0;
     bool reg_s = false, reg_g = false;
     bool post_s = false, post_g = false, legacy_s = !us.empty(), legacy_g = !ug.empty();
@@ -474,7 +480,7 @@ struct Eliminator {
       if (reg_s) {
         legacy_s = false;
         for (auto& u : us) {
-          u.giant = (use_post && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
+          u.giant = (post_ok && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
           (u.giant == 3 ? post_s : legacy_s) = true;
         }
       }
@@ -485,7 +491,7 @@ struct Eliminator {
       if (reg_g) {
         legacy_g = false;
         for (auto& u : ug) {
-          if (!u.giant) u.giant = (use_post && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
+          if (!u.giant) u.giant = (post_ok && union_post_eligible(u.m, u.k_old, u.k_f)) ? 3 : 2;
           (u.giant == 3 ? post_g : legacy_g) = true;
         }
       }

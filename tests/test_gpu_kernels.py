@@ -27,7 +27,9 @@ def N():
 
 @pytest.mark.parametrize("M,Nn,K,ta,tb", [(1, 1, 1, 0, 0), (7, 5, 3, 0, 0), (64, 64, 64, 0, 0),
                                           (100, 37, 129, 1, 0), (65, 130, 17, 0, 1),
-                                          (300, 200, 150, 1, 1), (513, 257, 96, 0, 0)])
+                                          (300, 200, 150, 1, 1), (513, 257, 96, 0, 0),
+                                          (1500, 1300, 70, 0, 0), (1301, 1407, 33, 1, 1),
+                                          (1400, 1290, 131, 0, 1), (1290, 1400, 50, 1, 0)])
 def test_gemm(N, M, Nn, K, ta, tb):
     rng = np.random.default_rng(M * 7 + Nn)
     A = rng.standard_normal((K, M) if ta else (M, K))
