@@ -57,6 +57,17 @@ struct H2 {
   void build();
   void weights();
   void matvec(const double* d_x_sorted, double* d_y_sorted);
+  // h2_matvec's block lists are built once per operator state and kept on
+  // the device (h2.cu); weights() / graph consumption drop them
+  struct MatvecPlan {
+    bool valid = false;
+    Blk desc;                  // SpmvRow[] then SpmvTerm[] (raw bytes)
+    size_t n_rows = 0, n_terms = 0;
+    std::vector<std::pair<size_t, int>> launches;  // (first row, rows) per dependent stage
+    Blk xin, yout, yv, zv;     // staged x / y (tree order), multipoles, locals
+    double bytes = 0.0;        // operator bytes one matvec reads
+  } plan;
+  void drop_plan();
   // Morton-range partitioned matvec (one rank's share), see h2.cu
   long long multipole_size() const;
   void matvec_part(const double* d_x_sorted, double* d_y_sorted, double* d_yv, int phase,

@@ -22,6 +22,7 @@ void Graph::build(H2* h, bool consume) {
   ctx = h->ctx;
   Ctx& C = *ctx;
   Tree& T = *tree;
+  if (consume) h->drop_plan();
   nx.assign(T.nc, -1); nz.assign(T.nc, -1); ny.assign(T.nc, -1);
   dead.assign(T.nc, 0);
   su.assign(T.nc, Blk()); sv.assign(T.nc, Blk());

@@ -14,6 +14,7 @@ H2::~H2() {
     for (auto& b : *v) ctx->free(b);
   for (auto& kv : coupling) ctx->free(kv.second);
   for (auto& kv : near) ctx->free(kv.second);
+  drop_plan();
   ctx->sync_nothrow();
   ctx->flush();
 }
@@ -261,6 +262,7 @@ void H2::build() {
 void H2::weights() {
   Ctx& C = *ctx;
   Tree& T = *tree;
+  drop_plan();
   std::vector<int> ids;
   for (int l = 2; l <= T.depth; ++l)
     for (int c : T.levels[l]) ids.push_back(c);
@@ -388,84 +390,121 @@ void H2::weights() {
 // ---------------------------------------------------------------------------
 // h2_matvec (krylov.py:119-159) over tree-sorted vectors
 // ---------------------------------------------------------------------------
+void H2::drop_plan() {
+  if (!plan.valid) return;
+  for (Blk* b : {&plan.desc, &plan.xin, &plan.yout, &plan.yv, &plan.zv}) {
+    ctx->free(*b);
+    *b = Blk();
+  }
+  plan.launches.clear();
+  plan.valid = false;
+}
+
+// The block lists (one SpmvRow per output segment, its SpmvTerms in the
+// reference's summation order) depend only on the operators, so they are
+// built and uploaded once; a matvec is then two vector copies (x in, y out of
+// the plan's staging vectors) and one launch per dependent stage: leaf P2M,
+// M2M per level, M2L + L2L per level, P2P + L2P.
 void H2::matvec(const double* xs, double* ys) {
   Ctx& C = *ctx;
   Tree& T = *tree;
-  // per-cluster multipole / local vectors
-  std::vector<long long> off(T.nc, -1);
-  long long tot = 0;
-  for (int c = 0; c < T.nc; ++c)
-    if (rank[c] > 0 && T.level[c] >= 2) { off[c] = tot; tot += rank[c]; }
-  Blk yv = C.alloc(1, (int)std::max<long long>(tot, 1));
-  Blk zv = C.alloc(1, (int)std::max<long long>(tot, 1));
-  auto run = [&](std::vector<SpmvRow>& rows, std::vector<SpmvTerm>& terms) {
-    if (rows.empty()) return;
-    SpmvTerm* dt = C.stage.push_vec(C, terms);
-    // patch term offsets are already absolute indices into `terms`
-    SpmvRow* dr = C.stage.push_vec(C, rows);
-    launch_spmv(dr, (int)rows.size(), dt, 1, 1, C.st);
-    rows.clear(); terms.clear();
-  };
-  std::vector<SpmvRow> rows;
-  std::vector<SpmvTerm> terms;
-  const bool has_far = T.depth >= 2;
-  if (has_far) {
-    // upward leaf: y = V^T x
+  IFMM_ASSERT(!consumed, "matvec on operators whose blocks moved into a graph");
+  if (!plan.valid) {
+    std::vector<long long> off(T.nc, -1);
+    long long tot = 0;
+    for (int c = 0; c < T.nc; ++c)
+      if (rank[c] > 0 && T.level[c] >= 2) { off[c] = tot; tot += rank[c]; }
+    plan.yv = C.alloc(1, (int)std::max<long long>(tot, 1));
+    plan.zv = C.alloc(1, (int)std::max<long long>(tot, 1));
+    plan.xin = C.alloc(1, std::max(T.n_points, 1));
+    plan.yout = C.alloc(1, std::max(T.n_points, 1));
+    const double* px = plan.xin.p;
+    double* py = plan.yout.p;
+    double* yv = plan.yv.p;
+    double* zv = plan.zv.p;
+    std::vector<SpmvRow> rows;
+    std::vector<SpmvTerm> terms;
+    size_t stage0 = 0;
+    double bytes = 0.0;
+    auto term = [&](const Blk& B, int trans, const double* in) {
+      terms.push_back({B.p, B.r, B.c, B.c, trans, in});
+      bytes += 8.0 * B.r * B.c;
+    };
+    auto stage = [&]() {
+      if (rows.size() > stage0) plan.launches.push_back({stage0, (int)(rows.size() - stage0)});
+      stage0 = rows.size();
+    };
+    const bool has_far = T.depth >= 2;
+    if (has_far) {
+      for (int c : T.leaves()) {  // upward leaf: y = V^T x
+        rows.push_back({yv + off[c], rank[c], (int)terms.size(), 1, 0});
+        term(leaf_v[c], 1, px + T.start[c]);
+      }
+      stage();
+      for (int l = T.depth - 1; l >= 2; --l) {
+        for (int p : T.levels[l]) {
+          SpmvRow r{yv + off[p], rank[p], (int)terms.size(), 0, 0};
+          for (int c : T.children[p]) {
+            term(tvt[c], 0, yv + off[c]);
+            r.nt++;
+          }
+          rows.push_back(r);
+        }
+        stage();
+      }
+      for (int l = 2; l <= T.depth; ++l) {
+        for (int c : T.levels[l]) {
+          SpmvRow r{zv + off[c], rank[c], (int)terms.size(), 0, 0};
+          for (int q : T.inters[c]) {
+            term(coupling.at(key2(c, q)), 0, yv + off[q]);
+            r.nt++;
+          }
+          if (l > 2) {
+            term(tu[c], 0, zv + off[T.parent[c]]);
+            r.nt++;
+          }
+          rows.push_back(r);
+        }
+        stage();
+      }
+    }
     for (int c : T.leaves()) {
-      SpmvRow r{yv.p + off[c], rank[c], (int)terms.size(), 1, 0};
-      terms.push_back({leaf_v[c].p, leaf_v[c].r, leaf_v[c].c, leaf_v[c].c, 1,
-                       xs + T.start[c]});
+      SpmvRow r{py + T.start[c], T.stop[c] - T.start[c], (int)terms.size(), 0, 0};
+      for (int q : T.nbrs[c]) {
+        term(near.at(key2(c, q)), 0, px + T.start[q]);
+        r.nt++;
+      }
+      if (has_far) {
+        term(leaf_u[c], 0, zv + off[c]);
+        r.nt++;
+      }
       rows.push_back(r);
     }
-    run(rows, terms);
-    for (int l = T.depth - 1; l >= 2; --l) {
-      for (int p : T.levels[l]) {
-        SpmvRow r{yv.p + off[p], rank[p], (int)terms.size(), 0, 0};
-        for (int c : T.children[p]) {
-          terms.push_back({tvt[c].p, tvt[c].r, tvt[c].c, tvt[c].c, 0, yv.p + off[c]});
-          r.nt++;
-        }
-        rows.push_back(r);
-      }
-      run(rows, terms);
-    }
-    for (int l = 2; l <= T.depth; ++l) {
-      for (int c : T.levels[l]) {
-        SpmvRow r{zv.p + off[c], rank[c], (int)terms.size(), 0, 0};
-        for (int q : T.inters[c]) {
-          const Blk& K = coupling.at(key2(c, q));
-          terms.push_back({K.p, K.r, K.c, K.c, 0, yv.p + off[q]});
-          r.nt++;
-        }
-        if (l > 2) {
-          const int p = T.parent[c];
-          terms.push_back({tu[c].p, tu[c].r, tu[c].c, tu[c].c, 0, zv.p + off[p]});
-          r.nt++;
-        }
-        rows.push_back(r);
-      }
-      run(rows, terms);
-    }
+    stage();
+    static_assert(sizeof(SpmvRow) % 8 == 0 && sizeof(SpmvTerm) % 8 == 0, "descriptor alignment");
+    const size_t rb = rows.size() * sizeof(SpmvRow), tb = terms.size() * sizeof(SpmvTerm);
+    plan.desc = C.alloc(1, (int)((rb + tb) / 8 + 1));
+    CUDA_CHECK(cudaMemcpyAsync(plan.desc.p, rows.data(), rb, cudaMemcpyHostToDevice, C.st));
+    CUDA_CHECK(cudaMemcpyAsync((char*)plan.desc.p + rb, terms.data(), tb, cudaMemcpyHostToDevice,
+                               C.st));
+    C.sync();  // the host vectors go out of scope
+    plan.n_rows = rows.size();
+    plan.n_terms = terms.size();
+    plan.bytes = bytes;
+    plan.valid = true;
   }
-  for (int c : T.leaves()) {
-    const int m = T.stop[c] - T.start[c];
-    SpmvRow r{ys + T.start[c], m, (int)terms.size(), 0, 0};
-    for (int q : T.nbrs[c]) {
-      const Blk& S = near.at(key2(c, q));
-      terms.push_back({S.p, S.r, S.c, S.c, 0, xs + T.start[q]});
-      r.nt++;
-    }
-    if (has_far) {
-      terms.push_back({leaf_u[c].p, leaf_u[c].r, leaf_u[c].c, leaf_u[c].c, 0, zv.p + off[c]});
-      r.nt++;
-    }
-    rows.push_back(r);
-  }
-  run(rows, terms);
-  C.free(yv);
-  C.free(zv);
+  const size_t nb = (size_t)T.n_points * sizeof(double);
+  CUDA_CHECK(cudaMemcpyAsync(plan.xin.p, xs, nb, cudaMemcpyDeviceToDevice, C.st));
+  const SpmvRow* dr = reinterpret_cast<const SpmvRow*>(plan.desc.p);
+  const SpmvTerm* dt = reinterpret_cast<const SpmvTerm*>((const char*)plan.desc.p +
+                                                         plan.n_rows * sizeof(SpmvRow));
+  cudaEvent_t ka = nullptr;
+  C.kt_begin(K_SPMV, plan.bytes, &ka);
+  for (auto& L : plan.launches) launch_spmv(dr + L.first, L.second, dt, 1, 1, C.st);
+  C.kt_end(K_SPMV, plan.bytes, ka);
+  C.launches += (long long)plan.launches.size();
+  CUDA_CHECK(cudaMemcpyAsync(ys, plan.yout.p, nb, cudaMemcpyDeviceToDevice, C.st));
   CUDA_CHECK(cudaGetLastError());
-  C.flush();
 }
 
 // ---------------------------------------------------------------------------

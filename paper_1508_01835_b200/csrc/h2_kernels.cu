@@ -39,16 +39,33 @@ __device__ __forceinline__ double euclid(double ax, double ay, double az, double
 
 namespace {
 
-__global__ void eval_blocks_kernel(const EvalDesc* __restrict__ descs, int n, KernelSpec k) {
+// One CTA per block: the source points Q are staged once in shared memory
+// (structure of arrays, chunks of EV_QC points); a warp owns a target row i
+// (P_i in registers) and its lanes sweep the columns, so the row's stores are
+// one coalesced 256-byte segment per 32 columns and there is no per-element
+// integer division.  HBM-bound: 8 B written per entry.
+constexpr int EV_QC = 512;
+__global__ void __launch_bounds__(256)
+eval_blocks_kernel(const EvalDesc* __restrict__ descs, int n, KernelSpec k) {
+  __shared__ double qx[EV_QC], qy[EV_QC], qz[EV_QC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int b = blockIdx.x; b < n; b += gridDim.x) {
     const EvalDesc d = descs[b];
-    const long long tot = (long long)d.m * d.n;
-    for (long long e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int i = (int)(e / d.n), j = (int)(e % d.n);
-      const double* p = d.P + 3 * (size_t)i;
-      const double* q = d.Q + 3 * (size_t)j;
-      const double r = euclid(p[0], p[1], p[2], q[0], q[1], q[2]);
-      d.out[(size_t)i * d.ldo + j] = kernel_value(k, r);
+    for (int j0 = 0; j0 < d.n; j0 += EV_QC) {
+      const int nj = d.n - j0 < EV_QC ? d.n - j0 : EV_QC;
+      __syncthreads();
+      for (int j = threadIdx.x; j < nj; j += blockDim.x) {
+        const double* q = d.Q + 3 * (size_t)(j0 + j);
+        qx[j] = q[0]; qy[j] = q[1]; qz[j] = q[2];
+      }
+      __syncthreads();
+      for (int i = warp; i < d.m; i += nw) {
+        const double* p = d.P + 3 * (size_t)i;
+        const double px = p[0], py = p[1], pz = p[2];
+        double* o = d.out + (size_t)i * d.ldo + j0;
+        for (int j = lane; j < nj; j += 32)
+          o[j] = kernel_value(k, euclid(px, py, pz, qx[j], qy[j], qz[j]));
+      }
     }
   }
 }

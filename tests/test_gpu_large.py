@@ -87,3 +87,64 @@ def test_c3_colored_schedule_residual():
     print(f"c3 colored: exact residual ours {res:.4e} ref {res_ref:.4e}; levels "
           f"{[(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in fct.stats.levels]}")
     assert res <= 2.0 * res_ref, (res, res_ref)
+
+
+def _list_checksum(lists):
+    M = (1 << 61) - 1
+    acc = 0
+    for i, l in enumerate(lists):
+        a = np.asarray(l, dtype=np.int64)
+        if len(a):
+            acc = (acc + (i + 1) * int(((a + 1) * np.arange(1, len(a) + 1)).sum() % M)) % M
+    return acc
+
+
+def test_c4_structure_and_ranks_against_reference():
+    """c4 (the BASELINE headline config, N = 1,048,576): the reference cannot
+    factorize it in the build container, so parity is pinned on what it does
+    produce (tests/golden/make_golden_c4.py, unmodified reference): the tree
+    and the interaction lists bit-exact, and every cluster's H2 rank from the
+    reference's leaf / transfer reductions (h2.py:121-150) exact.  The engine
+    then factorizes and solves it once; the size-independent properties the
+    domain offers are checked: the leaf level drops every fill (Frobenius
+    pre-filter == compression decision), repeated solves are bitwise equal, the
+    solve is linear, and the exact-matvec residual is reported."""
+    import torch
+    import paper_1508_01835_b200 as P
+    g = np.load(os.path.join(GOLDEN, "large", "c4_structure.npz"))
+    N, eps = int(g["N"]), float(g["eps"])
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip("c4 needs ~136 GB of device memory")
+    pts = np.random.Generator(np.random.PCG64(int(g["seed"]))).uniform(0.0, 1.0, size=(N, 3))
+    b = np.random.Generator(np.random.PCG64(int(g["seed"]) + 1)).standard_normal(N)
+    tree, perm = P.build_octree(pts, int(g["leaf"]))
+    assert tree.depth == int(g["depth"]) and tree.n_clusters == int(g["n_clusters"])
+    assert int((np.asarray(perm, dtype=np.int64) * np.arange(1, N + 1)).sum()) == int(g["perm_checksum"])
+    assert int(sum((i + 1) * (c.start + 3 * c.stop) for i, c in enumerate(tree.clusters))
+               % ((1 << 61) - 1)) == int(g["range_checksum"])
+    topo = P.compute_topology(tree)
+    np.testing.assert_array_equal([len(x) for x in topo.neighbors], g["n_neighbors"])
+    np.testing.assert_array_equal([len(x) for x in topo.interactions], g["n_interactions"])
+    assert _list_checksum(topo.neighbors) == int(g["neighbors_checksum"])
+    assert _list_checksum(topo.interactions) == int(g["interactions_checksum"])
+    K = P.imq_kernel(N ** (-1.0 / 3.0))
+    ops = P.chebyshev_operators(tree, topo, K, int(g["n"]), epsilon=eps)
+    np.testing.assert_array_equal([ops.rank.get(c, -1) for c in range(tree.n_clusters)], g["ranks"])
+    P.initialize_weights(ops, topo)
+    graph = P.assemble_extended_graph(ops, consume=True)
+    fct = P.factorize(graph, eps, seed=0, schedule="wavefront")
+    lv = fct.stats.levels
+    assert lv[0].level == 5 and lv[0].compressed_pairs == 0 and lv[0].dropped_pairs > 4_000_000
+    db = torch.from_numpy(b).cuda()
+    x1, x2 = fct.solve(db), fct.solve(db)
+    assert torch.equal(x1, x2)
+    u = torch.from_numpy(np.random.default_rng(7).standard_normal(N)).cuda()
+    lin = float(torch.linalg.norm(fct.solve(db + 0.5 * u) - x1 - 0.5 * fct.solve(u)) / torch.linalg.norm(x1))
+    assert lin <= 1e-9, lin
+    x = x1.cpu().numpy()
+    res = float(np.linalg.norm(P.exact_matvec(pts, K, x) - b) / np.linalg.norm(b))
+    print(f"c4: levels {[(s.level, s.compressed_pairs, s.dropped_pairs, sum(s.ranks)) for s in lv]}; "
+          f"exact-matvec residual {res:.3e} (eps*sigma0 = {eps * fct.sigma0:.3g}: the direct solve at this "
+          f"absolute threshold is a preconditioner, not a solver); solve linearity defect {lin:.1e}")
+    assert np.isfinite(res)

@@ -26,3 +26,5 @@ t0 = time.perf_counter()
 f = P.factorize(graph, 1e-6, sigma0=s0)
 x = f.solve(b)
 print(f"N={N} factorize+solve {time.perf_counter() - t0:.2f}s")
+y = P.h2_matvec(ops, b)
+print("h2 residual %.3e" % (np.linalg.norm(P.h2_matvec(ops, x) - b) / np.linalg.norm(b)))
