@@ -47,6 +47,12 @@ int ifmm_tree_topology(void* tree, long long* nbr_ptr, int* nbr_idx,
  * kernel_kind: 1 exp(-r), 2 inverse multiquadric 1/sqrt(r^2+p0^2),
  * 3 benchmark kernel (kernels.py:42-56, d = p0), 4 zero.              */
 void* ifmm_h2_build(void* tree, int kernel_kind, double p0, int n_cheb, double epsilon);
+/* Same with a second kernel parameter.  kernel_kind 5: Rotne-Prager-Yamakawa
+ * mobility (kernels.py:59-91, block_dim 3: three unknowns per point,
+ * point-major), p0 = particle radius a, p1 = 1 / (6 pi eta a).  Vectors of
+ * an operator built on a block_dim-3 kernel have 3 * n_points entries.      */
+void* ifmm_h2_build_k(void* tree, int kernel_kind, double p0, double p1, int n_cheb,
+                      double epsilon);
 void ifmm_h2_destroy(void* h2);
 int ifmm_h2_ranks(void* h2, int* ranks_out /* n_clusters, -1 if none */);
 /* initialize_weights, rigorous mode (h2.py:185-231). */
@@ -158,6 +164,8 @@ int ifmm_h2_matvec_part(void* h2, const double* xs, double* ys, double* yv, int 
  * and vectors in the same (any) order.  Used for the residual criterion. */
 int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double* points,
                       const double* x, double* y, int on_device);
+int ifmm_exact_matvec_k(void* ctx, int kernel_kind, double p0, double p1, int n,
+                        const double* points, const double* x, double* y, int on_device);
 
 /* ---- GMRES Arnoldi on the device:  krylov.py:32-116 -------------------
  * Device pointers on the context's stream; V holds the Krylov vectors as
@@ -220,6 +228,9 @@ int ifmm_union_post_profile(unsigned long long* out, int reset);
  * the device (dense.py:23-32, dense_matrix).  P (m x 3), Q (n x 3).       */
 int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const double* P, int n,
                        const double* Q, double* out, int on_device);
+/* block_dim-3 kernels (kind 5): out is (3 m) x (3 n). */
+int ifmm_kernel_matrix_k(void* ctx, int kernel_kind, double p0, double p1, int m, const double* P,
+                         int n, const double* Q, double* out, int on_device);
 /* block_diag_preconditioner (krylov.py:172-196): LU of the diagonal blocks
  * of A (n x n, ld lda; last block shorter) on the device; apply solves them
  * blockwise.  A singular block fails with status 2.                       */

@@ -169,17 +169,23 @@ int ifmm_tree_topology(void* p, long long* nbr_ptr, int* nbr_idx, long long* int
 
 // ---- H2 ---------------------------------------------------------------------
 void* ifmm_h2_build(void* tree, int kernel_kind, double p0, int n_cheb, double epsilon) {
+  return ifmm_h2_build_k(tree, kernel_kind, p0, 0.0, n_cheb, epsilon);
+}
+
+void* ifmm_h2_build_k(void* tree, int kernel_kind, double p0, double p1, int n_cheb,
+                      double epsilon) {
   ABI_TRY
   Tree* t = (Tree*)tree;
   if (!t->ctx) throw Error(E_CUDA, "tree has no device context");
   if (n_cheb < 1) throw Error(E_VALUE, "n must be >= 1");
   if (n_cheb > MAX_CHEB) throw Error(E_VALUE, "n_cheb too large");
-  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
+  if (kernel_kind < 1 || kernel_kind > KERNEL_KIND_MAX) throw Error(E_VALUE, "unknown kernel kind");
   H2* h = new H2;
   h->ctx = t->ctx;
   h->tree = t;
   h->kern.kind = kernel_kind;
   h->kern.p0 = p0;
+  h->kern.p1 = p1;
   h->ncheb = n_cheb;
   h->eps = epsilon;
   try {
@@ -243,13 +249,13 @@ int ifmm_h2_block(void* p, int which, int i, int j, double* out, int* rows, int*
 
 // gather/scatter by the tree permutation on device
 namespace {
-__global__ void k_gather(const double* in, const int* perm, int n, double* out) {
+__global__ void k_gather(const double* in, const int* perm, int n, int bd, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = in[perm[i]];
+  if (i < n) out[i] = in[(size_t)perm[i / bd] * bd + i % bd];
 }
-__global__ void k_scatter(const double* in, const int* perm, int n, double* out) {
+__global__ void k_scatter(const double* in, const int* perm, int n, int bd, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[perm[i]] = in[i];
+  if (i < n) out[(size_t)perm[i / bd] * bd + i % bd] = in[i];
 }
 }  // namespace
 
@@ -258,13 +264,14 @@ int ifmm_h2_matvec(void* p, const double* x, double* y, int on_device) {
   H2* h = (H2*)p;
   if (h->consumed) throw Error(E_VALUE, "operators were consumed by a graph");
   Ctx& C = *h->ctx;
-  const int N = h->tree->n_points;
+  const int bd = h->kern.bd();
+  const int N = bd * h->tree->n_points;
   Blk xin = C.alloc(1, N), xs = C.alloc(1, N), ys = C.alloc(1, N), yo = C.alloc(1, N);
   if (on_device) CUDA_CHECK(cudaMemcpyAsync(xin.p, x, 8 * (size_t)N, cudaMemcpyDeviceToDevice, C.st));
   else CUDA_CHECK(cudaMemcpyAsync(xin.p, x, 8 * (size_t)N, cudaMemcpyHostToDevice, C.st));
-  k_gather<<<(N + 255) / 256, 256, 0, C.st>>>(xin.p, h->tree->d_perm, N, xs.p);
+  k_gather<<<(N + 255) / 256, 256, 0, C.st>>>(xin.p, h->tree->d_perm, N, bd, xs.p);
   h->matvec(xs.p, ys.p);
-  k_scatter<<<(N + 255) / 256, 256, 0, C.st>>>(ys.p, h->tree->d_perm, N, yo.p);
+  k_scatter<<<(N + 255) / 256, 256, 0, C.st>>>(ys.p, h->tree->d_perm, N, bd, yo.p);
   if (on_device) CUDA_CHECK(cudaMemcpyAsync(y, yo.p, 8 * (size_t)N, cudaMemcpyDeviceToDevice, C.st));
   else CUDA_CHECK(cudaMemcpyAsync(y, yo.p, 8 * (size_t)N, cudaMemcpyDeviceToHost, C.st));
   C.sync();
@@ -644,18 +651,24 @@ int ifmm_solve(void* p, const double* b, double* x, int on_device) {
 // ---- exact dense matvec (experiments._matvec_oracle / dense.dense_matrix) -------
 int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double* points,
                       const double* x, double* y, int on_device) {
+  return ifmm_exact_matvec_k(ctx, kernel_kind, p0, 0.0, n, points, x, y, on_device);
+}
+
+int ifmm_exact_matvec_k(void* ctx, int kernel_kind, double p0, double p1, int n,
+                        const double* points, const double* x, double* y, int on_device) {
   ABI_TRY
   Ctx& C = *(Ctx*)ctx;
-  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
-  KernelSpec k{kernel_kind, p0};
-  Blk P = C.alloc(n, 3), X = C.alloc(1, n), Y = C.alloc(1, n);
+  if (kernel_kind < 1 || kernel_kind > KERNEL_KIND_MAX) throw Error(E_VALUE, "unknown kernel kind");
+  KernelSpec k{kernel_kind, p0, p1};
+  const int nd = n * k.bd();
+  Blk P = C.alloc(n, 3), X = C.alloc(1, nd), Y = C.alloc(1, nd);
   const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   const cudaMemcpyKind kout = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   CUDA_CHECK(cudaMemcpyAsync(P.p, points, 24 * (size_t)n, kin, C.st));
-  CUDA_CHECK(cudaMemcpyAsync(X.p, x, 8 * (size_t)n, kin, C.st));
+  CUDA_CHECK(cudaMemcpyAsync(X.p, x, 8 * (size_t)nd, kin, C.st));
   launch_exact_matvec(P.p, X.p, n, k, Y.p, C.st);
   CUDA_CHECK(cudaGetLastError());
-  CUDA_CHECK(cudaMemcpyAsync(y, Y.p, 8 * (size_t)n, kout, C.st));
+  CUDA_CHECK(cudaMemcpyAsync(y, Y.p, 8 * (size_t)nd, kout, C.st));
   C.sync();
   C.free(P); C.free(X); C.free(Y);
   C.flush();
@@ -666,12 +679,18 @@ int ifmm_exact_matvec(void* ctx, int kernel_kind, double p0, int n, const double
 // ---- dense kernel matrix (dense.py:23-32) ---------------------------------------
 int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const double* P, int n,
                        const double* Q, double* out, int on_device) {
+  return ifmm_kernel_matrix_k(ctx, kernel_kind, p0, 0.0, m, P, n, Q, out, on_device);
+}
+
+int ifmm_kernel_matrix_k(void* ctx, int kernel_kind, double p0, double p1, int m, const double* P,
+                         int n, const double* Q, double* out, int on_device) {
   ABI_TRY
   Ctx& C = *(Ctx*)ctx;
-  if (kernel_kind < 1 || kernel_kind > 4) throw Error(E_VALUE, "unknown kernel kind");
+  if (kernel_kind < 1 || kernel_kind > KERNEL_KIND_MAX) throw Error(E_VALUE, "unknown kernel kind");
   if (m < 0 || n < 0) throw Error(E_VALUE, "negative matrix size");
   if ((long long)m * n == 0) return 0;
-  KernelSpec k{kernel_kind, p0};
+  KernelSpec k{kernel_kind, p0, p1};
+  const int bd = k.bd();
   const cudaMemcpyKind kin = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   Blk dP = C.alloc(m, 3), dQ = C.alloc(n, 3);
   CUDA_CHECK(cudaMemcpyAsync(dP.p, P, 24 * (size_t)m, kin, C.st));
@@ -681,19 +700,19 @@ int ifmm_kernel_matrix(void* ctx, int kernel_kind, double p0, int m, const doubl
   const long long panel = (long long)rows * n;
   Blk O;
   double* dst = out;
-  if (!on_device) { O = C.alloc(m, n); dst = O.p; }
+  if (!on_device) { O = C.alloc(bd * m, bd * n); dst = O.p; }
   std::vector<EvalDesc> ed;
   for (int r0 = 0; r0 < m; r0 += rows) {
     EvalDesc d;
     d.P = dP.p + 3 * (size_t)r0; d.Q = dQ.p; d.m = std::min(rows, m - r0); d.n = n;
-    d.out = dst + (size_t)r0 * n; d.ldo = n;
+    d.out = dst + (size_t)(bd * r0) * (bd * n); d.ldo = bd * n;
     ed.push_back(d);
   }
   (void)panel;
   launch_eval(C.stage.push_vec(C, ed), (int)ed.size(), k, C.st);
   CUDA_CHECK(cudaGetLastError());
   if (!on_device)
-    CUDA_CHECK(cudaMemcpyAsync(out, O.p, 8 * (size_t)m * n, cudaMemcpyDeviceToHost, C.st));
+    CUDA_CHECK(cudaMemcpyAsync(out, O.p, 8 * (size_t)m * n * bd * bd, cudaMemcpyDeviceToHost, C.st));
   C.sync();
   C.free(dP); C.free(dQ); C.free(O);
   C.flush();

@@ -89,6 +89,7 @@ struct Graph {
   std::vector<Blk> su, sv;
   long long peak_edges = 0;
   bool consumed = false;
+  int bd = 1;  // block_dim of the kernel (unknowns per point)
   ~Graph();
 
   int new_node(int sz, int k, int own) {
@@ -171,7 +172,8 @@ struct SolveList;
 struct Factor {
   Ctx* ctx = nullptr;
   int n_points = 0;
-  const int* d_perm = nullptr;  // tree's device permutation (tree outlives factor)
+  const int* d_perm = nullptr;  // tree's device permutation of the POINTS (tree outlives factor)
+  int bd = 1;                   // unknowns per point (block_dim); n_points counts unknowns
   double eps = 0, sigma0 = 0;
   std::vector<int> init_sizes;
   std::vector<int> leaf_nodes, leaf_start, leaf_stop;

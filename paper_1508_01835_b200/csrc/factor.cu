@@ -1824,7 +1824,8 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags, NormalSource 
   auto t0 = std::chrono::steady_clock::now();
   Factor* F = new Factor;
   F->ctx = &C;
-  F->n_points = T.n_points;
+  F->bd = g.bd;
+  F->n_points = g.bd * T.n_points;
   F->d_perm = T.d_perm;
   F->eps = eps;
   F->sigma0 = sigma0;
@@ -1832,8 +1833,8 @@ Factor* factorize(Graph* gp, double eps, double sigma0, int flags, NormalSource 
   F->n_clusters = T.nc;
   for (int c : T.leaves()) {
     F->leaf_nodes.push_back(g.nx[c]);
-    F->leaf_start.push_back(T.start[c]);
-    F->leaf_stop.push_back(T.stop[c]);
+    F->leaf_start.push_back(g.bd * T.start[c]);
+    F->leaf_stop.push_back(g.bd * T.stop[c]);
   }
   Eliminator el(C, g, *F, eps * sigma0, 0x1f2e3d4c5b6a7988ULL);
   el.exact_order = (flags & 1) != 0;

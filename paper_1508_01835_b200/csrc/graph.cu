@@ -26,7 +26,8 @@ void Graph::build(H2* h, bool consume) {
   nx.assign(T.nc, -1); nz.assign(T.nc, -1); ny.assign(T.nc, -1);
   dead.assign(T.nc, 0);
   su.assign(T.nc, Blk()); sv.assign(T.nc, Blk());
-  for (int c : T.leaves()) nx[c] = new_node(T.stop[c] - T.start[c], NK_X, c);
+  bd = h->kern.bd();
+  for (int c : T.leaves()) nx[c] = new_node(bd * (T.stop[c] - T.start[c]), NK_X, c);
   for (int l = 2; l <= T.depth; ++l)
     for (int c : T.levels[l]) {
       nz[c] = new_node(h->rank[c], NK_Z, c);
@@ -96,7 +97,7 @@ Graph* Graph::clone() const {
   IFMM_ASSERT(!consumed, "copy of a consumed graph");
   Ctx& C = *ctx;
   Graph* g = new Graph;
-  g->ctx = ctx; g->tree = tree; g->ops = ops;
+  g->ctx = ctx; g->tree = tree; g->ops = ops; g->bd = bd;
   g->size = size; g->kind = kind; g->owner = owner;
   g->nx = nx; g->nz = nz; g->ny = ny;
   g->rows = rows; g->cols = cols; g->dead = dead;

@@ -26,7 +26,18 @@ void H2::build() {
   Ctx& C = *ctx;
   Tree& T = *tree;
   const int g3 = ncheb * ncheb * ncheb;
+  // block_dim > 1 (kernels.py:33, h2.py:70-74 _kron_bd): every interpolation
+  // matrix is kron(., I_bd), so a cluster's grid has g3b = bd g3 coefficients
+  // and a leaf of m points has bd m rows (point-major ordering)
+  const int bd = kern.bd();
+  const int g3b = bd * g3;
   const double rel = std::max(eps, 1e-13);
+  // dst (bd r x bd c) = kron(src (r x c), I_bd): zero fill, then bd strided copies
+  auto kron = [&](CopyBatch& zero, CopyBatch& cp, const Blk& src, const Blk& dst) {
+    zero.add(nullptr, 0, 0, dst.p, dst.c, 1, dst.r, dst.c, 3);
+    for (int a = 0; a < bd; ++a)
+      cp.add(src.p, src.c, 1, dst.p + (size_t)a * dst.c + a, bd * dst.c, bd, src.r, src.c, 0);
+  };
   const int nc = T.nc;
   rank.assign(nc, -1);
   leaf_u.assign(nc, Blk()); leaf_v.assign(nc, Blk());
@@ -38,54 +49,61 @@ void H2::build() {
   {
     const auto leaves = T.leaves();
     const int nl = (int)leaves.size();
-    std::vector<Blk> Pm(nl), Ub(nl), Sb(nl), Vb(nl), Wk(nl);
+    std::vector<Blk> Pm(nl), Pk(nl), Ub(nl), Sb(nl), Vb(nl), Wk(nl);
+    CopyBatch kz, kc;
     Blk ranks_b = C.alloc(1, (nl + 1) / 2 + 1);
     int* d_rank = reinterpret_cast<int*>(ranks_b.p);
     std::vector<InterpDesc> idesc;
     std::vector<SvdDesc> sdesc;
     for (int t = 0; t < nl; ++t) {
       const int c = leaves[t];
-      const int m = T.stop[c] - T.start[c];
-      const int mn = std::min(m, g3);
-      Pm[t] = C.alloc(m, g3);
+      const int mp = T.stop[c] - T.start[c];
+      const int m = bd * mp;
+      const int mn = std::min(m, g3b);
+      Pm[t] = C.alloc(mp, g3);
+      Pk[t] = bd > 1 ? C.alloc(m, g3b) : Pm[t];
+      if (bd > 1) kron(kz, kc, Pm[t], Pk[t]);
       Ub[t] = C.alloc(m, mn);
       Sb[t] = C.alloc(1, mn);
-      Vb[t] = C.alloc(g3, mn);
-      Wk[t] = C.alloc(1, (int)svd_work_doubles(m, g3));
+      Vb[t] = C.alloc(g3b, mn);
+      Wk[t] = C.alloc(1, (int)svd_work_doubles(m, g3b));
       InterpDesc d;
       d.pts = T.d_points + 3 * (size_t)T.start[c];
-      d.count = m;
+      d.count = mp;
       d.cx = T.center[3 * c]; d.cy = T.center[3 * c + 1]; d.cz = T.center[3 * c + 2];
       d.hw = T.hw[c];
       d.out = Pm[t].p;
       d.ldo = g3;
       idesc.push_back(d);
       SvdDesc s;
-      s.src = Pm[t].p; s.m = m; s.n = g3; s.s_r = g3; s.s_c = 1;
+      s.src = Pk[t].p; s.m = m; s.n = g3b; s.s_r = g3b; s.s_c = 1;
       s.U = Ub[t].p; s.S = Sb[t].p; s.V = Vb[t].p; s.rank = d_rank + t; s.work = Wk[t].p;
       sdesc.push_back(s);
     }
     launch_interp(C.stage.push_vec(C, idesc), nl, ncheb, C.st);
+    kz.run(C);
+    kc.run(C);
     launch_svd(C.stage.push_vec(C, sdesc), nl, rel, 64, C.st, 1);
     CUDA_CHECK(cudaGetLastError());
     const int* hr = C.readback_ints(d_rank, nl);
     CopyBatch cb;
     for (int t = 0; t < nl; ++t) {
       const int c = leaves[t];
-      const int m = T.stop[c] - T.start[c];
+      const int m = bd * (T.stop[c] - T.start[c]);
       const int k = hr[t];
       rank[c] = k;
       leaf_u[c] = C.alloc(m, k);
       leaf_v[c] = C.alloc(m, k);
-      G[c] = C.alloc(k, g3);
+      G[c] = C.alloc(k, g3b);
       // U col-major (ld m) -> row-major m x k
       cb.add(Ub[t].p, 1, m, leaf_u[c].p, k, 1, m, k, 0);
       cb.add(Ub[t].p, 1, m, leaf_v[c].p, k, 1, m, k, 0);
       // G[a][j] = s_a * V(j, a), V col-major (ld g3)
-      cb.add(Vb[t].p, g3, 1, G[c].p, g3, 1, k, g3, 0, 1.0, Sb[t].p);
+      cb.add(Vb[t].p, g3b, 1, G[c].p, g3b, 1, k, g3b, 0, 1.0, Sb[t].p);
     }
     cb.run(C);
     for (int t = 0; t < nl; ++t) {
+      if (bd > 1) C.free(Pk[t]);
       C.free(Pm[t]); C.free(Ub[t]); C.free(Sb[t]); C.free(Vb[t]); C.free(Wk[t]);
     }
     C.free(ranks_b);
@@ -119,13 +137,15 @@ void H2::build() {
     Blk ranks_b = C.alloc(1, (np + 1) / 2 + 1);
     int* d_rank = reinterpret_cast<int*>(ranks_b.p);
     GemmBatch gb;
+    CopyBatch kz, kc;
+    std::vector<Blk> Tk;  // kron(T, I_bd) when bd > 1
     std::vector<SvdDesc> sdesc;
     for (int t = 0; t < np; ++t) {
       const int p = ps[t];
       int rows = 0;
       for (int c : T.children[p]) rows += rank[c];
       tot[t] = rows;
-      stack[t] = C.alloc(rows, g3);
+      stack[t] = C.alloc(rows, g3b);
       int r0 = 0;
       for (int c : T.children[p]) {
         Blk tm = C.alloc(g3, g3);
@@ -136,19 +156,27 @@ void H2::build() {
         d.hw = T.hw[p];
         d.out = tm.p; d.ldo = g3;
         idesc.push_back(d);
-        gb.add(G[c].p, g3, 0, tm.p, g3, 0, stack[t].p + (size_t)r0 * g3, g3, rank[c], g3, g3,
-               1.0, 0.0);
+        Blk tk = tm;
+        if (bd > 1) {
+          tk = C.alloc(g3b, g3b);
+          Tk.push_back(tk);
+          kron(kz, kc, tm, tk);
+        }
+        gb.add(G[c].p, g3b, 0, tk.p, g3b, 0, stack[t].p + (size_t)r0 * g3b, g3b, rank[c], g3b,
+               g3b, 1.0, 0.0);
         r0 += rank[c];
       }
-      const int mn = std::min(rows, g3);
-      Ub[t] = C.alloc(rows, mn); Sb[t] = C.alloc(1, mn); Vb[t] = C.alloc(g3, mn);
-      Wk[t] = C.alloc(1, (int)svd_work_doubles(rows, g3));
+      const int mn = std::min(rows, g3b);
+      Ub[t] = C.alloc(rows, mn); Sb[t] = C.alloc(1, mn); Vb[t] = C.alloc(g3b, mn);
+      Wk[t] = C.alloc(1, (int)svd_work_doubles(rows, g3b));
       SvdDesc s;
-      s.src = stack[t].p; s.m = rows; s.n = g3; s.s_r = g3; s.s_c = 1;
+      s.src = stack[t].p; s.m = rows; s.n = g3b; s.s_r = g3b; s.s_c = 1;
       s.U = Ub[t].p; s.S = Sb[t].p; s.V = Vb[t].p; s.rank = d_rank + t; s.work = Wk[t].p;
       sdesc.push_back(s);
     }
     launch_interp(C.stage.push_vec(C, idesc), (int)idesc.size(), ncheb, C.st);
+    kz.run(C);
+    kc.run(C);
     gb.run(C);
     launch_svd(C.stage.push_vec(C, sdesc), np, rel, 64, C.st, 1);
     CUDA_CHECK(cudaGetLastError());
@@ -167,11 +195,12 @@ void H2::build() {
         cb.add(Ub[t].p + r0, 1, tot[t], tvt[c].p, 1, rank[c], rank[c], k, 0);
         r0 += rank[c];
       }
-      G[p] = C.alloc(k, g3);
-      cb.add(Vb[t].p, g3, 1, G[p].p, g3, 1, k, g3, 0, 1.0, Sb[t].p);
+      G[p] = C.alloc(k, g3b);
+      cb.add(Vb[t].p, g3b, 1, G[p].p, g3b, 1, k, g3b, 0, 1.0, Sb[t].p);
     }
     cb.run(C);
     for (auto& b : Tm) C.free(b);
+    for (auto& b : Tk) C.free(b);
     for (int t = 0; t < np; ++t) {
       C.free(stack[t]); C.free(Ub[t]); C.free(Sb[t]); C.free(Vb[t]); C.free(Wk[t]);
     }
@@ -186,7 +215,7 @@ void H2::build() {
       for (int i : T.levels[l])
         for (int j : T.inters[i])
           if (j > i) pairs.emplace_back(i, j);
-    const size_t per = (size_t)g3 * g3;
+    const size_t per = (size_t)g3b * g3b;
     const size_t chunk = std::max<size_t>(1, ((size_t)256 << 20) / (per * 8));
     for (size_t a = 0; a < pairs.size(); a += chunk) {
       const size_t b = std::min(pairs.size(), a + chunk);
@@ -194,7 +223,7 @@ void H2::build() {
       Blk kg = C.alloc(n, (int)per);
       int kmax = 0;
       for (size_t t = a; t < b; ++t) kmax = std::max(kmax, rank[pairs[t].first]);
-      Blk t1 = C.alloc(n, kmax * g3);
+      Blk t1 = C.alloc(n, kmax * g3b);
       std::vector<EvalDesc> ed;
       GemmBatch g1, g2;
       CopyBatch cb;
@@ -203,13 +232,13 @@ void H2::build() {
         const size_t o = (t - a);
         EvalDesc e;
         e.P = grid[i].p; e.Q = grid[j].p; e.m = g3; e.n = g3;
-        e.out = kg.p + o * per; e.ldo = g3;
+        e.out = kg.p + o * per; e.ldo = g3b;
         ed.push_back(e);
-        double* T1 = t1.p + o * (size_t)kmax * g3;
-        g1.add(G[i].p, g3, 0, e.out, g3, 0, T1, g3, rank[i], g3, g3, 1.0, 0.0);
+        double* T1 = t1.p + o * (size_t)kmax * g3b;
+        g1.add(G[i].p, g3b, 0, e.out, g3b, 0, T1, g3b, rank[i], g3b, g3b, 1.0, 0.0);
         Blk kij = C.alloc(rank[i], rank[j]);
         Blk kji = C.alloc(rank[j], rank[i]);
-        g2.add(T1, g3, 0, G[j].p, g3, 1, kij.p, rank[j], rank[i], rank[j], g3, 1.0, 0.0);
+        g2.add(T1, g3b, 0, G[j].p, g3b, 1, kij.p, rank[j], rank[i], rank[j], g3b, 1.0, 0.0);
         cb.add(kij.p, 1, rank[j], kji.p, rank[i], 1, rank[j], rank[i], 0);
         coupling[key2(i, j)] = kij;
         coupling[key2(j, i)] = kji;
@@ -231,11 +260,11 @@ void H2::build() {
       const int mi = T.stop[i] - T.start[i];
       for (int j : T.nbrs[i]) {
         const int mj = T.stop[j] - T.start[j];
-        Blk s = C.alloc(mi, mj);
+        Blk s = C.alloc(bd * mi, bd * mj);
         EvalDesc e;
         e.P = T.d_points + 3 * (size_t)T.start[i];
         e.Q = T.d_points + 3 * (size_t)T.start[j];
-        e.m = mi; e.n = mj; e.out = s.p; e.ldo = mj;
+        e.m = mi; e.n = mj; e.out = s.p; e.ldo = bd * mj;
         ed.push_back(e);
         near[key2(i, j)] = s;
         if (ed.size() >= 65536) {
@@ -416,8 +445,9 @@ void H2::matvec(const double* xs, double* ys) {
       if (rank[c] > 0 && T.level[c] >= 2) { off[c] = tot; tot += rank[c]; }
     plan.yv = C.alloc(1, (int)std::max<long long>(tot, 1));
     plan.zv = C.alloc(1, (int)std::max<long long>(tot, 1));
-    plan.xin = C.alloc(1, std::max(T.n_points, 1));
-    plan.yout = C.alloc(1, std::max(T.n_points, 1));
+    const int bd = kern.bd();
+    plan.xin = C.alloc(1, std::max(bd * T.n_points, 1));
+    plan.yout = C.alloc(1, std::max(bd * T.n_points, 1));
     const double* px = plan.xin.p;
     double* py = plan.yout.p;
     double* yv = plan.yv.p;
@@ -438,7 +468,7 @@ void H2::matvec(const double* xs, double* ys) {
     if (has_far) {
       for (int c : T.leaves()) {  // upward leaf: y = V^T x
         rows.push_back({yv + off[c], rank[c], (int)terms.size(), 1, 0});
-        term(leaf_v[c], 1, px + T.start[c]);
+        term(leaf_v[c], 1, px + (size_t)bd * T.start[c]);
       }
       stage();
       for (int l = T.depth - 1; l >= 2; --l) {
@@ -469,9 +499,9 @@ void H2::matvec(const double* xs, double* ys) {
       }
     }
     for (int c : T.leaves()) {
-      SpmvRow r{py + T.start[c], T.stop[c] - T.start[c], (int)terms.size(), 0, 0};
+      SpmvRow r{py + (size_t)bd * T.start[c], bd * (T.stop[c] - T.start[c]), (int)terms.size(), 0, 0};
       for (int q : T.nbrs[c]) {
-        term(near.at(key2(c, q)), 0, px + T.start[q]);
+        term(near.at(key2(c, q)), 0, px + (size_t)bd * T.start[q]);
         r.nt++;
       }
       if (has_far) {
@@ -493,7 +523,7 @@ void H2::matvec(const double* xs, double* ys) {
     plan.bytes = bytes;
     plan.valid = true;
   }
-  const size_t nb = (size_t)T.n_points * sizeof(double);
+  const size_t nb = (size_t)kern.bd() * T.n_points * sizeof(double);
   CUDA_CHECK(cudaMemcpyAsync(plan.xin.p, xs, nb, cudaMemcpyDeviceToDevice, C.st));
   const SpmvRow* dr = reinterpret_cast<const SpmvRow*>(plan.desc.p);
   const SpmvTerm* dt = reinterpret_cast<const SpmvTerm*>((const char*)plan.desc.p +

@@ -37,6 +37,31 @@ __device__ __forceinline__ double euclid(double ax, double ay, double az, double
   return sqrt(s);
 }
 
+// Rotne-Prager-Yamakawa mobility block f(r) I + g(r) rhat rhat^T
+// (kernels.py:59-91): far field r > 2a, overlap r <= 2a, self r = 0.
+// d = P_i - Q_j; writes the row-major 3 x 3 block into B.
+__device__ __forceinline__ void rpy_block(const KernelSpec& k, double dx, double dy, double dz,
+                                          double (&B)[9]) {
+  const double a = k.p0, c0 = k.p1;
+  const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  const double rs = r == 0.0 ? 1.0 : r;
+  double f, g;
+  if (r > 2.0 * a) {
+    const double a3 = a * a * a, r3 = rs * rs * rs;
+    f = c0 * (3.0 * a / (4.0 * rs) + a3 / (2.0 * r3));
+    g = c0 * (3.0 * a / (4.0 * rs) - 3.0 * a3 / (2.0 * r3));
+  } else {
+    f = c0 * (1.0 - 9.0 * r / (32.0 * a));
+    g = c0 * (3.0 * r / (32.0 * a));
+  }
+  if (r == 0.0) g = 0.0;
+  const double h[3] = {dx / rs, dy / rs, dz / rs};
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) B[3 * p + q] = (p == q ? f : 0.0) + g * (h[p] * h[q]);
+}
+
 namespace {
 
 // One CTA per block: the source points Q are staged once in shared memory
@@ -62,6 +87,18 @@ eval_blocks_kernel(const EvalDesc* __restrict__ descs, int n, KernelSpec k) {
       for (int i = warp; i < d.m; i += nw) {
         const double* p = d.P + 3 * (size_t)i;
         const double px = p[0], py = p[1], pz = p[2];
+        if (k.kind == KERNEL_RPY) {
+          double* o = d.out + (size_t)(3 * i) * d.ldo + 3 * j0;
+          for (int j = lane; j < nj; j += 32) {
+            double B[9];
+            rpy_block(k, px - qx[j], py - qy[j], pz - qz[j], B);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) o[(size_t)a * d.ldo + 3 * j + c] = B[3 * a + c];
+          }
+          continue;
+        }
         double* o = d.out + (size_t)i * d.ldo + j0;
         for (int j = lane; j < nj; j += 32)
           o[j] = kernel_value(k, euclid(px, py, pz, qx[j], qy[j], qz[j]));
@@ -157,28 +194,44 @@ __global__ void __launch_bounds__(256)
 exact_matvec_kernel(const double* __restrict__ pts, const double* __restrict__ x, int n,
                     KernelSpec k, double* __restrict__ y) {
   __shared__ double sp[EM_TILE * 3];
-  __shared__ double sx[EM_TILE];
+  __shared__ double sx[EM_TILE * 3];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double px = 0, py = 0, pz = 0;
   if (i < n) { px = pts[3 * i]; py = pts[3 * i + 1]; pz = pts[3 * i + 2]; }
-  double acc = 0.0;
+  const int bd = k.bd();
+  double acc = 0.0, acc1 = 0.0, acc2 = 0.0;
   for (int t0 = 0; t0 < n; t0 += EM_TILE) {
     const int cnt = min(EM_TILE, n - t0);
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
       sp[3 * e] = pts[3 * (t0 + e)];
       sp[3 * e + 1] = pts[3 * (t0 + e) + 1];
       sp[3 * e + 2] = pts[3 * (t0 + e) + 2];
-      sx[e] = x[t0 + e];
+      for (int a = 0; a < bd; ++a) sx[bd * e + a] = x[(size_t)bd * (t0 + e) + a];
     }
     __syncthreads();
-    if (i < n)
-      for (int e = 0; e < cnt; ++e) {
-        const double r = euclid(px, py, pz, sp[3 * e], sp[3 * e + 1], sp[3 * e + 2]);
-        acc = fma(kernel_value(k, r), sx[e], acc);
+    if (i < n) {
+      if (bd == 3) {
+        for (int e = 0; e < cnt; ++e) {
+          double B[9];
+          rpy_block(k, px - sp[3 * e], py - sp[3 * e + 1], pz - sp[3 * e + 2], B);
+          const double x0 = sx[3 * e], x1 = sx[3 * e + 1], x2 = sx[3 * e + 2];
+          acc = fma(B[0], x0, fma(B[1], x1, fma(B[2], x2, acc)));
+          acc1 = fma(B[3], x0, fma(B[4], x1, fma(B[5], x2, acc1)));
+          acc2 = fma(B[6], x0, fma(B[7], x1, fma(B[8], x2, acc2)));
+        }
+      } else {
+        for (int e = 0; e < cnt; ++e) {
+          const double r = euclid(px, py, pz, sp[3 * e], sp[3 * e + 1], sp[3 * e + 2]);
+          acc = fma(kernel_value(k, r), sx[e], acc);
+        }
       }
+    }
     __syncthreads();
   }
-  if (i < n) y[i] = acc;
+  if (i < n) {
+    if (bd == 3) { y[3 * (size_t)i] = acc; y[3 * (size_t)i + 1] = acc1; y[3 * (size_t)i + 2] = acc2; }
+    else y[i] = acc;
+  }
 }
 }  // namespace
 

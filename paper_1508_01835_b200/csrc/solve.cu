@@ -305,13 +305,15 @@ __global__ void top_update_kernel(const double* LU, int n, int r0, int r1, int c
   if (lane == 0) v[row] -= s;
 }
 
-__global__ void gather_perm_kernel(const double* b, const int* perm, int n, double* out) {
+// tree order <-> original order of the n = bd * points unknowns (point-major:
+// unknown p * bd + a of point p, factor.py:104-105,154-157)
+__global__ void gather_perm_kernel(const double* b, const int* perm, int n, int bd, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = b[perm[i]];
+  if (i < n) out[i] = b[(size_t)perm[i / bd] * bd + i % bd];
 }
-__global__ void scatter_perm_kernel(const double* in, const int* perm, int n, double* x) {
+__global__ void scatter_perm_kernel(const double* in, const int* perm, int n, int bd, double* x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[perm[i]] = in[i];
+  if (i < n) x[(size_t)perm[i / bd] * bd + i % bd] = in[i];
 }
 
 }  // namespace
@@ -558,7 +560,7 @@ void Factor::enqueue_program(cudaStream_t s) {
   double* W = P.work.p;
   const size_t wbytes = (size_t)P.work.r * P.work.c * sizeof(double);
   CUDA_CHECK(cudaMemsetAsync(W, 0, wbytes, s));
-  gather_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(P.bin.p, d_perm, N, W);
+  gather_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(P.bin.p, d_perm, N, bd, W);
   const SolveOp* ops = reinterpret_cast<const SolveOp*>(P.ops_d.p);
   const ListEnt* lists = reinterpret_cast<const ListEnt*>(P.list_d.p);
   const SolveTask* tasks = reinterpret_cast<const SolveTask*>(P.task_d.p);
@@ -603,7 +605,7 @@ void Factor::enqueue_program(cudaStream_t s) {
   }
   if (parts & 4)
     for (int li = P.n_fwd_launch; li + 1 < (int)P.task_start.size(); ++li) run(li);
-  scatter_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(W + P.sol0, d_perm, N, P.bout.p);
+  scatter_perm_kernel<<<(N + 255) / 256, 256, 0, s>>>(W + P.sol0, d_perm, N, bd, P.bout.p);
   CUDA_CHECK(cudaGetLastError());
 }
 

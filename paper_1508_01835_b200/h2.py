@@ -132,8 +132,8 @@ def chebyshev_operators(tree: Octree, topology: ClusterTopology, kernel: Kernel,
     """h2.py:104-182 on the device."""
     if n < 1:
         raise ValueError("n must be >= 1")
-    kind, p0 = kernel.device_spec()
-    h = N.lib().ifmm_h2_build(tree.handle().h, kind, p0, int(n), float(epsilon))
+    kind, p0, p1 = kernel.device_spec()
+    h = N.lib().ifmm_h2_build_k(tree.handle().h, kind, p0, p1, int(n), float(epsilon))
     return H2Operators(tree, topology, kernel, n, N.check_handle(h))
 
 

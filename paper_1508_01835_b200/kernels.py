@@ -17,7 +17,7 @@ from typing import Callable
 
 import numpy as np
 
-KIND = {"exp": 1, "imq": 2, "inverse_multiquadric": 2, "benchmark": 3, "zero": 4}
+KIND = {"exp": 1, "imq": 2, "inverse_multiquadric": 2, "benchmark": 3, "zero": 4, "rpy": 5}
 
 
 def _dist(P, Q):
@@ -39,21 +39,25 @@ class Kernel:
         return self.block(np.atleast_2d(ri), np.atleast_2d(rj))
 
     def device_spec(self):
-        """(kind, p0) understood by the CUDA engine, or ValueError."""
-        if self.block_dim != 1:
-            raise ValueError(f"kernel '{self.name}': block_dim {self.block_dim} has no device "
-                             "implementation yet (scalar kernels only)")
+        """(kind, p0, p1) understood by the CUDA engine, or ValueError.
+        kind 5 (RPY, block_dim 3): p0 = radius a, p1 = 1 / (6 pi eta a)."""
         if not self.symmetric:
             raise ValueError("non-symmetric kernels are not supported by the engine")
         kind = KIND.get(self.name)
         if kind is None:
             raise ValueError(f"kernel '{self.name}' has no device implementation; "
                              f"supported: {sorted(KIND)}")
+        if self.block_dim != (3 if kind == 5 else 1):
+            raise ValueError(f"kernel '{self.name}': block_dim {self.block_dim} has no device "
+                             "implementation")
         if kind == 2:
-            return kind, float(self.params["h"])
+            return kind, float(self.params["h"]), 0.0
         if kind == 3:
-            return kind, float(self.params["d"])
-        return kind, 0.0
+            return kind, float(self.params["d"]), 0.0
+        if kind == 5:
+            a = float(self.params["radius"])
+            return kind, a, 1.0 / (6.0 * np.pi * float(self.params["viscosity"]) * a)
+        return kind, 0.0, 0.0
 
 
 def exp_kernel() -> Kernel:
@@ -133,8 +137,8 @@ def rpy_kernel(radius: float, viscosity: float = 1.0) -> Kernel:
     f(r) I + g(r) r^ r^T with c = 1/(6 pi eta a); far field (r > 2a)
     f = c(3a/4r + a^3/2r^3), g = c(3a/4r - 3a^3/2r^3); overlap f = c(1 - 9r/32a),
     g = c(3r/32a); self f = c, g = 0.  The host ``block`` gives the
-    reference's point-major (3m x 3n) layout; the engine has no device
-    implementation of block_dim 3 kernels, so ``device_spec`` raises."""
+    reference's point-major (3m x 3n) layout; the engine evaluates the same
+    blocks in ``csrc/h2_kernels.cu`` (rpy_block, kernel kind 5)."""
     if radius <= 0 or viscosity <= 0:
         raise ValueError("radius and viscosity must be positive")
     a = float(radius)

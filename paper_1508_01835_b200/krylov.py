@@ -215,28 +215,29 @@ def exact_matvec(points, kernel, x):
     pts = np.ascontiguousarray(np.asarray(points, dtype=float))
     if pts.ndim != 2 or pts.shape[1] != 3:
         raise ValueError("points must be an (N, 3) array")
-    kind, p0 = kernel.device_spec()
+    kind, p0, p1 = kernel.device_spec()
+    dim = len(pts) * kernel.block_dim
     try:
         import torch
         is_t = isinstance(x, torch.Tensor) and x.is_cuda
     except Exception:
         is_t = False
     if is_t:
-        if x.shape != (len(pts),):
+        if x.shape != (dim,):
             raise ValueError("vector length mismatch")
         xd = x.to(torch.float64).contiguous()
         dp_ = torch.from_numpy(pts).to(xd.device)
         y = torch.empty_like(xd)
         torch.cuda.current_stream().synchronize()
-        N.check(N.lib().ifmm_exact_matvec(N.ctx(), kind, p0, len(pts), C.c_void_p(dp_.data_ptr()),
-                                          C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()), 1))
+        N.check(N.lib().ifmm_exact_matvec_k(N.ctx(), kind, p0, p1, len(pts), C.c_void_p(dp_.data_ptr()),
+                                            C.c_void_p(xd.data_ptr()), C.c_void_p(y.data_ptr()), 1))
         return y
     x = np.ascontiguousarray(np.asarray(x, dtype=float))
-    if len(x) != len(pts):
+    if len(x) != dim:
         raise ValueError("vector length mismatch")
     y = np.empty_like(x)
-    N.check(N.lib().ifmm_exact_matvec(N.ctx(), kind, p0, len(pts), pts.ctypes.data_as(C.c_void_p),
-                                      x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 0))
+    N.check(N.lib().ifmm_exact_matvec_k(N.ctx(), kind, p0, p1, len(pts), pts.ctypes.data_as(C.c_void_p),
+                                        x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 0))
     return y
 
 

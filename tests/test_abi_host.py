@@ -123,7 +123,9 @@ def test_kernel_plugin_contract():
     np.testing.assert_allclose(P.imq_kernel(0.1).block(A, B), O.imq_block(0.1)(A, B), rtol=1e-14)
     np.testing.assert_allclose(P.benchmark_kernel(0.3).block(A, B), O.benchmark_block(0.3)(A, B),
                                rtol=1e-14)
-    assert P.imq_kernel(0.1).device_spec() == (2, 0.1)
+    assert P.imq_kernel(0.1).device_spec() == (2, 0.1, 0.0)
+    k, a, c0 = P.rpy_kernel(0.25, 2.0).device_spec()
+    assert (k, a) == (5, 0.25) and abs(c0 - 1.0 / (6.0 * np.pi * 2.0 * 0.25)) < 1e-16
     with pytest.raises(ValueError):
         P.Kernel("custom", 1, {}, lambda P_, Q: None).device_spec()
 

@@ -113,9 +113,9 @@ def test_c4_structure_and_ranks_against_reference():
     import paper_1508_01835_b200 as P
     g = np.load(os.path.join(GOLDEN, "large", "c4_structure.npz"))
     N, eps = int(g["N"]), float(g["eps"])
-    free, _ = torch.cuda.mem_get_info()
-    if free < 150 * 2**30:
-        pytest.skip("c4 needs ~136 GB of device memory")
+    _, total = torch.cuda.mem_get_info()
+    if total < 170 * 2**30:
+        pytest.skip("c4 needs ~136 GB of device memory (arena + dedicated allocations)")
     pts = np.random.Generator(np.random.PCG64(int(g["seed"]))).uniform(0.0, 1.0, size=(N, 3))
     b = np.random.Generator(np.random.PCG64(int(g["seed"]) + 1)).standard_normal(N)
     tree, perm = P.build_octree(pts, int(g["leaf"]))

@@ -29,9 +29,9 @@ def test_scenes_match_reference_fixture():
         P.concentric_shells([1], [1.0, 2.0])
     with pytest.raises(ValueError):
         P.rpy_kernel(0.0)
-    # block_dim 3 has no device implementation: refused up front, no fallback
+    # a block_dim the engine does not implement is refused up front, no fallback
     with pytest.raises(ValueError):
-        P.rpy_kernel(0.3).device_spec()
+        P.Kernel("rpy", 2, {"radius": 0.3, "viscosity": 1.0}, lambda A, B: None).device_spec()
 
 
 def test_scene_text_roundtrip(tmp_path):
