@@ -31,7 +31,16 @@ graph = P.assemble_extended_graph(ops, consume=True)
 print("setup %.1f s, ranks sum %d (ref %d)" % (time.perf_counter() - t0, sum(ops.rank.values()),
                                                st["ranks_sum"]), flush=True)
 t0 = time.perf_counter()
-fct = P.factorize(graph, inp["eps"], seed=0, sigma0=st["sigma0"], schedule=sch)
+if sch == "morton_devrng":  # diagnostics: Morton one-at-a-time order with the device generator
+    from paper_1508_01835_b200 import _native as NN
+    from paper_1508_01835_b200.factor import IFMMFactorization
+    h = NN.check_handle(NN.lib().ifmm_factorize(graph._h, float(inp["eps"]), float(st["sigma0"]), 4))
+    graph.consumed = True
+    fct = IFMMFactorization(graph, h, inp["eps"], st["sigma0"], 0.0, 0.0)
+    fct.schedule = sch
+else:
+    fct = P.factorize(graph, inp["eps"], seed=int(os.environ.get("IFMM_C3_SEED", "0")), sigma0=st["sigma0"],
+                      schedule=sch)
 tf = time.perf_counter() - t0
 print("schedule", sch, "factorize %.2f s" % tf, "rsvd", fct.rsvd,
       {k: round(v, 2) for k, v in fct.timings.items()}, flush=True)
