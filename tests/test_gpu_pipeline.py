@@ -122,6 +122,68 @@ def test_partitioned_matvec_device_phases(world):
         assert float(torch.linalg.norm(y1 - ref) / torch.linalg.norm(ref)) < 1e-14
 
 
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_halo_exchange_device_phases(world):
+    """The halo-exchange protocol (partition.HaloPlan / distributed_matvec_halo)
+    over the DEVICE phases, one rank at a time on this GPU: what the peers
+    would send is taken from a full single-rank pass (their packed x ranges and
+    multipole segments), everything the plan does not deliver is NaN before
+    phase 1, and each rank's rows must equal the single-process h2_matvec."""
+    import ctypes as C
+    import torch
+    import paper_1508_01835_b200 as P
+    from paper_1508_01835_b200 import _native as N
+    from paper_1508_01835_b200.partition import HaloPlan, distributed_matvec_halo, h2_matvec_halo
+    g = load_golden("imq3d_n4096_leaf32")
+    tree, topo, ops = _pipeline(P, g)
+    n = ops.dim
+    x = torch.from_numpy(np.random.Generator(np.random.PCG64(9)).standard_normal(n)).cuda()
+    perm = torch.as_tensor(np.asarray(tree.perm), device="cuda")
+    ref = P.h2_matvec(ops, x)[perm]
+    xs = x[perm].contiguous()
+    ms = C.c_longlong()
+    N.check(N.lib().ifmm_h2_multipole_size(ops._h, C.byref(ms)))
+    full_yv = torch.zeros(ms.value, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    N.check(N.lib().ifmm_h2_matvec_part(ops._h, C.c_void_p(xs.data_ptr()), None,
+                                        C.c_void_p(full_yv.data_ptr()), 0, 0, n))
+
+    def phase_fn(a, b, c, phase, lo, hi):
+        torch.cuda.synchronize()
+        N.check(N.lib().ifmm_h2_matvec_part(ops._h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                            C.c_void_p(c.data_ptr()), phase, lo, hi))
+
+    zeros = lambda k: torch.zeros(k, dtype=torch.float64, device="cuda")  # noqa: E731
+    for me in range(world):
+        plan = HaloPlan.from_tree(tree, topo, ops.rank, world, me)
+        assert plan.n_multipole == ms.value
+        lo, hi = plan.ranges[me]
+        stage = {"n": 0}
+
+        def exchange(send, recv_len):  # the peers' packed buffers, from the full pass
+            segs, src, as_len = ((plan.x_recv, xs, False) if stage["n"] == 0 else (plan.y_recv, full_yv, True))
+            stage["n"] += 1
+            out = {}
+            for r, sl in segs.items():
+                out[r] = torch.cat([src[a:(a + b) if as_len else b] for a, b in sl])
+                assert out[r].numel() == recv_len[r]
+            return out
+
+        def allreduce(v):  # the summed partials of the clusters spanning ranks
+            v.copy_(torch.cat([full_yv[a:a + k] for a, k in plan.shared]))
+
+        ys = distributed_matvec_halo(xs[lo:hi].clone(), n, ms.value, plan, phase_fn, exchange, allreduce,
+                                     zeros, torch.cat, poison=float("nan"))
+        rel = float(torch.linalg.norm(ys - ref[lo:hi]) / torch.linalg.norm(ref[lo:hi]))
+        assert rel < 1e-13, (me, rel)
+        if world > 1:
+            vx, vy, vs = plan.volume()
+            assert vx < n and vy + vs < ms.value
+    plan1 = HaloPlan.from_tree(tree, topo, ops.rank, 1, 0)
+    y1 = h2_matvec_halo(ops, xs, plan1)  # the public entry without a process group
+    assert float(torch.linalg.norm(y1 - ref) / torch.linalg.norm(ref)) < 1e-13
+
+
 @pytest.mark.parametrize("name", ["imq3d_n2048", "exp2d_n2048_n6"])
 def test_exact_order_parity(name):
     """Strict reference pair order (one pair per wave, still pipelined):
