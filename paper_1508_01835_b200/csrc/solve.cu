@@ -105,6 +105,36 @@ Factor::~Factor() {
 // ---------------------------------------------------------------------------
 namespace {
 
+// Compensated dot products (TwoProd / TwoSum, _rn intrinsics so nothing is
+// contracted): every row sum of the replay is accumulated to about twice the
+// working precision and rounded once.  The replay multiplies by explicit
+// pivot-block inverses, whose rows cancel heavily on ill-conditioned blocks;
+// with plain FMA sums the solve's rounding error (~eps |P^-1| |b|, not
+// ~eps |x|) made the preconditioner visibly nonlinear and stalled GMRES's
+// true residual two orders above its recurrence residual (c5 recipe).
+IFMM_DEV void dd_fma(double a, double b, double& s, double& c) {
+  const double p = __dmul_rn(a, b);
+  const double e = __fma_rn(a, b, -p);
+  const double t = __dadd_rn(s, p);
+  const double z = __dadd_rn(t, -s);
+  c = __dadd_rn(c, __dadd_rn(__dadd_rn(__dadd_rn(s, -__dadd_rn(t, -z)), __dadd_rn(p, -z)), e));
+  s = t;
+}
+IFMM_DEV double warp_sum_dd(double s, double c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const double c2 = __shfl_xor_sync(0xffffffffu, c, o);
+    // symmetric in (s, s2): both partners compute the same pair
+    const double hi = fmax(s, s2), lo = fmin(s, s2);
+    const double t = __dadd_rn(hi, lo);
+    const double z = __dadd_rn(t, -hi);
+    c = __dadd_rn(__dadd_rn(c, c2), __dadd_rn(__dadd_rn(hi, -__dadd_rn(t, -z)), __dadd_rn(lo, -z)));
+    s = t;
+  }
+  return __dadd_rn(s, c);
+}
+
 // ---- row-task kernels (one launch per wave and phase) ----------------------
 // Each CTA takes one task; its 8 warps take the task's rows round robin, one
 // warp per row (lanes split the dot product, fixed shuffle tree).
@@ -121,9 +151,9 @@ solve_fwd_g_kernel(const SolveOp* __restrict__ ops, const SolveTask* __restrict_
   const double* rx = W + op.a;
   for (int i = t.r0 + warp; i < t.r1; i += 8) {
     const double* row = op.LU + (size_t)i * n;  // P^{-1} row i, first m columns
-    double s = 0.0;
-    for (int j = lane; j < m; j += 32) s = fma(row[j], rx[j], s);
-    s = warp_sum(s);
+    double s = 0.0, cc = 0.0;
+    for (int j = lane; j < m; j += 32) dd_fma(row[j], rx[j], s, cc);
+    s = warp_sum_dd(s, cc);
     if (lane == 0) {
       W[op.g + i] = s;
       if (i >= m) W[op.b + i - m] += s;  // rhs_y += g[m:]
@@ -142,9 +172,9 @@ solve_fwd_t_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ 
   const double* g = W + op.g;
   for (int i = t.r0 + warp; i < t.r1; i += 8) {
     const double* row = op.M + (size_t)(e.off + i) * op.ldm;
-    double s = 0.0;
-    for (int j = lane; j < m; j += 32) s = fma(row[j], g[j], s);
-    s = warp_sum(s);
+    double s = 0.0, cc = 0.0;
+    for (int j = lane; j < m; j += 32) dd_fma(row[j], g[j], s, cc);
+    s = warp_sum_dd(s, cc);
     if (lane == 0) W[e.slot + i] = W[e.slot + i] - s;
   }
 }
@@ -164,12 +194,12 @@ solve_bwd_v_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ 
         continue;
       }
       const double* row = op.M + (size_t)i * op.ldm;
-      double s = 0.0;
+      double s = 0.0, cc = 0.0;
       for (int l = op.list0; l < op.list0 + op.nlist; ++l) {
         const ListEnt e = lists[l];
-        for (int j = lane; j < e.len; j += 32) s = fma(row[e.off + j], W[e.slot + j], s);
+        for (int j = lane; j < e.len; j += 32) dd_fma(row[e.off + j], W[e.slot + j], s, cc);
       }
-      s = warp_sum(s);
+      s = warp_sum_dd(s, cc);
       if (lane == 0) W[op.g + i] = W[op.a + i] - s;
     }
     return;
@@ -187,10 +217,10 @@ solve_bwd_v_kernel(const SolveOp* __restrict__ ops, const ListEnt* __restrict__ 
       continue;
     }
     const double* row = op.M + (size_t)i * op.ldm;
-    double s = 0.0;
+    double s = 0.0, cc = 0.0;
 #pragma unroll 4
-    for (int j = lane; j < op.cols; j += 32) s = fma(row[j], gsol[j], s);
-    s = warp_sum(s);
+    for (int j = lane; j < op.cols; j += 32) dd_fma(row[j], gsol[j], s, cc);
+    s = warp_sum_dd(s, cc);
     if (lane == 0) W[op.g + i] = W[op.a + i] - s;
   }
 }
@@ -205,9 +235,9 @@ solve_bwd_x_kernel(const SolveOp* __restrict__ ops, const SolveTask* __restrict_
   const double* v = W + op.g;
   for (int i = t.r0 + warp; i < t.r1; i += 8) {
     const double* row = op.LU + (size_t)i * n;
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(row[j], v[j], s);
-    s = warp_sum(s);
+    double s = 0.0, cc = 0.0;
+    for (int j = lane; j < n; j += 32) dd_fma(row[j], v[j], s, cc);
+    s = warp_sum_dd(s, cc);
     if (lane == 0) {
       if (i < m) W[op.c + i] = s;
       else W[op.d + i - m] = s;

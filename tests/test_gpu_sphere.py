@@ -64,13 +64,10 @@ def test_c5_reduced_matches_reference(N, schedule):
     rel = np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"])
     print(f"c5 N={N} {schedule}: iterations {tr.iterations} (reference {int(g['iterations'])}), "
           f"|x - x_ref|/|x_ref| = {rel:.2e}, h2 residual {r:.2e} (reference x: {r_ref:.2e})")
-    # Known gap: the replay solve applies explicit pivot-block
-    # inverses, so its forward error is ~cond(P) eps instead of a backward-stable
-    # LU solve's, and the TRUE residual of the preconditioned iteration
-    # stagnates near 1e-8 at N = 16,384 (the recurrence residual reaches 1e-10
-    # in the reference's iteration count; the reference's x has a true
-    # residual of 1.3e-10).  Gated at 5e-8 so a regression still shows.
-    assert r <= max(5e-8, 3.0 * r_ref), (r, r_ref)
+    # the replay's compensated row sums keep the preconditioner linear to
+    # rounding, so the true residual follows the recurrence residual as in the
+    # reference (plain FMA sums left it at 1e-8 at N = 16,384)
+    assert r <= 3.0 * max(r_ref, 1e-10), (r, r_ref)
     assert rel <= 1e-6, rel
 
 
