@@ -339,28 +339,31 @@ def run_ours(args, rank, world):
     # outside the timed region: reported beside the headline, never as it ----
     relaxed = None
     if args.relaxed and sched != "colored":
-        if consume and state["ops"] is None:
-            state["ops"] = make_ops()
-        graph = P.assemble_extended_graph(state["ops"], consume=consume)
-        if consume:
-            state["ops"] = None
-        NN.lib().ifmm_dev_sync(NN.ctx())
-        NN.event(0)
-        s0c = P.estimate_sigma0(graph, seed=0)
-        fc = P.factorize(graph, inp["eps"], seed=0, sigma0=s0c, schedule="colored")
-        NN.event(1)
-        xc = fc.solve(b_dev)
-        NN.event(2)
-        tcf, tcs = NN.elapsed_ms(0, 1) * 1e-3, NN.elapsed_ms(1, 2) * 1e-3
-        relaxed = {"schedule": "colored", "t_factorize_s": tcf, "t_solve_s": tcs,
-                   "unknowns_per_s": N / (tcf + tcs),
-                   "levels_compressed": [s.compressed_pairs for s in fc.stats.levels],
-                   "note": "relaxed elimination order (SURVEY.md 8e): not comparable with the "
-                           "reference's statistics; validated by the residual criterion only"}
-        if gold is not None:
-            Kxc = P.exact_matvec(inp["pts"], K, xc.cpu().numpy())
-            relaxed["exact_residual"] = float(np.linalg.norm(Kxc - b_host) / np.linalg.norm(b_host))
-        del fc, xc
+        try:
+            if consume and state["ops"] is None:
+                state["ops"] = make_ops()
+            graph = P.assemble_extended_graph(state["ops"], consume=consume)
+            if consume:
+                state["ops"] = None
+            NN.lib().ifmm_dev_sync(NN.ctx())
+            NN.event(0)
+            s0c = P.estimate_sigma0(graph, seed=0)
+            fc = P.factorize(graph, inp["eps"], seed=0, sigma0=s0c, schedule="colored")
+            NN.event(1)
+            xc = fc.solve(b_dev)
+            NN.event(2)
+            tcf, tcs = NN.elapsed_ms(0, 1) * 1e-3, NN.elapsed_ms(1, 2) * 1e-3
+            relaxed = {"schedule": "colored", "t_factorize_s": tcf, "t_solve_s": tcs,
+                       "unknowns_per_s": N / (tcf + tcs),
+                       "levels_compressed": [s.compressed_pairs for s in fc.stats.levels],
+                       "note": "relaxed elimination order (SURVEY.md 8e): not comparable with the "
+                               "reference's statistics; validated by the residual criterion only"}
+            if gold is not None:
+                Kxc = P.exact_matvec(inp["pts"], K, xc.cpu().numpy())
+                relaxed["exact_residual"] = float(np.linalg.norm(Kxc - b_host) / np.linalg.norm(b_host))
+            del fc, xc
+        except Exception as e:  # the relaxed order is experimental
+            relaxed = {"schedule": "colored", "failed": f"{type(e).__name__}: {e}"[:200]}
     dom = max(kt.items(), key=lambda kv: kv[1][0])
     cat, (ksec, kwork, kcnt) = dom
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \

@@ -566,6 +566,9 @@ void Factor::build_program(const std::vector<int>& final_size) {
   }
   P.task_start.push_back((int)tasks.size());
   P.n_fwd_launch = n_fwd_launch;
+  if (getenv("IFMM_MEMTRACE"))
+    fprintf(stderr, "[ifmm] solve program: %d eliminations, forward %d waves, backward %d waves, %zu row tasks, top n %d\n",
+            P.n_fwd, P.fwd_waves, P.bwd_waves, tasks.size(), P.top_n);
   P.bytes += 8.0 * (double)P.top_n * P.top_n;  // both triangles of the top LU, once
   const size_t ob = all.size() * sizeof(SolveOp), lb = lists.size() * sizeof(ListEnt);
   const size_t tb = tasks.size() * sizeof(SolveTask);

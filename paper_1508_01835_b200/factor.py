@@ -263,6 +263,11 @@ def factorize(graph: ExtendedGraph, epsilon: float, seed: int = 0,
         order, so per-level fill statistics and x are not comparable with the
         reference's; this mode is validated by the residual criterion only
         (exact-matvec residual <= 2x the reference's, tests/test_gpu_large.py).
+        Experimental: it is NOT robust on the hardest recipes -- at depth-5
+        trees with a large absolute threshold (c4; the c5 recipe at
+        N = 262,144) the relaxed order meets near-singular pivot blocks
+        (SingularPivotError, or a preconditioner GMRES cannot use), where
+        the reference order does not.
     The fill pairs of one elimination always run as waves of cluster-disjoint
     pairs (they commute); ``exact_order=True`` runs them one at a time
     (diagnostics).  Environment defaults: IFMM_SCHEDULE, IFMM_EXACT_ORDER."""
