@@ -57,6 +57,11 @@ void ifmm_h2_destroy(void* h2);
 int ifmm_h2_ranks(void* h2, int* ranks_out /* n_clusters, -1 if none */);
 /* initialize_weights, rigorous mode (h2.py:185-231). */
 int ifmm_h2_weights(void* h2);
+/* initialize_weights(mode="sampled") (h2.py:197-225, _sampled_gram h2.py:250-262):
+ * sample_ptr (n_clusters + 1 offsets) / sample_idx hold, per cluster, the
+ * sorted row sample of its basis the caller drew (the reference's
+ * rng.choice stream); clusters with an empty interaction list have none.   */
+int ifmm_h2_weights_sampled(void* h2, const long long* sample_ptr, const int* sample_idx);
 /* Host copy of one stored block for inspection (tests / views):
  * which: 0 leaf_u[i], 1 leaf_v[i], 2 transfer_u[i], 3 transfer_vt[i],
  *        4 coupling[(i,j)], 5 near[(i,j)], 6 sigma_u[i], 7 sigma_v[i].

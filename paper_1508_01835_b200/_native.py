@@ -35,6 +35,7 @@ _SIGS = {
     "ifmm_tree_topology_sizes": (C.c_int, [vp, lp, lp]),
     "ifmm_tree_topology": (C.c_int, [vp, lp, ip, lp, ip]),
     "ifmm_h2_build": (vp, [vp, C.c_int, C.c_double, C.c_int, C.c_double]),
+    "ifmm_h2_weights_sampled": (C.c_int, [vp, vp, vp]),
     "ifmm_h2_build_k": (vp, [vp, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double]),
     "ifmm_kernel_matrix_k": (C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_int, vp, C.c_int, vp,
                                        vp, C.c_int]),

@@ -219,6 +219,15 @@ int ifmm_h2_weights(void* p) {
   ABI_CATCH
 }
 
+int ifmm_h2_weights_sampled(void* p, const long long* sample_ptr, const int* sample_idx) {
+  ABI_TRY
+  if (((H2*)p)->consumed) throw Error(E_VALUE, "operators were consumed by a graph");
+  if (!sample_ptr || !sample_idx) throw Error(E_VALUE, "sample lists missing");
+  ((H2*)p)->weights(sample_ptr, sample_idx);
+  return 0;
+  ABI_CATCH
+}
+
 int ifmm_h2_block(void* p, int which, int i, int j, double* out, int* rows, int* cols) {
   ABI_TRY
   H2* h = (H2*)p;

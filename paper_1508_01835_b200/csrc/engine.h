@@ -55,7 +55,9 @@ struct H2 {
   std::vector<Blk> su, sv;               // 1 x k
   ~H2();
   void build();
-  void weights();
+  // sptr / sidx (optional, CSR by cluster id): the sampled mode's row samples
+  // of each cluster's basis (h2.py:250-262), drawn by the caller
+  void weights(const long long* sptr = nullptr, const int* sidx = nullptr);
   void matvec(const double* d_x_sorted, double* d_y_sorted);
   // h2_matvec's block lists are built once per operator state and kept on
   // the device (h2.cu); weights() / graph consumption drop them

@@ -847,13 +847,17 @@ void Eliminator::rebase_edges(std::vector<RebaseReq>& reqs) {
     const int kn = bu.rank, ko = bu.k_old;
     IFMM_ASSERT(!g.get(nyn, nyn), "live cluster with a y-y self edge");
     if (!(bu.identity && kn == ko)) {
-      std::vector<int> rs(g.rows[nyn].begin(), g.rows[nyn].end());
-      for (int b : rs) {
+      // the edge set of y is unchanged by a block replacement: iterate it in
+      // place, one map lookup per edge (the old block is freed at the next
+      // flush, after the GEMM that reads it)
+      for (int b : g.rows[nyn]) {
         if (b == nzn || b == py) continue;
-        const Blk E = *g.get(nyn, b);
+        Blk* e = g.get(nyn, b);
+        const Blk E = *e;
         Blk nb = C.alloc(kn, E.c);
         rowg.add(bu.OM.p, ko, 0, E.p, E.c, 0, nb.p, E.c, kn, E.c, ko, 1.0, 0.0);
-        g.set(nyn, b, nb);
+        *e = nb;
+        C.free_raw(E.p, E.cls);
       }
     }
   }
@@ -866,13 +870,14 @@ void Eliminator::rebase_edges(std::vector<RebaseReq>& reqs) {
     const int py = g.ny[q.partner];
     const int kn = bu.rank, ko = bu.k_old;
     if (!(bv.identity && kn == ko)) {
-      std::vector<int> cs(g.cols[nyn].begin(), g.cols[nyn].end());
-      for (int a : cs) {
+      for (int a : g.cols[nyn]) {
         if (a == nzn || a == py) continue;
-        const Blk E = *g.get(a, nyn);
+        Blk* e = g.get(a, nyn);
+        const Blk E = *e;
         Blk nb = C.alloc(E.r, kn);
         colg.add(E.p, E.c, 0, bv.OM.p, ko, 1, nb.p, kn, E.r, kn, ko, 1.0, 0.0);
-        g.set(a, nyn, nb);
+        *e = nb;
+        C.free_raw(E.p, E.cls);
       }
     }
   }

@@ -168,59 +168,62 @@ double Graph::sigma0(const double* omega, int width, int power_iters) {
   Blk work = C.alloc(1, (int)(2 * dim * w + 4 * w * w + 64));
   Blk out = C.alloc(1, 1);
   CUDA_CHECK(cudaMemcpyAsync(Om.p, omega, sizeof(double) * dim * w, cudaMemcpyHostToDevice, C.st));
-  // row tasks for E and E^T (terms in sorted node order -> deterministic)
+  // Row tasks for E and E^T (terms in sorted node order -> deterministic),
+  // built and uploaded ONCE: E always maps Z -> Y (the sketch is copied into
+  // Z first), E^T always Q -> Z.
   std::vector<SpmvRow> rE, rT;
   std::vector<SpmvTerm> tE, tT;
-  auto build = [&](const double* in, double* outp) {
-    rE.clear(); tE.clear(); rT.clear(); tT.clear();
-    for (int t = 0; t < nn; ++t) {
-      SpmvRow r{outp + off[t] * w, size[t], (int)tE.size(), 0, 0};
-      for (int s : rows[t]) {
-        const Blk& B = E.at(key2(t, s));
-        tE.push_back({B.p, B.r, B.c, B.c, 0, in + off[s] * w});
-        r.nt++;
-      }
-      rE.push_back(r);
+  for (int t = 0; t < nn; ++t) {
+    SpmvRow r{Y.p + off[t] * w, size[t], (int)tE.size(), 0, 0};
+    for (int s : rows[t]) {
+      const Blk& B = E.at(key2(t, s));
+      tE.push_back({B.p, B.r, B.c, B.c, 0, Z.p + off[s] * w});
+      r.nt++;
     }
-  };
-  auto buildT = [&](const double* in, double* outp) {
-    rT.clear(); tT.clear();
-    for (int s = 0; s < nn; ++s) {
-      SpmvRow r{outp + off[s] * w, size[s], (int)tT.size(), 0, 0};
-      for (int t : cols[s]) {
-        const Blk& B = E.at(key2(t, s));
-        tT.push_back({B.p, B.r, B.c, B.c, 1, in + off[t] * w});
-        r.nt++;
-      }
-      rT.push_back(r);
+    rE.push_back(r);
+  }
+  for (int s = 0; s < nn; ++s) {
+    SpmvRow r{Z.p + off[s] * w, size[s], (int)tT.size(), 0, 0};
+    for (int t : cols[s]) {
+      const Blk& B = E.at(key2(t, s));
+      tT.push_back({B.p, B.r, B.c, B.c, 1, Q.p + off[t] * w});
+      r.nt++;
     }
+    rT.push_back(r);
+  }
+  static_assert(sizeof(SpmvRow) % 8 == 0 && sizeof(SpmvTerm) % 8 == 0, "descriptor alignment");
+  auto upload = [&](const void* src, size_t bytes) {
+    Blk d = C.alloc(1, (int)(bytes / 8 + 1));
+    if (bytes) CUDA_CHECK(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, C.st));
+    return d;
   };
-  auto applyE = [&](const double* in, double* outp) {
-    build(in, outp);
-    SpmvTerm* dt = C.stage.push_vec(C, tE);
-    SpmvRow* dr = C.stage.push_vec(C, rE);
-    launch_spmv(dr, (int)rE.size(), dt, w, w, C.st);
+  Blk drE = upload(rE.data(), rE.size() * sizeof(SpmvRow));
+  Blk dtE = upload(tE.data(), tE.size() * sizeof(SpmvTerm));
+  Blk drT = upload(rT.data(), rT.size() * sizeof(SpmvRow));
+  Blk dtT = upload(tT.data(), tT.size() * sizeof(SpmvTerm));
+  auto applyE = [&]() {
+    launch_spmv(reinterpret_cast<const SpmvRow*>(drE.p), (int)rE.size(),
+                reinterpret_cast<const SpmvTerm*>(dtE.p), w, w, C.st);
   };
-  auto applyET = [&](const double* in, double* outp) {
-    buildT(in, outp);
-    SpmvTerm* dt = C.stage.push_vec(C, tT);
-    SpmvRow* dr = C.stage.push_vec(C, rT);
-    launch_spmv(dr, (int)rT.size(), dt, w, w, C.st);
+  auto applyET = [&]() {
+    launch_spmv(reinterpret_cast<const SpmvRow*>(drT.p), (int)rT.size(),
+                reinterpret_cast<const SpmvTerm*>(dtT.p), w, w, C.st);
   };
-  applyE(Om.p, Y.p);
+  CUDA_CHECK(cudaMemcpyAsync(Z.p, Om.p, sizeof(double) * dim * w, cudaMemcpyDeviceToDevice, C.st));
+  applyE();
   for (int it = 0; it < power_iters; ++it) {
     launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
-    applyET(Q.p, Z.p);
-    applyE(Z.p, Y.p);
+    applyET();
+    applyE();
   }
   launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
-  applyET(Q.p, Z.p);
+  applyET();
   launch_tall_sigmax(Z.p, (int)dim, w, out.p, work.p, C.st);
   CUDA_CHECK(cudaGetLastError());
   double s0 = 0.0;
   CUDA_CHECK(cudaMemcpyAsync(&s0, out.p, sizeof(double), cudaMemcpyDeviceToHost, C.st));
   C.sync();
-  for (Blk* b : {&Om, &Y, &Z, &Q, &work, &out}) C.free(*b);
+  for (Blk* b : {&Om, &Y, &Z, &Q, &work, &out, &drE, &dtE, &drT, &dtT}) C.free(*b);
   C.flush();
   return s0;
 }

@@ -288,7 +288,7 @@ void H2::build() {
 // right-rotations other clusters apply, so every cluster is computed in
 // parallel from the unrotated couplings and rotated once.
 // ---------------------------------------------------------------------------
-void H2::weights() {
+void H2::weights(const long long* sptr, const int* sidx) {
   Ctx& C = *ctx;
   Tree& T = *tree;
   drop_plan();
@@ -302,6 +302,7 @@ void H2::weights() {
   size_t pos = 0;
   while (pos < ids.size()) {
     std::vector<WeightDesc> wd;
+    std::vector<int> wj;  // cluster of each descriptor
     std::vector<Blk> Hs, Ws;
     CopyBatch cb;
     size_t used = 0;
@@ -329,16 +330,57 @@ void H2::weights() {
       WeightDesc d;
       d.H = H.p; d.k = k; d.W = W; d.P = P[j].p; d.w = su[j].p; d.work = w.p;
       wd.push_back(d);
+      wj.push_back(j);
       Hs.push_back(H);
       Ws.push_back(w);
-      used += (size_t)k * W + weights_work_doubles(k, W);
+      used += (size_t)k * W + weights_work_doubles(k, W) + (sptr ? (size_t)(64 + k) * W : 0);
     }
     cb.run(C);
+    std::vector<Blk> Ss;
+    if (sptr) {
+      // sampled mode (h2.py:250-262 _sampled_gram): H_j <- (m / s) Bs^T (Bs H_j)
+      // for the caller's sorted row sample Bs of the cluster's basis B (leaf:
+      // U_j; parent: the children's transfers stacked).  Left-multiplication
+      // only, so the parallel evaluation stays valid.
+      CopyBatch gs;
+      GemmBatch ga, gb;
+      for (size_t i = 0; i < wd.size(); ++i) {
+        const int j = wj[i];
+        const int k = rank[j], W = wd[i].W;
+        const int s = (int)(sptr[j + 1] - sptr[j]);
+        const int* idx = sidx + sptr[j];
+        int m = 0;
+        if (T.is_leaf(j)) m = leaf_u[j].r;
+        else for (int c : T.children[j]) m += tu[c].r;
+        IFMM_ASSERT(s >= 1 && s <= m, "sampled weights: bad sample size");
+        Blk Bs = C.alloc(s, k), Tm = C.alloc(s, W), H2b = C.alloc(k, W);
+        for (int r = 0; r < s; ++r) {
+          int row = idx[r];
+          IFMM_ASSERT(row >= 0 && row < m, "sampled weights: row index out of range");
+          const double* src = nullptr;
+          if (T.is_leaf(j)) src = leaf_u[j].p + (size_t)row * k;
+          else
+            for (int c : T.children[j]) {
+              if (row < tu[c].r) { src = tu[c].p + (size_t)row * k; break; }
+              row -= tu[c].r;
+            }
+          gs.add(src, k, 1, Bs.p + (size_t)r * k, k, 1, 1, k, 0);
+        }
+        ga.add(Bs.p, k, 0, wd[i].H, W, 0, Tm.p, W, s, W, k, 1.0, 0.0);
+        gb.add(Bs.p, k, 1, Tm.p, W, 0, H2b.p, W, k, W, s, (double)m / (double)s, 0.0);
+        wd[i].H = H2b.p;
+        Ss.push_back(Bs); Ss.push_back(Tm); Ss.push_back(H2b);
+      }
+      gs.run(C);
+      ga.run(C);
+      gb.run(C);
+    }
     if (!wd.empty()) launch_weights(C.stage.push_vec(C, wd), (int)wd.size(), C.st);
     CUDA_CHECK(cudaGetLastError());
     C.sync();
     for (auto& b : Hs) C.free(b);
     for (auto& b : Ws) C.free(b);
+    for (auto& b : Ss) C.free(b);
     C.flush();
   }
   {

@@ -62,7 +62,7 @@ class Arena {
   // exact-size cache in front of the best-fit backend: most edge blocks are
   // re-requested with the same shape, so reuse is an O(1) vector pop.  The
   // cache is drained back (with coalescing) only when the backend is full.
-  std::unordered_map<size_t, std::vector<size_t>> cache_;
+  std::map<size_t, std::vector<size_t>> cache_;  // ordered: a larger class can serve a miss
   size_t cached_ = 0;
   // large requests the fragmented slab cannot serve go to cudaMalloc
   std::unordered_map<void*, size_t> extern_;

@@ -143,7 +143,35 @@ def initialize_weights(ops: H2Operators, topology: ClusterTopology, mode: str = 
     if mode not in ("rigorous", "sampled"):
         raise ValueError("mode must be 'rigorous' or 'sampled'")
     if mode == "sampled":
-        raise ValueError("sampled weights are not implemented by the engine (rigorous only)")
+        # the row samples of every cluster's basis, drawn on the host in the
+        # reference's loop order from its Generator(PCG64(seed)) (h2.py:200,
+        # 250-262); the Gram products, SVDs and rotations run on the device
+        rng = np.random.Generator(np.random.PCG64(seed))
+        tree, bd = ops.tree, ops.block_dim
+        rank = ops.rank
+        ptr = np.zeros(tree.n_clusters + 1, dtype=np.int64)
+        chunks = []
+        order = [j for level in range(2, tree.depth + 1) for j in tree.levels[level]]
+        sizes = {}
+        for j in order:
+            if not topology.interactions[j]:
+                continue
+            cl = tree.clusters[j]
+            m = (cl.stop - cl.start) * bd if not cl.children else sum(rank[c] for c in cl.children)
+            s = min(int(sample_size), m)
+            if s < 1:
+                raise ValueError("sample_size must be >= 1")
+            idx = np.sort(rng.choice(m, size=s, replace=False)) if s < m else np.arange(m)
+            sizes[j] = np.asarray(idx, dtype=np.int32)
+        for j in range(tree.n_clusters):
+            ptr[j + 1] = ptr[j] + (len(sizes[j]) if j in sizes else 0)
+            if j in sizes:
+                chunks.append(sizes[j])
+        idx_all = np.ascontiguousarray(np.concatenate(chunks) if chunks else np.zeros(1, dtype=np.int32))
+        N.check(N.lib().ifmm_h2_weights_sampled(ops._h, ptr.ctypes.data_as(C.c_void_p),
+                                                idx_all.ctypes.data_as(C.c_void_p)))
+        ops._weighted = True
+        return ops
     N.check(N.lib().ifmm_h2_weights(ops._h))
     ops._weighted = True
     return ops

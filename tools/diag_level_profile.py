@@ -29,7 +29,11 @@ ops = P.chebyshev_operators(tree, topo, K, inp["nc"], epsilon=inp["eps"])
 P.initialize_weights(ops, topo)
 graph = P.assemble_extended_graph(ops, consume=inp["N"] >= 500000)
 print(f"setup {time.perf_counter() - t0:.1f}s", flush=True)
+t0 = time.perf_counter()
 s0 = P.estimate_sigma0(graph)
+print(f"sigma0 {s0:.6g} in {time.perf_counter() - t0:.2f}s", flush=True)
+if os.environ.get("IFMM_DIAG_SIGMA0_ONLY"):
+    sys.exit(0)
 NN.ktime(1)
 t0 = time.perf_counter()
 f = P.factorize(graph, inp["eps"], sigma0=s0)
