@@ -168,6 +168,14 @@ void launch_weights(const WeightDesc* d_descs, int n, cudaStream_t s);
 // (np.linalg.qr(Y)[0], lowrank.py:74-76); single CTA.  work >= 2*n*w+2*w.
 void launch_tall_orth(const double* Y, int n, int w, double* Q, double* work, cudaStream_t s);
 // Largest singular value of a tall row-major n x w matrix; single CTA.
+// the same on the whole grid (tall.cu: CholeskyQR2, w <= 12); *flag is raised
+// on a Cholesky breakdown
+bool tall_grid_supported(int w);
+size_t tall_grid_work_doubles(int w);
+void launch_tall_orth_grid(const double* Y, int n, int w, double* Q, double* work, int* flag,
+                           cudaStream_t s);
+void launch_tall_sigmax_grid(const double* Y, int n, int w, double* out, double* work,
+                             cudaStream_t s);
 void launch_tall_sigmax(const double* Y, int n, int w, double* out, double* work,
                         cudaStream_t s);
 

@@ -165,8 +165,8 @@ double Graph::sigma0(const double* omega, int width, int power_iters) {
   const int w = width;
   Blk Om = C.alloc((int)dim, w), Y = C.alloc((int)dim, w), Z = C.alloc((int)dim, w);
   Blk Q = C.alloc((int)dim, w);
-  Blk work = C.alloc(1, (int)(2 * dim * w + 4 * w * w + 64));
-  Blk out = C.alloc(1, 1);
+  Blk work = C.alloc(1, (int)(2 * dim * w + 4 * w * w + 64 + tall_grid_work_doubles(w)));
+  Blk out = C.alloc(1, 2);  // sigma0, then the breakdown flag
   CUDA_CHECK(cudaMemcpyAsync(Om.p, omega, sizeof(double) * dim * w, cudaMemcpyHostToDevice, C.st));
   // Row tasks for E and E^T (terms in sorted node order -> deterministic),
   // built and uploaded ONCE: E always maps Z -> Y (the sketch is copied into
@@ -209,20 +209,37 @@ double Graph::sigma0(const double* omega, int width, int power_iters) {
     launch_spmv(reinterpret_cast<const SpmvRow*>(drT.p), (int)rT.size(),
                 reinterpret_cast<const SpmvTerm*>(dtT.p), w, w, C.st);
   };
-  CUDA_CHECK(cudaMemcpyAsync(Z.p, Om.p, sizeof(double) * dim * w, cudaMemcpyDeviceToDevice, C.st));
-  applyE();
-  for (int it = 0; it < power_iters; ++it) {
-    launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
-    applyET();
-    applyE();
-  }
-  launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
-  applyET();
-  launch_tall_sigmax(Z.p, (int)dim, w, out.p, work.p, C.st);
-  CUDA_CHECK(cudaGetLastError());
+  // orth / sigma_max on the whole grid (tall.cu, CholeskyQR2) when w allows;
+  // a Cholesky breakdown (flag) repeats the estimate with the one-CTA
+  // Householder kernels
+  int* d_flag = reinterpret_cast<int*>(out.p + 1);
   double s0 = 0.0;
-  CUDA_CHECK(cudaMemcpyAsync(&s0, out.p, sizeof(double), cudaMemcpyDeviceToHost, C.st));
-  C.sync();
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool grid = attempt == 0 && tall_grid_supported(w);
+    if (attempt == 1 && tall_grid_supported(w) == false) break;
+    auto orth = [&]() {
+      if (grid) launch_tall_orth_grid(Y.p, (int)dim, w, Q.p, work.p, d_flag, C.st);
+      else launch_tall_orth(Y.p, (int)dim, w, Q.p, work.p, C.st);
+    };
+    CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int), C.st));
+    CUDA_CHECK(cudaMemcpyAsync(Z.p, Om.p, sizeof(double) * dim * w, cudaMemcpyDeviceToDevice, C.st));
+    applyE();
+    for (int it = 0; it < power_iters; ++it) {
+      orth();
+      applyET();
+      applyE();
+    }
+    orth();
+    applyET();
+    if (grid) launch_tall_sigmax_grid(Z.p, (int)dim, w, out.p, work.p, C.st);
+    else launch_tall_sigmax(Z.p, (int)dim, w, out.p, work.p, C.st);
+    CUDA_CHECK(cudaGetLastError());
+    int hflag = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&s0, out.p, sizeof(double), cudaMemcpyDeviceToHost, C.st));
+    CUDA_CHECK(cudaMemcpyAsync(&hflag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, C.st));
+    C.sync();
+    if (!grid || !hflag) break;
+  }
   for (Blk* b : {&Om, &Y, &Z, &Q, &work, &out, &drE, &dtE, &drT, &dtT}) C.free(*b);
   C.flush();
   return s0;
