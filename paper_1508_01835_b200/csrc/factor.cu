@@ -1327,7 +1327,10 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
   ph = new Phase(C, PH_ADD);
   // ---- classification (factor.py:301-318) ----
   struct Stash { int wi, ro, co, h, w; };
-  std::vector<std::map<std::pair<int, int>, Stash>> stash(ws.size());
+  // per eliminated cluster: (cluster pair) -> block of Fm, sorted by pair (a
+  // flat vector sorted once instead of a node-based map: ~700 entries per
+  // cluster, millions per level)
+  std::vector<std::vector<std::pair<std::pair<int, int>, Stash>>> stash(ws.size());
   {
     CopyBatch adds;
     for (size_t wi = 0; wi < ws.size(); ++wi) {
@@ -1355,12 +1358,24 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
             }
             st.added++;
           } else {
-            stash[wi][{ca, cbc}] = {(int)wi, A_off[ai], B_off[bi], A_h[ai], B_w[bi]};
+            stash[wi].push_back({{ca, cbc}, {(int)wi, A_off[ai], B_off[bi], A_h[ai], B_w[bi]}});
           }
         }
       }
     }
     adds.run(C);
+    for (auto& v : stash) {
+      std::stable_sort(v.begin(), v.end(),
+                       [](const auto& x, const auto& y) { return x.first < y.first; });
+      // a cluster pair occurs once per elimination (one live node per cluster);
+      // keep the map semantics (last write wins) all the same
+      size_t o = 0;
+      for (size_t i = 0; i < v.size(); ++i) {
+        if (i + 1 < v.size() && v[i + 1].first == v[i].first) continue;
+        v[o++] = v[i];
+      }
+      v.resize(o);
+    }
   }
   delete ph;
   // IFMM_DUMP=E,cj,ck,file: raw fills (ck, cj) and (cj, ck) of one pair when
@@ -1374,7 +1389,8 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
         if (ws[wi].c != E) continue;
         FILE* f = fopen(path, "wb");
         for (auto key : {std::make_pair(dk, dj), std::make_pair(dj, dk)}) {
-          auto it = stash[wi].find(key);
+          auto it = std::find_if(stash[wi].begin(), stash[wi].end(),
+                                 [&](const auto& kv) { return kv.first == key; });
           if (it == stash[wi].end()) { fprintf(f, "0 0\n"); continue; }
           const Stash& st = it->second;
           std::vector<double> hb((size_t)st.h * st.w);
@@ -1501,20 +1517,30 @@ void Eliminator::eliminate_wave(const std::vector<int>& cs, LevelStats& st) {
   // ---- pairs of every cluster (cluster-disjoint across the wave) ----
   std::vector<PairJob> jobs;
   for (size_t wi = 0; wi < ws.size(); ++wi) {
-    std::map<std::pair<int, int>, const FillFac*> fm;
-    for (size_t i = first[wi]; i < first[wi + 1]; ++i) fm[items[i].first] = &fac[i];
-    std::set<std::pair<int, int>> pairs;
-    for (auto& kv : fm)
-      pairs.insert({std::min(kv.first.first, kv.first.second),
-                    std::max(kv.first.first, kv.first.second)});
+    // items[first[wi] .. first[wi + 1]) are sorted by (ca, cb)
+    const size_t i0 = first[wi], i1 = first[wi + 1];
+    auto find = [&](int ca, int cb) -> const FillFac* {
+      const std::pair<int, int> key{ca, cb};
+      size_t lo = i0, hi = i1;
+      while (lo < hi) {
+        const size_t mid = (lo + hi) / 2;
+        if (items[mid].first < key) lo = mid + 1; else hi = mid;
+      }
+      return (lo < i1 && items[lo].first == key) ? &fac[lo] : nullptr;
+    };
+    std::vector<std::pair<int, int>> pairs;
+    pairs.reserve(i1 - i0);
+    for (size_t i = i0; i < i1; ++i)
+      pairs.push_back({std::min(items[i].first.first, items[i].first.second),
+                       std::max(items[i].first.first, items[i].first.second)});
+    std::sort(pairs.begin(), pairs.end());
+    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
     for (auto& pr : pairs) {
       PairJob pj;
       pj.cj = pr.first;
       pj.ck = pr.second;
-      auto a = fm.find({pr.second, pr.first});
-      auto b = fm.find({pr.first, pr.second});
-      pj.f_kj = a == fm.end() ? nullptr : a->second;
-      pj.f_jk = b == fm.end() ? nullptr : b->second;
+      pj.f_kj = find(pr.second, pr.first);
+      pj.f_jk = find(pr.first, pr.second);
       jobs.push_back(std::move(pj));
     }
   }
