@@ -335,6 +335,32 @@ def run_ours(args, rank, world):
         ks = kt["solve"]
         hbm_lines["solve"] = {"ms": 1e3 * ks[0] / ks[2], "algorithmic_GB": ks[1] / ks[2] / 1e9,
                               "GB_per_s": ks[1] / ks[0] / 1e9}
+    # ---- the grouped DMMA GEMM (csrc/gemm.cu) alone on a large problem: what
+    # the elimination's dense products reach when a launch is not latency-bound ----
+    gemm_peak = None
+    try:
+        import ctypes as C
+        ng = 4096
+        ga = torch.randn(ng, ng, dtype=torch.float64, device="cuda")
+        gb_ = torch.randn(ng, ng, dtype=torch.float64, device="cuda")
+        gc = torch.zeros(ng, ng, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        call = lambda: NN.check(NN.lib().ifmm_dev_gemm(  # noqa: E731
+            NN.ctx(), ng, ng, ng, C.c_void_p(ga.data_ptr()), ng, 0, C.c_void_p(gb_.data_ptr()), ng, 0,
+            C.c_void_p(gc.data_ptr()), ng, 1.0, 0.0))
+        call()
+        NN.lib().ifmm_dev_sync(NN.ctx())
+        NN.event(0)
+        for _ in range(3):
+            call()
+        NN.event(1)
+        tg = NN.elapsed_ms(0, 1) * 1e-3 / 3
+        gemm_peak = {"problem": "4096^3 fp64, one problem through ifmm_dev_gemm", "ms": 1e3 * tg,
+                     "TFLOP_per_s": 2.0 * ng ** 3 / tg / 1e12,
+                     "frac_of_dgemm_peak": 2.0 * ng ** 3 / tg / 1e12 / fp64_peak}
+        del ga, gb_, gc
+    except Exception as e:  # diagnostics only
+        gemm_peak = {"failed": str(e)[:120]}
     # ---- the relaxed (colour-wave) schedule on the same problem, one step,
     # outside the timed region: reported beside the headline, never as it ----
     relaxed = None
@@ -408,7 +434,8 @@ def run_ours(args, rank, world):
             "clocks": clk,
             "detail": {"t_factorize_s": statistics.mean(tf), "t_solve_dev_s": statistics.mean(ts),
                        "t_solve_host_s": statistics.mean(tsh), "t_setup_s": t_setup,
-                       "rel_residual_h2": res, "hbm_stages": hbm_lines, "relaxed_schedule": relaxed,
+                       "rel_residual_h2": res, "hbm_stages": hbm_lines, "gemm_kernel": gemm_peak,
+                       "relaxed_schedule": relaxed,
                        "hbm_peak_GB_per_s": hbm,
                        "fp64_dgemm_tflops": fp64_peak}}
     print(json.dumps(line), flush=True)
