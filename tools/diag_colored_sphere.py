@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_1508_01835_b200 as P
 from test_gpu_sphere import c5_problem
-for N in (4096, 16384, 65536):
+for N in [int(a) for a in sys.argv[1:]] or (4096, 16384, 65536):
     pts, K, b = c5_problem(P, N)
     tree, _ = P.build_octree(pts, 64)
     topo = P.compute_topology(tree)
