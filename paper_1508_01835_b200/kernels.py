@@ -51,13 +51,38 @@ class Kernel:
             raise ValueError(f"kernel '{self.name}': block_dim {self.block_dim} has no device "
                              "implementation")
         if kind == 2:
-            return kind, float(self.params["h"]), 0.0
-        if kind == 3:
-            return kind, float(self.params["d"]), 0.0
-        if kind == 5:
+            spec = (kind, float(self.params["h"]), 0.0)
+        elif kind == 3:
+            spec = (kind, float(self.params["d"]), 0.0)
+        elif kind == 5:
             a = float(self.params["radius"])
-            return kind, a, 1.0 / (6.0 * np.pi * float(self.params["viscosity"]) * a)
-        return kind, 0.0, 0.0
+            spec = (kind, a, 1.0 / (6.0 * np.pi * float(self.params["viscosity"]) * a))
+        else:
+            spec = (kind, 0.0, 0.0)
+        self._check_block_matches(kind)
+        return spec
+
+    def _check_block_matches(self, kind):
+        """The engine evaluates the kernel from ``name`` / ``params``; a plugin
+        whose ``block`` computes something else under a known name (e.g.
+        ``Kernel("exp", 1, {}, other_fn)``) must not be silently replaced by
+        the built-in formula.  A fixed 5 x 4 probe (incl. a coincident pair)
+        compares ``block`` with the built-in of the same name and parameters."""
+        if self.block is None or getattr(self, "_probed", False):
+            return
+        ref = {1: lambda: exp_kernel(), 2: lambda: imq_kernel(self.params["h"]),
+               3: lambda: benchmark_kernel(self.params["d"]), 4: lambda: zero_kernel(),
+               5: lambda: rpy_kernel(self.params["radius"], self.params["viscosity"])}[kind]()
+        g = np.random.Generator(np.random.PCG64(20150807))
+        Pp = g.uniform(-1.0, 1.0, size=(5, 3))
+        Qq = np.vstack([g.uniform(-1.0, 1.0, size=(3, 3)), Pp[:1]])
+        mine = np.asarray(self.block(Pp, Qq), dtype=float)
+        want = np.asarray(ref.block(Pp, Qq), dtype=float)
+        if mine.shape != want.shape or not np.allclose(mine, want, rtol=1e-12, atol=1e-14):
+            raise ValueError(f"kernel '{self.name}': block() differs from the engine's device "
+                             f"implementation of '{self.name}' with these params; a custom "
+                             "kernel function has no device implementation")
+        object.__setattr__(self, "_probed", True)
 
 
 def exp_kernel() -> Kernel:

@@ -128,6 +128,12 @@ def test_kernel_plugin_contract():
     assert (k, a) == (5, 0.25) and abs(c0 - 1.0 / (6.0 * np.pi * 2.0 * 0.25)) < 1e-16
     with pytest.raises(ValueError):
         P.Kernel("custom", 1, {}, lambda P_, Q: None).device_spec()
+    # a known name with a different function is refused, not silently replaced (kernels.py:22-39)
+    with pytest.raises(ValueError, match="differs"):
+        P.Kernel("exp", 1, {}, lambda A_, B_: np.ones((len(A_), len(B_)))).device_spec()
+    from scipy.spatial.distance import cdist
+    ref_style = P.Kernel("imq", 1, {"h": 0.2}, lambda A_, B_: 1.0 / np.sqrt(cdist(A_, B_) ** 2 + 0.04))
+    assert ref_style.device_spec() == (2, 0.2, 0.0)
 
 
 @pytest.mark.parametrize("seed", [0, 1, 123456789])
