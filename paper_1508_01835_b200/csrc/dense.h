@@ -78,10 +78,10 @@ size_t svd_smem_doubles(int max_smem_dim);
 
 // Host launchers.  `descs` / side arrays must already be device-resident.
 // (gemm.cu) d_tile_start: prefix sums of the problems' output-tile counts for
-// the tile shape gemm_tile_dims(big) reports (128 x 128 or 64 x 64).
-void gemm_tile_dims(int big, int* bm, int* bn);
+// the tile shape gemm_tile_dims reports (64 x 64).
+void gemm_tile_dims(int* bm, int* bn);
 void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob,
-                 int total_tiles, cudaStream_t s, int big);
+                 int total_tiles, cudaStream_t s);
 void launch_copy(const CopyDesc* d_descs, int n, cudaStream_t s);
 // rel_mode: thr is relative to sigma_max and rank >= 1 (h2.py:124-127).
 void launch_svd(const SvdDesc* d_descs, int n, double thr, int max_smem_dim,

@@ -11,8 +11,9 @@
 // contiguous index, [k][row] (ld rows + 4) otherwise -- so the copies are
 // coalesced and both layouts give conflict-free DMMA fragment reads (a
 // half-warp's 16 (row, k) addresses fall in 16 different 8-byte banks).
-// Two tile shapes: 128 x 128 (8 warps of 32 x 64) for the large problems
-// and 64 x 64 (4 warps of 32 x 32) for the rest.
+// One tile shape, 64 x 64 (4 warps of 32 x 32, 3 CTAs per SM): a 128 x 128
+// variant (8 warps of 32 x 64, 1 CTA per SM) measured no faster at any size
+// and much slower on mid-size problems (wave quantisation), so it was removed.
 #include "common.cuh"
 #include "dense.h"
 #include "runtime.h"
@@ -163,34 +164,25 @@ constexpr size_t gemm_smem_bytes() { return (size_t)G_STAGES * (BM + BN) * G_LDK
 
 }  // namespace
 
-void gemm_tile_dims(int big, int* bm, int* bn) {
-  *bm = big ? 128 : 64;
-  *bn = big ? 128 : 64;
+void gemm_tile_dims(int* bm, int* bn) {
+  *bm = 64;
+  *bn = 64;
 }
 
 void launch_gemm(const GemmDesc* d_descs, const int* d_tile_start, int nprob, int total_tiles,
-                 cudaStream_t s, int big) {
+                 cudaStream_t s) {
   DbgSync dbg_sync_{s, "launch_gemm"};
   if (total_tiles <= 0) return;
   static bool init = false;
   if (!init) {
-    CUDA_CHECK(cudaFuncSetAttribute(gemm_grouped_kernel<128, 128, 4, 2, 1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)gemm_smem_bytes<128, 128>()));
     CUDA_CHECK(cudaFuncSetAttribute(gemm_grouped_kernel<64, 64, 2, 2, 3>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)gemm_smem_bytes<64, 64>()));
     init = true;
   }
-  if (big) {
-    const int grid = total_tiles < 148 ? total_tiles : 148;  // 120 KB of shared memory: 1 CTA / SM
-    gemm_grouped_kernel<128, 128, 4, 2, 1><<<grid, 256, gemm_smem_bytes<128, 128>(), s>>>(
-        d_descs, d_tile_start, nprob, total_tiles);
-  } else {
-    const int grid = total_tiles < 148 * 3 ? total_tiles : 148 * 3;  // 60 KB: 3 CTAs / SM
-    gemm_grouped_kernel<64, 64, 2, 2, 3><<<grid, 128, gemm_smem_bytes<64, 64>(), s>>>(
-        d_descs, d_tile_start, nprob, total_tiles);
-  }
+  const int grid = total_tiles < 148 * 3 ? total_tiles : 148 * 3;  // 60 KB: 3 CTAs / SM
+  gemm_grouped_kernel<64, 64, 2, 2, 3><<<grid, 128, gemm_smem_bytes<64, 64>(), s>>>(
+      d_descs, d_tile_start, nprob, total_tiles);
 }
 
 }  // namespace ifmm

@@ -269,45 +269,34 @@ static constexpr size_t kMaxBatch = (size_t)1 << 19;  // descriptors per launch
 
 void GemmBatch::run(Ctx& ctx) {
   if (d.empty()) return;
-  // Large problems (both output dimensions >= 96) take the 128 x 128 tiles
-  // when together they fill at least half of the SMs; the rest 64 x 64.
-  std::vector<GemmDesc> grp[2];
-  long long big_tiles = 0;
-  auto is_big = [](const GemmDesc& x) { return x.M >= 96 && x.N >= 96; };
-  for (auto& x : d)
-    if (is_big(x)) big_tiles += (long long)((x.M + 127) / 128) * ((x.N + 127) / 128);
-  if (big_tiles < 74) {
-    grp[0].swap(d);
-  } else {
-    for (auto& x : d) grp[is_big(x) ? 1 : 0].push_back(x);
-  }
-  for (int big = 1; big >= 0; --big) {
-    std::vector<GemmDesc>& all = grp[big];
-    int bm = 64, bn = 64;
-    gemm_tile_dims(big, &bm, &bn);
-    for (size_t c0 = 0; c0 < all.size(); c0 += kMaxBatch) {
-      const size_t c1 = std::min(all.size(), c0 + kMaxBatch);
-      const GemmDesc* part = all.data() + c0;
-      const size_t np = c1 - c0;
-      std::vector<int> ts(np + 1);
-      long long tot = 0;
-      double fl = 0;
-      for (size_t i = 0; i < np; ++i) {
-        ts[i] = (int)tot;
-        tot += (long long)((part[i].M + bm - 1) / bm) * ((part[i].N + bn - 1) / bn);
-        fl += 2.0 * part[i].M * part[i].N * (double)part[i].K;
-      }
-      IFMM_ASSERT(tot < (1LL << 31), "GEMM batch tile count overflow");
-      ts[np] = (int)tot;
-      GemmDesc* dd = reinterpret_cast<GemmDesc*>(ctx.stage.push(ctx, part, np * sizeof(GemmDesc)));
-      int* dt = ctx.stage.push_vec(ctx, ts);
-      cudaEvent_t ka = nullptr;
-      ctx.kt_begin(K_GEMM, fl, &ka);
-      launch_gemm(dd, dt, (int)np, (int)tot, ctx.st, big);
-      ctx.kt_end(K_GEMM, fl, ka);
-      ctx.launches++;
-      CUDA_CHECK(cudaGetLastError());
+  // One tile shape for every problem: the 64 x 64 cp.async kernel at 3 CTAs per
+  // SM measured equal to or faster than a 128 x 128 variant at every size
+  // (27.7 vs 27.4 TF/s at 4096^3, 16.7 vs 9.4 at 280 x 7000 x 280;
+  // profiles/r02_gemm_ncu.md), so the large-tile path was removed.
+  int bm = 64, bn = 64;
+  gemm_tile_dims(&bm, &bn);
+  for (size_t c0 = 0; c0 < d.size(); c0 += kMaxBatch) {
+    const size_t c1 = std::min(d.size(), c0 + kMaxBatch);
+    const GemmDesc* part = d.data() + c0;
+    const size_t np = c1 - c0;
+    std::vector<int> ts(np + 1);
+    long long tot = 0;
+    double fl = 0;
+    for (size_t i = 0; i < np; ++i) {
+      ts[i] = (int)tot;
+      tot += (long long)((part[i].M + bm - 1) / bm) * ((part[i].N + bn - 1) / bn);
+      fl += 2.0 * part[i].M * part[i].N * (double)part[i].K;
     }
+    IFMM_ASSERT(tot < (1LL << 31), "GEMM batch tile count overflow");
+    ts[np] = (int)tot;
+    GemmDesc* dd = reinterpret_cast<GemmDesc*>(ctx.stage.push(ctx, part, np * sizeof(GemmDesc)));
+    int* dt = ctx.stage.push_vec(ctx, ts);
+    cudaEvent_t ka = nullptr;
+    ctx.kt_begin(K_GEMM, fl, &ka);
+    launch_gemm(dd, dt, (int)np, (int)tot, ctx.st);
+    ctx.kt_end(K_GEMM, fl, ka);
+    ctx.launches++;
+    CUDA_CHECK(cudaGetLastError());
   }
   d.clear();
 }
